@@ -1,0 +1,413 @@
+#!/usr/bin/env python3
+"""bench.py -- connection evaluations per second of the ASNN activation sweep.
+
+Metric (BASELINE.json): edges/sec (connection evals/s) + HBM GB/s vs roofline
+at 1/2/4/8 B200 vs host CPU.  Headline workload: config 4, a large power-law
+ASNN (~10M nodes, ~500M edges) with a batch of 64 input vectors sharded over
+the GPUs.  One step = one full activation sweep (sensors,
+every dependency level, output gather) of the whole batch.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
+  python bench.py --impl reference ...      # the reference's CPU evaluator
+
+Multi-GPU: torchrun, one rank per GPU, each rank holds the full CSR and its
+64/N batch columns (no per-level traffic); outputs are all-gathered with NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (description, builder kwargs, batch)
+    "c1": ("small random ASNN (1k nodes, 10k connections), single input vector", 1),
+    "c2": ("pruned-MLP sparse network (100k nodes, ~5M edges, 90% sparsity), batch 1024", 1024),
+    "c3": ("deep narrow NEAT-style DAG (50k nodes, 2000 levels), batch 256", 256),
+    "c4": ("large random power-law ASNN (10M nodes, ~500M edges), batch 64", 64),
+    "c5": ("NEAT population: 10k networks x 200 nodes, 128 inputs each", 128),
+}
+
+
+def make_network(cfg: str, scale: float = 1.0):
+    import paper_2005_04347_b200 as A
+    if cfg == "c1":
+        return [A.generate(A.GenSpec(16, 4, 980, 10000, 10, -1.0, 1.0, 1))]
+    if cfg == "c2":
+        return [A.generate_mlp(200, 500, 0.1, 2)]
+    if cfg == "c3":
+        return [A.generate(A.GenSpec(16, 4, 49980, 500000, 2000, -1.0, 1.0, 3))]
+    if cfg == "c4":
+        n = int(10_000_000 * scale)
+        return [A.generate_powerlaw(n, 100, 1024, 1024, int(500_000_000 * scale), 2.1, 4)]
+    if cfg == "c5":
+        rng = A.SplitMix64(5)
+        count = int(10_000 * scale)
+        return [A.generate(A.GenSpec(8, 4, 188, 1000, 8, -1.0, 1.0, rng.next())) for _ in range(count)]
+    raise ValueError(cfg)
+
+
+def band_starts(cfg: str, net) -> np.ndarray:
+    """Level boundaries of the banded generators (configs 2 and 4): every
+    non-input node has a mandatory predecessor in the previous band and all
+    sources in earlier bands, so its level is its band and positions in
+    (level, id) order are the ids themselves (netgen.cpp)."""
+    N = len(net.nodes)
+    if cfg == "c2":
+        return np.arange(0, N + 1, 500, dtype=np.uint32)
+    n_in, n_out, bands = len(net.inputs), len(net.outputs), 100
+    hidden = N - n_in - n_out
+    base, rem = divmod(hidden, bands - 2)
+    sizes = [n_in] + [base + (1 if b < rem else 0) for b in range(bands - 2)] + [n_out]
+    return np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint32)
+
+
+def host_layout_banded(cfg: str, net) -> dict:
+    """Flattened layout of a banded generator network, straight from the
+    generator's target-major edge list (sources already ascending)."""
+    N = len(net.nodes)
+    counts = np.bincount(net.target, minlength=N).astype(np.uint64)
+    row_ptr = np.zeros(N + 1, np.uint64)
+    np.cumsum(counts, out=row_ptr[1:])
+    starts = band_starts(cfg, net)
+    return dict(total_layers=len(starts) - 1, layer_offsets=starts, node_ids=net.nodes,
+                row_ptr=row_ptr, in_nodes=net.source, in_weights=net.weight,
+                input_order=net.inputs, id_bound=N, dropped_connections=0)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic(cfg):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        return json.loads(p.read_text()).get(cfg)
+    return None
+
+
+def cpu_baseline(nets, X_all, cfg, budget_s=20.0):
+    """The reference's own CPU evaluator (oracle/_ref, the unmodified
+    reference compiled from its sources) on a bounded sample of the same
+    workload: as many input vectors as fit in ~budget_s, best of
+    eval_parallel (all threads) and an OpenMP loop of eval_sequential."""
+    from oracle.bind import Ref, Oracle, available_ref
+    import paper_2005_04347_b200 as A
+    kind = "reference" if available_ref() else "port"
+    if kind == "reference":
+        ref = Ref()
+        threads = ref.L.ref_max_threads()
+    else:
+        ref = None
+        threads = 1
+    results = []
+    total_edges = 0
+    t_used = 0.0
+    evals = 0
+    for gi, net in enumerate(nets):
+        if cfg in ("c2", "c4"):
+            lay = host_layout_banded(cfg, net)
+            rn = ref.layout_from_csr(lay) if ref else None
+        else:
+            rn = ref.network(net) if ref else None
+            if rn is not None:
+                assert rn.preprocess() == 0
+            lay = None
+        E = len(net.source)
+        X = X_all[gi]
+        if rn is None:
+            o = Oracle()
+            lay = lay or o.layout(net)
+            t0 = time.perf_counter()
+            n = 0
+            while n < X.shape[0] and time.perf_counter() - t0 < budget_s / len(nets):
+                o.eval_batch(lay, X[n:n + 1])
+                n += 1
+            dt = time.perf_counter() - t0
+            results.append(("port-seq", E * n, dt))
+            continue
+        # mode 1: eval_parallel over all host threads, vector by vector
+        n1, t1 = 0, 0.0
+        while n1 < X.shape[0] and t1 < budget_s / (2 * len(nets)):
+            t, _ = rn.eval_batch(X[n1:n1 + 1], mode=1, workers=threads)
+            t1 += t
+            n1 += 1
+        # mode 2: OpenMP loop of eval_sequential over vectors
+        n2 = min(X.shape[0], max(threads, 1))
+        t2, _ = rn.eval_batch(X[:n2], mode=2, workers=threads)
+        results.append(("par", E * n1, t1))
+        results.append(("omp-seq", E * n2, t2))
+        total_edges += E
+    best = {}
+    for mode, ev, dt in results:
+        m = best.setdefault(mode, [0, 0.0])
+        m[0] += ev
+        m[1] += dt
+    rates = {k: v[0] / v[1] for k, v in best.items() if v[1] > 0}
+    mode = max(rates, key=rates.get)
+    sample = ", ".join(f"{k}: {best[k][0] / max(1, sum(len(n.source) for n in nets)):.0f} vectors "
+                       f"in {best[k][1]:.1f}s" for k in best)
+    return {"value": rates[mode], "unit": "conn_evals/s", "cores": threads, "kind": kind,
+            "mode": mode, "sample": sample}
+
+
+def run_ours(args, cfg):
+    import torch
+    import paper_2005_04347_b200 as A
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    t_setup = time.perf_counter()
+    nets = make_network(cfg, args.scale)
+    B_total = CONFIGS[cfg][1]
+    rng = np.random.default_rng(12345)
+    if cfg == "c5":
+        # population: networks are sharded, each keeps its 128 vectors
+        shard = nets[rank::world] if world > 1 else nets
+        lo = 0
+        X = [rng.uniform(-2, 2, (B_total, len(n.inputs))).astype(np.float32) for n in nets]
+        Xs = [X[i] for i in range(rank, len(nets), world)]
+        B = B_total
+    else:
+        shard = nets
+        X_full = rng.uniform(-2, 2, (B_total, len(nets[0].inputs))).astype(np.float32)
+        per = (B_total + world - 1) // world
+        lo, hi = rank * per, min(B_total, (rank + 1) * per)
+        Xs = [X_full[lo:hi]]
+        X = [X_full]
+        B = hi - lo
+    t_gen = time.perf_counter() - t_setup
+
+    dev = A.Device.get(local)
+    stream = torch.cuda.current_stream()
+    dev.set_stream(stream.cuda_stream)
+    t0 = time.perf_counter()
+    if cfg == "c5":
+        dl = A.DeviceLayout.from_population(shard, device=local)
+    elif args.prep == "upload" and cfg in ("c2", "c4"):
+        d = host_layout_banded(cfg, shard[0])
+        dl = A.DeviceLayout.from_layout(A.LayeredLayout(
+            d["total_layers"], d["layer_offsets"], d["node_ids"], d["row_ptr"], d["in_nodes"],
+            d["in_weights"], d["input_order"], 0, d["id_bound"], shard[0].outputs), device=local)
+    else:
+        dl = A.DeviceLayout.from_network(shard[0], device=local)
+    dev.synchronize()
+    t_pre = time.perf_counter() - t0
+    pre_t = dev.timings()
+    info = dl.info()
+    plan = dl.plan(B)
+
+    x_dev = torch.from_numpy(np.concatenate([x.reshape(-1) for x in Xs])).cuda()
+    out_dev = torch.empty(info["n_outputs"] * B, dtype=torch.float32, device="cuda")
+
+    def step():
+        dl.activate_device(x_dev.data_ptr(), B, out_dev.data_ptr())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        # NCCL gather of every rank's outputs (the only collective)
+        gathered = [torch.empty_like(out_dev) for _ in range(world)]
+        dist.all_gather(gathered, out_dev)
+
+    # e2e: host (pinned) buffers through the C-ABI call, copies inside
+    x_pin = torch.from_numpy(np.concatenate([x.reshape(-1) for x in Xs])).pin_memory()
+    out_pin = torch.empty(info["n_outputs"] * B, dtype=torch.float32).pin_memory()
+    dl.activate_host_ptr(x_pin.data_ptr(), B, x_pin.numel(), out_pin.data_ptr())
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        dl.activate_host_ptr(x_pin.data_ptr(), B, x_pin.numel(), out_pin.data_ptr())
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    E = sum(len(n.source) for n in nets)
+    conn_evals_total = E * B_total if cfg != "c5" else E * B_total
+    value = conn_evals_total / (ms / 1e3)
+    peak, peak_src = measured_peak()
+    achieved = plan["alg_bytes"] / (ms / 1e3) / 1e9
+    cb = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = cpu_baseline(nets, X, cfg, budget_s=args.cpu_budget)
+    if rank == 0:
+        line = {
+            "metric": "connection evals/s (edges x vectors per second), full activation sweep",
+            "value": value, "unit": "conn_evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if cfg != "c5" else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generator, DESIGN.md corpora)",
+            "config": {"workload": CONFIGS[cfg][0], "config": cfg, "edges": E,
+                       "nodes": int(sum(len(n.nodes) for n in nets)),
+                       "levels": info["total_layers"], "batch": B_total,
+                       "batch_per_gpu": B, "parallelism": f"batch-sharded dp{world}",
+                       "l2": "working set > 126 MB L2 (no flush)" if cfg in ("c2", "c4") else
+                             "L2-resident working set; per-step state rewritten"},
+            "e2e": {"value": conn_evals_total / e2e_s, "unit": "conn_evals/s",
+                    "h2d_bytes_per_step": int(x_pin.numel() * 4 * world),
+                    "d2h_bytes_per_step": int(out_pin.numel() * 4 * world)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": profiled_traffic(cfg),
+                         "peak_source": peak_src,
+                         "alg_bytes_per_step": plan["alg_bytes"]},
+            "cpu_baseline": cb,
+            "gpu_launches": plan["kernels"] * args.steps,
+            "clocks": clk.summary(),
+            "preprocess": {"wall_s": t_pre, "device_ms": pre_t, "generate_s": t_gen},
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    nets = make_network(cfg, args.scale)
+    rng = np.random.default_rng(12345)
+    B_total = CONFIGS[cfg][1]
+    if cfg == "c5":
+        X = [rng.uniform(-2, 2, (B_total, len(n.inputs))).astype(np.float32) for n in nets]
+    else:
+        X = [rng.uniform(-2, 2, (B_total, len(nets[0].inputs))).astype(np.float32)]
+    vals = []
+    for _ in range(args.warmup + args.steps):
+        vals.append(cpu_baseline(nets, X, cfg, budget_s=max(2.0, args.cpu_budget / 4)))
+    cb = vals[-1]
+    timed = vals[args.warmup:]
+    value = statistics.mean(v["value"] for v in timed)
+    E = sum(len(n.source) for n in nets)
+    line = {
+        "impl": "reference",
+        "metric": "connection evals/s (edges x vectors per second), full activation sweep",
+        "value": value, "unit": "conn_evals/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "ms_per_step": E * B_total / value * 1e3, "dtype": "f32",
+        "data": "synthetic (seeded generator, DESIGN.md corpora)",
+        "config": {"workload": CONFIGS[cfg][0], "config": cfg, "edges": E, "batch": B_total},
+        "cpu_baseline": {**cb, "value": value},
+        "e2e": {"value": value, "unit": "conn_evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "vs_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink c4/c5 for quick runs")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prep", default="device", choices=["device", "upload"],
+                    help="device: compute_required/segment/flatten on the GPU; upload: "
+                         "asnn_dev_upload_layout of the generator's banded layout")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args, args.config)
+    else:
+        run_ours(args, args.config)
+
+
+if __name__ == "__main__":
+    main()

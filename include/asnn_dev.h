@@ -1,0 +1,214 @@
+/*
+ * asnn_dev.h -- C-ABI of the B200-native ASNN activation engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (arxiv/paper_2005_04347, /root/reference/proj):
+ *
+ *   compute_required (network.cpp:222-255)      -> asnn_dev_compute_required
+ *   segment          (segmentation.cpp:20-101)  -> asnn_dev_segment
+ *   flatten          (layout.cpp:12-83)         -> asnn_dev_build_layout (+ _download)
+ *   eval_parallel, Backend::DeviceCompute
+ *                    (eval.hpp:20,37-39; the seam at eval.cpp:51-52)
+ *                                               -> asnn_dev_upload_layout + asnn_dev_activate
+ *   read_outputs     (eval.cpp:82-87)           -> `out` argument of asnn_dev_activate
+ *   layer_slice_bounds / max_layer_width / depth
+ *                    (layout.cpp:85-91, eval.cpp:89-94, segmentation.cpp:103-105)
+ *                                               -> asnn_dev_layout_info / _layer_slice
+ *
+ * Conventions:
+ *  - plain pointers and sizes; every host pointer is caller-owned and only
+ *    read (const) or written during the call; nothing is retained;
+ *  - errors are status codes (asnn_status), each mapping 1:1 to a reference
+ *    exception type (errors.hpp:9-55); asnn_dev_last_error() holds the text;
+ *  - one asnn_dev owns one CUDA stream; calls on one handle are serialised by
+ *    an internal mutex; use one handle per thread for concurrency;
+ *  - every call returns only after its results are visible to the caller
+ *    (SPEC.md:329), except the *_device variants, which are stream-ordered.
+ * Node ids, layers and positions are uint32; edge counts are uint64.
+ */
+#ifndef ASNN_DEV_H
+#define ASNN_DEV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum asnn_status {
+    ASNN_OK = 0,
+    ASNN_E_UNAVAILABLE = 1,       /* BackendUnavailable (errors.hpp:33-35; eval.cpp:51-52) */
+    ASNN_E_ARITY = 2,             /* InputArityMismatch (errors.hpp:9-11; eval.cpp:26-28) */
+    ASNN_E_UNASSIGNED_OUTPUT = 3, /* UnassignedOutput = OutputUnreachable (errors.hpp:14-17;
+                                     layout.cpp:13-17) */
+    ASNN_E_LAYER_RANGE = 4,       /* LayerOutOfRange (errors.hpp:19-21; layout.cpp:87-89) */
+    ASNN_E_INVALID = 5,           /* invalid argument (null pointer, size overflow) */
+    ASNN_E_CUDA = 6,              /* CUDA runtime / launch failure */
+    ASNN_E_OOM = 7,               /* device or pinned allocation failed */
+    ASNN_E_INFEASIBLE = 8         /* InfeasibleSpec (errors.hpp:23-25; netgen.cpp:29-53) */
+} asnn_status;
+
+#define ASNN_UNASSIGNED 0xFFFFFFFFu
+
+typedef struct asnn_dev asnn_dev;               /* device + stream + last error      */
+typedef struct asnn_dev_layout asnn_dev_layout; /* device-resident level-sorted CSR  */
+
+/* Network (network.hpp:25-32) as plain arrays.  `nodes` sorted ascending and
+ * unique; inputs/outputs in declared order; connections as SoA. */
+typedef struct asnn_network_desc {
+    uint32_t n_nodes;
+    const uint32_t* nodes;
+    uint32_t n_inputs;
+    const uint32_t* inputs;
+    uint32_t n_outputs;
+    const uint32_t* outputs;
+    uint64_t n_connections;
+    const uint32_t* source;
+    const uint32_t* target;
+    const float* weight;
+} asnn_network_desc;
+
+/* LayeredLayout (layout.hpp:27-37) in CSR form: node k of the flat array
+ * (sorted by (layer, id)) has predecessors in_nodes[row_ptr[k]..row_ptr[k+1])
+ * -- ids, in the stored accumulation order -- with parallel in_weights.
+ * `outputs` (optional, may be 0/NULL) are the ids read_outputs() projects. */
+typedef struct asnn_layout_desc {
+    uint32_t total_layers;
+    const uint32_t* layer_offsets; /* [total_layers + 1] */
+    uint32_t node_count;
+    const uint32_t* node_ids;      /* [node_count] */
+    const uint64_t* row_ptr;       /* [node_count + 1] */
+    const uint32_t* in_nodes;      /* [row_ptr[node_count]] */
+    const float* in_weights;       /* [row_ptr[node_count]] */
+    uint32_t n_inputs;
+    const uint32_t* input_order;   /* [n_inputs] sensor ids, declared order */
+    uint32_t id_bound;
+    uint32_t n_outputs;
+    const uint32_t* outputs;       /* [n_outputs] */
+} asnn_layout_desc;
+
+/* Sizes of a device layout (all networks it holds, see build_population). */
+typedef struct asnn_layout_info {
+    uint32_t n_networks;
+    uint32_t total_layers;        /* max over networks */
+    uint32_t node_count;          /* assigned nodes, all networks */
+    uint64_t edge_count;          /* stored predecessor entries */
+    uint64_t dropped_connections; /* layout.cpp:56-58 */
+    uint32_t id_bound;            /* sum over networks */
+    uint32_t n_inputs;            /* sum over networks */
+    uint32_t n_outputs;           /* sum over networks */
+    uint32_t max_layer_width;     /* eval.cpp:89-94 */
+    uint32_t max_in_degree;
+} asnn_layout_info;
+
+/* Per-phase device times of the last build / activate call (CUDA events). */
+typedef struct asnn_timings {
+    float upload_ms;
+    float required_ms;
+    float segment_ms;
+    float flatten_ms;
+    float activate_ms;
+} asnn_timings;
+
+/* ---- device handle ------------------------------------------------------ */
+int asnn_dev_device_count(int* count);
+int asnn_dev_open(int device, asnn_dev** out);       /* ASNN_E_UNAVAILABLE: no GPU */
+void asnn_dev_close(asnn_dev* dev);
+const char* asnn_dev_last_error(const asnn_dev* dev); /* per handle; "" when none */
+const char* asnn_dev_version(void);
+/* Run on a caller stream (a cudaStream_t, e.g. torch's current stream);
+ * NULL restores the handle's own stream. */
+int asnn_dev_set_stream(asnn_dev* dev, void* cuda_stream);
+void* asnn_dev_get_stream(asnn_dev* dev);
+int asnn_dev_synchronize(asnn_dev* dev);
+int asnn_dev_last_timings(const asnn_dev* dev, asnn_timings* out);
+
+/* ---- preprocessing (GPU) ------------------------------------------------
+ * compute_required (network.cpp:222-255): required[n_nodes] <- 1 for members,
+ * indexed like net->nodes. */
+int asnn_dev_compute_required(asnn_dev* dev, const asnn_network_desc* net, uint8_t* required);
+
+/* segment (segmentation.cpp:20-101): level[n_nodes] <- layer of each node
+ * (ASNN_UNASSIGNED for the rest), *n_layers <- depth() (>= 1).  `required`
+ * may be NULL (then computed on the device). */
+int asnn_dev_segment(asnn_dev* dev, const asnn_network_desc* net, const uint8_t* required,
+                     uint32_t* level, uint32_t* n_layers);
+
+/* compute_required + segment + flatten on the device; the result stays
+ * resident.  ASNN_E_UNASSIGNED_OUTPUT when an output has no layer. */
+int asnn_dev_build_layout(asnn_dev* dev, const asnn_network_desc* net, asnn_dev_layout** out);
+
+/* A NEAT population: n_networks independent networks in one layout; their
+ * levels run side by side (one block-diagonal DAG). */
+int asnn_dev_build_population(asnn_dev* dev, uint32_t n_networks, const asnn_network_desc* nets,
+                              asnn_dev_layout** out);
+
+/* Upload a host-flattened layout (what eval_parallel receives, eval.cpp:49).
+ * Re-upload on every eval_parallel call: the reference mutates layouts in
+ * place between evaluations (asnn_main.cpp:264-278). */
+int asnn_dev_upload_layout(asnn_dev* dev, const asnn_layout_desc* layout, asnn_dev_layout** out);
+
+void asnn_dev_free_layout(asnn_dev_layout* layout);
+
+int asnn_dev_layout_info(const asnn_dev_layout* layout, asnn_layout_info* info);
+
+/* layer_slice_bounds (layout.cpp:85-91) of network 0. */
+int asnn_dev_layer_slice(const asnn_dev_layout* layout, uint32_t layer, uint32_t* start,
+                         uint32_t* count);
+
+/* Download network `net_index`'s flattened layout (flatten parity):
+ * arrays sized from asnn_dev_network_info. */
+int asnn_dev_network_info(const asnn_dev_layout* layout, uint32_t net_index,
+                          asnn_layout_info* info);
+int asnn_dev_layout_download(asnn_dev_layout* layout, uint32_t net_index, uint32_t* layer_offsets,
+                             uint32_t* node_ids, uint64_t* row_ptr, uint32_t* in_nodes,
+                             float* in_weights, uint32_t* input_order);
+
+/* ---- activation -----------------------------------------------------------
+ * eval_parallel(DeviceCompute) over a batch: x is [n_vec][n_inputs] per
+ * network (networks concatenated), `out` (optional) receives the declared
+ * outputs [n_vec][n_outputs] per network (read_outputs order), `state`
+ * (optional) the id-indexed op array [n_vec][id_bound] per network
+ * (ActivationState.outputs, eval.hpp:14-17; unassigned ids 0.0f).
+ * Host pointers; copies happen inside the call.  n_x must equal the total
+ * inputs per vector or ASNN_E_ARITY is returned (eval.cpp:26-28). */
+int asnn_dev_activate(asnn_dev_layout* layout, const float* x, uint32_t n_vec, uint64_t n_x,
+                      float* out, float* state);
+
+/* Same, with device pointers, stream-ordered on the handle's stream (no
+ * synchronisation).  x_dev [n_vec][n_inputs], out_dev [n_vec][n_outputs]. */
+int asnn_dev_activate_device(asnn_dev_layout* layout, const float* x_dev, uint32_t n_vec,
+                             float* out_dev);
+
+/* Number of kernels one activate of n_vec vectors launches, and the
+ * algorithmic bytes it moves. */
+int asnn_dev_activate_plan(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* kernels,
+                           uint64_t* alg_bytes, uint64_t* conn_evals);
+
+/* The device's sigmoid32 (network.hpp:54-59) over n host floats, for
+ * exhaustive parity checks of the epilogue. */
+int asnn_dev_sigmoid32(asnn_dev* dev, const float* x, float* y, uint64_t n);
+
+/* ---- synthetic corpora (host, deterministic) ------------------------------
+ * generate(GenSpec) byte-identical to the reference (netgen.cpp:71-157),
+ * the MLP-adjacent shape (config 2) and the banded power-law shape
+ * (config 4).  A corpus handle owns its arrays; read them with
+ * asnn_corpus_desc (pointers valid until asnn_corpus_free). */
+typedef struct asnn_corpus asnn_corpus;
+int asnn_gen_reference(uint32_t input_count, uint32_t output_count, uint32_t hidden_count,
+                       uint64_t connection_count, uint32_t target_depth, float weight_min,
+                       float weight_max, uint64_t seed, asnn_corpus** out);
+uint64_t asnn_gen_max_connections(uint32_t input_count, uint32_t output_count,
+                                  uint32_t hidden_count, uint32_t target_depth);
+int asnn_gen_mlp(uint32_t layers, uint32_t width, double p, uint64_t seed, asnn_corpus** out);
+int asnn_gen_powerlaw(uint32_t n_nodes, uint32_t bands, uint32_t n_inputs, uint32_t n_outputs,
+                      uint64_t target_edges, double alpha, uint64_t seed, asnn_corpus** out);
+int asnn_corpus_desc(const asnn_corpus* corpus, asnn_network_desc* desc);
+void asnn_corpus_free(asnn_corpus* corpus);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ASNN_DEV_H */

@@ -1,0 +1,731 @@
+// engine.cu -- device handle, layout assembly/upload, activation driver and
+// the C-ABI entry points of include/asnn_dev.h (except preprocessing, which
+// lives in preprocess.cu and corpora in netgen.cpp).
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "kernels.cuh"
+
+using namespace asnn_b200;
+
+namespace asnn_b200 {
+
+int fail(asnn_dev* dev, int status, const std::string& msg) {
+    if (dev) dev->err = msg;
+    return status;
+}
+
+int cuda_fail(asnn_dev* dev, cudaError_t e, const char* what) {
+    const int st = (e == cudaErrorMemoryAllocation) ? ASNN_E_OOM : ASNN_E_CUDA;
+    cudaGetLastError();  // clear sticky-free errors
+    return fail(dev, st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace asnn_b200
+
+#define CK(expr)                                              \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) return cuda_fail(dev, _e, #expr); \
+    } while (0)
+
+namespace {
+
+constexpr uint32_t kThreads = 256;
+
+inline uint32_t blocks_for(uint64_t n, uint32_t t = kThreads) {
+    return static_cast<uint32_t>((n + t - 1) / t);
+}
+
+// g such that prefix[g] <= v < prefix[g+1] (prefix has n+1 entries, n >= 1).
+__device__ __forceinline__ uint32_t find_seg(const uint32_t* __restrict__ prefix, uint32_t n,
+                                             uint32_t v) {
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(&prefix[mid]) <= v) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// meta layout on device: 6 arrays of (G+1) u32:
+//   0 pos_base, 1 idb_prefix, 2 in_prefix, 3 out_prefix, 4 edge_base, 5 sensor_prefix
+struct MetaPtrs {
+    const uint32_t* pos;
+    const uint32_t* idb;
+    const uint32_t* in;
+    const uint32_t* out;
+    const uint32_t* edge;
+    const uint32_t* sens;
+    uint32_t G;
+};
+
+__global__ void k_state_map(MetaPtrs m, const uint32_t* __restrict__ node_ids, uint32_t P,
+                            uint32_t* __restrict__ state_map, uint32_t* __restrict__ bad) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const uint32_t g = find_seg(m.pos, m.G, p);
+    const uint32_t idb = m.idb[g + 1] - m.idb[g];
+    const uint32_t id = node_ids[p];
+    if (id >= idb) {
+        atomicOr(bad, 1u);
+        return;
+    }
+    state_map[m.idb[g] + id] = p;
+}
+
+// edges[k] = {position of source id (or the zero row P), weight bits}.
+__global__ void k_edges(MetaPtrs m, const uint32_t* __restrict__ in_ids, const float* __restrict__ w,
+                        uint64_t E, const uint32_t* __restrict__ state_map, uint32_t zero_row,
+                        uint2* __restrict__ edges, uint32_t* __restrict__ bad) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= E) return;
+    const uint32_t g = find_seg(m.edge, m.G, static_cast<uint32_t>(k));
+    const uint32_t idb = m.idb[g + 1] - m.idb[g];
+    const uint32_t id = in_ids[k];
+    uint32_t pos = zero_row;
+    if (id >= idb) atomicOr(bad, 2u);
+    else {
+        const uint32_t q = state_map[m.idb[g] + id];
+        // A predecessor without a position reads its never-written 0.0f slot,
+        // exactly like the reference's zero-initialised op array.
+        pos = (q == kUnassigned) ? zero_row : q;
+    }
+    edges[k] = make_uint2(pos, __float_as_uint(w[k]));
+}
+
+// kofid[idb + id] = max(i + 1) over declared input index i of that id.
+__global__ void k_input_index(MetaPtrs m, const uint32_t* __restrict__ inputs, uint32_t n_in_total,
+                              uint32_t* __restrict__ kofid, uint32_t* __restrict__ bad) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_in_total) return;
+    const uint32_t g = find_seg(m.in, m.G, j);
+    const uint32_t idb = m.idb[g + 1] - m.idb[g];
+    const uint32_t id = inputs[j];
+    if (id >= idb) {
+        atomicOr(bad, 4u);
+        return;
+    }
+    atomicMax(&kofid[m.idb[g] + id], j - m.in[g] + 1);
+}
+
+__global__ void k_sinfo(MetaPtrs m, const uint32_t* __restrict__ node_ids,
+                        const uint32_t* __restrict__ kofid, uint32_t S, uint4* __restrict__ sinfo) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const uint32_t g = find_seg(m.sens, m.G, s);
+    const uint32_t p = m.pos[g] + (s - m.sens[g]);
+    const uint32_t k1 = kofid[m.idb[g] + node_ids[p]];
+    sinfo[s] = make_uint4(p, m.in[g], m.in[g + 1] - m.in[g], k1 ? k1 - 1 : kUnassigned);
+}
+
+__global__ void k_oinfo(MetaPtrs m, const uint32_t* __restrict__ outputs, uint32_t n_out_total,
+                        const uint32_t* __restrict__ state_map, uint4* __restrict__ oinfo) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_out_total) return;
+    const uint32_t g = find_seg(m.out, m.G, j);
+    const uint32_t idb = m.idb[g + 1] - m.idb[g];
+    const uint32_t id = outputs[j];
+    const uint32_t pos = id < idb ? state_map[m.idb[g] + id] : kUnassigned;
+    oinfo[j] = make_uint4(pos, m.out[g], m.out[g + 1] - m.out[g], j - m.out[g]);
+}
+
+__global__ void k_max_deg(const uint32_t* __restrict__ row_ptr, uint32_t P, uint32_t* __restrict__ out) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t d = 0;
+    if (p < P) d = row_ptr[p + 1] - row_ptr[p];
+    for (int o = 16; o; o >>= 1) d = max(d, __shfl_xor_sync(0xFFFFFFFFu, d, o));
+    if ((threadIdx.x & 31) == 0 && d) atomicMax(out, d);
+}
+
+__global__ void k_row64_to_32(const uint64_t* __restrict__ in, uint32_t n, uint32_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = static_cast<uint32_t>(in[i]);
+}
+
+// Padded batch width: powers of two up to 128 columns, multiples of 128
+// beyond, so an item (LANES threads x V columns) tiles a row exactly.
+uint32_t padded_batch(uint32_t n_vec) {
+    if (n_vec <= 1) return 1;
+    if (n_vec <= 128) {
+        uint32_t p = 1;
+        while (p < n_vec) p <<= 1;
+        return p;
+    }
+    return (n_vec + 127) / 128 * 128;
+}
+
+struct LevelLaunch {
+    void (*fn)(const uint32_t*, const uint2*, float*, uint32_t, const uint32_t*, uint32_t, uint32_t);
+    uint32_t lanes;
+    uint32_t tiles;
+};
+
+LevelLaunch level_launch_for(uint32_t ldA) {
+    switch (ldA) {
+        case 1: return {k_level<1, 1>, 1, 1};
+        case 2: return {k_level<2, 1>, 1, 1};
+        case 4: return {k_level<4, 1>, 1, 1};
+        case 8: return {k_level<4, 2>, 2, 1};
+        case 16: return {k_level<4, 4>, 4, 1};
+        case 32: return {k_level<4, 8>, 8, 1};
+        case 64: return {k_level<4, 16>, 16, 1};
+        default: return {k_level<4, 32>, 32, ldA / 128};
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+namespace asnn_b200 {
+
+int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& flat,
+                    asnn_dev_layout** result) {
+    const uint32_t G = static_cast<uint32_t>(nets.size());
+    if (G == 0) return fail(dev, ASNN_E_INVALID, "layout without networks");
+    auto* L = new asnn_dev_layout;
+    L->dev = dev;
+    std::vector<uint32_t> meta(6 * (G + 1), 0);
+    uint64_t E = 0;
+    for (uint32_t g = 0; g < G; ++g) {
+        NetMeta& n = nets[g];
+        n.pos_base = meta[0 * (G + 1) + g];
+        n.idb_prefix = meta[1 * (G + 1) + g];
+        n.in_prefix = meta[2 * (G + 1) + g];
+        n.out_prefix = meta[3 * (G + 1) + g];
+        n.edge_base = E;
+        meta[0 * (G + 1) + g + 1] = n.pos_base + n.n_pos;
+        meta[1 * (G + 1) + g + 1] = n.idb_prefix + n.id_bound;
+        meta[2 * (G + 1) + g + 1] = n.in_prefix + n.n_in;
+        meta[3 * (G + 1) + g + 1] = n.out_prefix + n.n_out;
+        meta[4 * (G + 1) + g] = static_cast<uint32_t>(E);
+        E += n.n_edges;
+        meta[4 * (G + 1) + g + 1] = static_cast<uint32_t>(E);
+        meta[5 * (G + 1) + g + 1] = meta[5 * (G + 1) + g] + n.n_sensors;
+        L->dropped += n.dropped;
+    }
+    if (E >= 0xFFFFFFFFull) {
+        delete L;
+        return fail(dev, ASNN_E_INVALID, "more than 2^32-1 stored edges");
+    }
+    L->total_pos = meta[0 * (G + 1) + G];
+    L->total_idb = meta[1 * (G + 1) + G];
+    L->total_in = meta[2 * (G + 1) + G];
+    L->total_out = meta[3 * (G + 1) + G];
+    L->total_sensors = meta[5 * (G + 1) + G];
+    L->total_edges = E;
+    cudaStream_t st = dev->stream;
+
+    auto cleanup_fail = [&](int rc) {
+        delete L;
+        return rc;
+    };
+    DevBuf<uint32_t> d_meta;
+    DevBuf<uint32_t> bad, kofid, maxdeg;
+    cudaError_t e;
+#define CKL(expr)                                                      \
+    do {                                                               \
+        e = (expr);                                                    \
+        if (e != cudaSuccess) return cleanup_fail(cuda_fail(dev, e, #expr)); \
+    } while (0)
+    CKL(d_meta.alloc(meta.size()));
+    CKL(cudaMemcpyAsync(d_meta.p, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, st));
+    MetaPtrs m{d_meta.p, d_meta.p + (G + 1), d_meta.p + 2 * (G + 1), d_meta.p + 3 * (G + 1),
+               d_meta.p + 4 * (G + 1), d_meta.p + 5 * (G + 1), G};
+    CKL(bad.alloc(2));
+    CKL(cudaMemsetAsync(bad.p, 0, 8, st));
+    CKL(L->state_map.alloc(L->total_idb));
+    CKL(cudaMemsetAsync(L->state_map.p, 0xFF, static_cast<size_t>(L->total_idb) * 4, st));
+    if (L->total_pos)
+        k_state_map<<<blocks_for(L->total_pos), kThreads, 0, st>>>(m, flat.node_ids.p, L->total_pos,
+                                                                   L->state_map.p, bad.p);
+    CKL(L->edges.alloc(E));
+    if (E)
+        k_edges<<<blocks_for(E), kThreads, 0, st>>>(m, flat.in_ids.p, flat.w.p, E, L->state_map.p,
+                                                   L->total_pos, L->edges.p, bad.p);
+    CKL(kofid.alloc(L->total_idb));
+    CKL(cudaMemsetAsync(kofid.p, 0, static_cast<size_t>(L->total_idb) * 4, st));
+    if (L->total_in)
+        k_input_index<<<blocks_for(L->total_in), kThreads, 0, st>>>(m, flat.inputs.p, L->total_in,
+                                                                    kofid.p, bad.p);
+    CKL(L->sinfo.alloc(L->total_sensors));
+    if (L->total_sensors)
+        k_sinfo<<<blocks_for(L->total_sensors), kThreads, 0, st>>>(m, flat.node_ids.p, kofid.p,
+                                                                   L->total_sensors, L->sinfo.p);
+    CKL(L->oinfo.alloc(L->total_out));
+    if (L->total_out)
+        k_oinfo<<<blocks_for(L->total_out), kThreads, 0, st>>>(m, flat.outputs.p, L->total_out,
+                                                               L->state_map.p, L->oinfo.p);
+    CKL(maxdeg.alloc(1));
+    CKL(cudaMemsetAsync(maxdeg.p, 0, 4, st));
+    if (L->total_pos)
+        k_max_deg<<<blocks_for(L->total_pos), kThreads, 0, st>>>(flat.row_ptr.p, L->total_pos,
+                                                                 maxdeg.p);
+    CKL(cudaGetLastError());
+
+    // Level-major schedule: global level l runs layer l of every network.
+    uint32_t n_levels = 0;
+    for (const auto& n : nets) n_levels = std::max(n_levels, n.n_layers);
+    L->n_levels = n_levels;
+    L->lvl_off.assign(n_levels + 1, 0);
+    std::vector<uint32_t> sched;
+    sched.reserve(L->total_pos - L->total_sensors);
+    for (uint32_t l = 1; l < n_levels; ++l) {
+        L->lvl_off[l] = static_cast<uint32_t>(sched.size());
+        for (const auto& n : nets) {
+            if (l >= n.n_layers) continue;
+            for (uint32_t p = n.layer_offsets[l]; p < n.layer_offsets[l + 1]; ++p)
+                sched.push_back(n.pos_base + p);
+        }
+    }
+    if (n_levels) L->lvl_off[n_levels] = static_cast<uint32_t>(sched.size());
+    for (const auto& n : nets)
+        for (uint32_t l = 0; l < n.n_layers; ++l)
+            L->max_width = std::max(L->max_width, n.layer_offsets[l + 1] - n.layer_offsets[l]);
+    CKL(L->sched.alloc(sched.size()));
+    if (!sched.empty())
+        CKL(cudaMemcpyAsync(L->sched.p, sched.data(), sched.size() * 4, cudaMemcpyHostToDevice, st));
+    CKL(L->idb_prefix.alloc(G + 1));
+    CKL(cudaMemcpyAsync(L->idb_prefix.p, d_meta.p + (G + 1), (G + 1) * 4, cudaMemcpyDeviceToDevice,
+                        st));
+    uint32_t h_bad[2] = {0, 0};
+    CKL(cudaMemcpyAsync(h_bad, bad.p, 8, cudaMemcpyDeviceToHost, st));
+    CKL(cudaMemcpyAsync(&L->max_deg, maxdeg.p, 4, cudaMemcpyDeviceToHost, st));
+    CKL(cudaStreamSynchronize(st));
+#undef CKL
+    if (h_bad[0]) {
+        delete L;
+        return fail(dev, ASNN_E_INVALID,
+                    "layout references an id >= id_bound (code " + std::to_string(h_bad[0]) + ")");
+    }
+    L->row_ptr = std::move(flat.row_ptr);
+    L->node_ids = std::move(flat.node_ids);
+    L->nets = std::move(nets);
+    *result = L;
+    return ASNN_OK;
+}
+
+}  // namespace asnn_b200
+
+// ---------------------------------------------------------------------------
+namespace {
+
+// One activation sweep, stream-ordered: sensors, every level, outputs, state.
+int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out, float* state,
+                 cudaStream_t st) {
+    asnn_dev* dev = L->dev;
+    const uint32_t ldA = padded_batch(n_vec);
+    if (L->total_sensors)
+        k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(
+            L->sinfo.p, L->total_sensors, x, n_vec, L->A.p, ldA);
+    const LevelLaunch ll = level_launch_for(ldA);
+    for (uint32_t l = 1; l < L->n_levels; ++l) {
+        const uint32_t n = L->lvl_off[l + 1] - L->lvl_off[l];
+        if (!n) continue;
+        const uint64_t items = static_cast<uint64_t>(n) * ll.tiles;
+        ll.fn<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(
+            L->row_ptr.p, L->edges.p, L->A.p, ldA, L->sched.p + L->lvl_off[l],
+            static_cast<uint32_t>(items), ll.tiles);
+    }
+    if (out && L->total_out)
+        k_gather_out<<<blocks_for(static_cast<uint64_t>(L->total_out) * n_vec), kThreads, 0, st>>>(
+            L->oinfo.p, L->total_out, L->A.p, ldA, n_vec, out);
+    if (state && L->total_idb)
+        k_state<<<blocks_for(static_cast<uint64_t>(L->total_idb) * n_vec), kThreads, 0, st>>>(
+            L->state_map.p, L->idb_prefix.p, static_cast<uint32_t>(L->nets.size()), L->total_idb,
+            L->A.p, ldA, n_vec, state);
+    CK(cudaGetLastError());
+    return ASNN_OK;
+}
+
+int ensure_workspace(asnn_dev_layout* L, uint32_t n_vec) {
+    asnn_dev* dev = L->dev;
+    const uint32_t ldA = padded_batch(n_vec);
+    // +1 row: the never-written zero row for predecessors without a position.
+    const size_t need = (static_cast<size_t>(L->total_pos) + 1) * ldA;
+    if (need > L->A.n) {
+        L->graph.reset();
+        CK(L->A.alloc(need));
+        CK(cudaMemsetAsync(L->A.p, 0, need * sizeof(float), L->dev->stream));
+    }
+    return ASNN_OK;
+}
+
+// Sweep through a cached CUDA graph (one launch per sweep instead of one per
+// level).  The graph is re-captured when buffers or the stream change.
+int run_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out, float* state) {
+    asnn_dev* dev = L->dev;
+    int rc = ensure_workspace(L, n_vec);
+    if (rc) return rc;
+    cudaStream_t st = dev->stream;
+    SweepGraph& g = L->graph;
+    if (!(g.exec && g.n_vec == n_vec && g.x == x && g.out == out && g.state == state &&
+          g.stream == st)) {
+        g.reset();
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        rc = launch_sweep(L, x, n_vec, out, state, st);
+        cudaError_t ce = cudaStreamEndCapture(st, &graph);
+        if (rc) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        CK(ce);
+        ce = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(ce);
+        g.n_vec = n_vec;
+        g.x = x;
+        g.out = out;
+        g.state = state;
+        g.stream = st;
+    }
+    CK(cudaGraphLaunch(g.exec, st));
+    return ASNN_OK;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* asnn_dev_version(void) { return "asnn-b200 0.1 (sm_100a)"; }
+
+int asnn_dev_sigmoid32(asnn_dev* dev, const float* x, float* y, uint64_t n) {
+    if (!dev || (n && (!x || !y))) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    if (!n) return ASNN_OK;
+    CK(cudaSetDevice(dev->device));
+    DevBuf<float> dx, dy;
+    CK(dx.alloc(n));
+    CK(dy.alloc(n));
+    cudaStream_t st = dev->stream;
+    CK(cudaMemcpyAsync(dx.p, x, n * 4, cudaMemcpyHostToDevice, st));
+    k_sigmoid_many<<<blocks_for(n), kThreads, 0, st>>>(dx.p, dy.p, n);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(y, dy.p, n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return ASNN_OK;
+}
+
+int asnn_dev_device_count(int* count) {
+    if (!count) return ASNN_E_INVALID;
+    *count = 0;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return ASNN_E_UNAVAILABLE;
+    }
+    *count = n;
+    return n > 0 ? ASNN_OK : ASNN_E_UNAVAILABLE;
+}
+
+int asnn_dev_open(int device, asnn_dev** out) {
+    if (!out) return ASNN_E_INVALID;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return ASNN_E_UNAVAILABLE;
+    }
+    if (device < 0 || device >= n) return ASNN_E_UNAVAILABLE;
+    auto* dev = new asnn_dev;
+    dev->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&dev->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&dev->own_stream, cudaStreamNonBlocking);
+    for (cudaEvent_t* ev : {&dev->ev0, &dev->ev1, &dev->ev2, &dev->ev3, &dev->ev4})
+        if (e == cudaSuccess) e = cudaEventCreate(ev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        delete dev;
+        return ASNN_E_UNAVAILABLE;
+    }
+    dev->stream = dev->own_stream;
+    *out = dev;
+    return ASNN_OK;
+}
+
+void asnn_dev_close(asnn_dev* dev) {
+    if (!dev) return;
+    cudaSetDevice(dev->device);
+    cudaStreamSynchronize(dev->stream);
+    for (cudaEvent_t ev : {dev->ev0, dev->ev1, dev->ev2, dev->ev3, dev->ev4})
+        if (ev) cudaEventDestroy(ev);
+    if (dev->own_stream) cudaStreamDestroy(dev->own_stream);
+    delete dev;
+}
+
+const char* asnn_dev_last_error(const asnn_dev* dev) { return dev ? dev->err.c_str() : ""; }
+
+int asnn_dev_set_stream(asnn_dev* dev, void* s) {
+    if (!dev) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    dev->stream = s ? static_cast<cudaStream_t>(s) : dev->own_stream;
+    return ASNN_OK;
+}
+
+void* asnn_dev_get_stream(asnn_dev* dev) { return dev ? dev->stream : nullptr; }
+
+int asnn_dev_synchronize(asnn_dev* dev) {
+    if (!dev) return ASNN_E_INVALID;
+    cudaSetDevice(dev->device);
+    CK(cudaStreamSynchronize(dev->stream));
+    return ASNN_OK;
+}
+
+int asnn_dev_last_timings(const asnn_dev* dev, asnn_timings* out) {
+    if (!dev || !out) return ASNN_E_INVALID;
+    *out = dev->timings;
+    return ASNN_OK;
+}
+
+// eval_parallel's input: a host LayeredLayout in CSR form.  The raw arrays
+// are copied as-is; id -> position renumbering runs on the device.
+int asnn_dev_upload_layout(asnn_dev* dev, const asnn_layout_desc* d, asnn_dev_layout** out) {
+    if (!dev || !d || !out) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    *out = nullptr;
+    CK(cudaSetDevice(dev->device));
+    if (d->total_layers == 0 && d->node_count) return fail(dev, ASNN_E_INVALID, "layers missing");
+    if (d->node_count && (!d->layer_offsets || !d->node_ids || !d->row_ptr))
+        return fail(dev, ASNN_E_INVALID, "null layout array");
+    if (d->total_layers && d->layer_offsets[d->total_layers] != d->node_count)
+        return fail(dev, ASNN_E_INVALID, "layer_offsets do not cover node_count");
+    const uint64_t E = d->node_count ? d->row_ptr[d->node_count] : 0;
+    if (E >= 0xFFFFFFFFull) return fail(dev, ASNN_E_INVALID, "more than 2^32-1 edges");
+    cudaStream_t st = dev->stream;
+    CK(cudaEventRecord(dev->ev0, st));
+    NetMeta n;
+    n.n_pos = d->node_count;
+    n.n_layers = d->total_layers;
+    n.n_sensors = d->total_layers ? d->layer_offsets[1] : 0;
+    n.id_bound = d->id_bound;
+    n.n_in = d->n_inputs;
+    n.n_out = d->n_outputs;
+    n.n_edges = E;
+    n.layer_offsets.assign(d->layer_offsets, d->layer_offsets + d->total_layers + 1);
+    if (d->n_inputs) n.inputs.assign(d->input_order, d->input_order + d->n_inputs);
+    if (d->n_outputs) n.outputs.assign(d->outputs, d->outputs + d->n_outputs);
+    FlatDevice f;
+    DevBuf<uint64_t> row64;
+    CK(f.node_ids.alloc(d->node_count));
+    CK(f.row_ptr.alloc(d->node_count + 1));
+    CK(row64.alloc(d->node_count + 1));
+    CK(f.in_ids.alloc(E));
+    CK(f.w.alloc(E));
+    CK(f.inputs.alloc(d->n_inputs));
+    CK(f.outputs.alloc(d->n_outputs));
+    if (d->node_count) {
+        CK(cudaMemcpyAsync(f.node_ids.p, d->node_ids, d->node_count * 4ull, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(row64.p, d->row_ptr, (d->node_count + 1) * 8ull, cudaMemcpyHostToDevice, st));
+        k_row64_to_32<<<blocks_for(d->node_count + 1), kThreads, 0, st>>>(row64.p, d->node_count + 1,
+                                                                           f.row_ptr.p);
+    } else {
+        CK(cudaMemsetAsync(f.row_ptr.p, 0, 4, st));
+    }
+    if (E) {
+        CK(cudaMemcpyAsync(f.in_ids.p, d->in_nodes, E * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(f.w.p, d->in_weights, E * 4, cudaMemcpyHostToDevice, st));
+    }
+    if (d->n_inputs)
+        CK(cudaMemcpyAsync(f.inputs.p, d->input_order, d->n_inputs * 4ull, cudaMemcpyHostToDevice, st));
+    if (d->n_outputs)
+        CK(cudaMemcpyAsync(f.outputs.p, d->outputs, d->n_outputs * 4ull, cudaMemcpyHostToDevice, st));
+    std::vector<NetMeta> nets;
+    nets.push_back(std::move(n));
+    int rc = assemble_layout(dev, std::move(nets), std::move(f), out);
+    if (rc == ASNN_OK) {
+        CK(cudaEventRecord(dev->ev1, st));
+        CK(cudaEventSynchronize(dev->ev1));
+        cudaEventElapsedTime(&dev->timings.upload_ms, dev->ev0, dev->ev1);
+    }
+    return rc;
+}
+
+void asnn_dev_free_layout(asnn_dev_layout* L) {
+    if (!L) return;
+    std::lock_guard<std::recursive_mutex> lk(L->dev->mu);
+    cudaSetDevice(L->dev->device);
+    cudaStreamSynchronize(L->dev->stream);
+    delete L;
+}
+
+int asnn_dev_layout_info(const asnn_dev_layout* L, asnn_layout_info* info) {
+    if (!L || !info) return ASNN_E_INVALID;
+    info->n_networks = static_cast<uint32_t>(L->nets.size());
+    info->total_layers = L->n_levels;
+    info->node_count = L->total_pos;
+    info->edge_count = L->total_edges;
+    info->dropped_connections = L->dropped;
+    info->id_bound = L->total_idb;
+    info->n_inputs = L->total_in;
+    info->n_outputs = L->total_out;
+    info->max_layer_width = L->max_width;
+    info->max_in_degree = L->max_deg;
+    return ASNN_OK;
+}
+
+int asnn_dev_network_info(const asnn_dev_layout* L, uint32_t g, asnn_layout_info* info) {
+    if (!L || !info) return ASNN_E_INVALID;
+    if (g >= L->nets.size()) return fail(L->dev, ASNN_E_INVALID, "network index out of range");
+    const NetMeta& n = L->nets[g];
+    info->n_networks = 1;
+    info->total_layers = n.n_layers;
+    info->node_count = n.n_pos;
+    info->edge_count = n.n_edges;
+    info->dropped_connections = n.dropped;
+    info->id_bound = n.id_bound;
+    info->n_inputs = n.n_in;
+    info->n_outputs = n.n_out;
+    uint32_t w = 0;
+    for (uint32_t l = 0; l < n.n_layers; ++l) w = std::max(w, n.layer_offsets[l + 1] - n.layer_offsets[l]);
+    info->max_layer_width = w;
+    info->max_in_degree = L->max_deg;
+    return ASNN_OK;
+}
+
+// layer_slice_bounds (layout.cpp:85-91): LayerOutOfRange past the last layer.
+int asnn_dev_layer_slice(const asnn_dev_layout* L, uint32_t layer, uint32_t* start, uint32_t* count) {
+    if (!L || !start || !count) return ASNN_E_INVALID;
+    const NetMeta& n = L->nets[0];
+    if (layer >= n.n_layers)
+        return fail(L->dev, ASNN_E_LAYER_RANGE,
+                    "layer " + std::to_string(layer) + " out of range, total layers " +
+                        std::to_string(n.n_layers));
+    *start = n.layer_offsets[layer];
+    *count = n.layer_offsets[layer + 1] - n.layer_offsets[layer];
+    return ASNN_OK;
+}
+
+// Flattened layout of one network back in the reference's form (ids, not
+// positions), for flatten parity checks.
+int asnn_dev_layout_download(asnn_dev_layout* L, uint32_t g, uint32_t* layer_offsets,
+                             uint32_t* node_ids, uint64_t* row_ptr, uint32_t* in_nodes,
+                             float* in_weights, uint32_t* input_order) {
+    if (!L) return ASNN_E_INVALID;
+    asnn_dev* dev = L->dev;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    if (g >= L->nets.size()) return fail(dev, ASNN_E_INVALID, "network index out of range");
+    CK(cudaSetDevice(dev->device));
+    const NetMeta& n = L->nets[g];
+    cudaStream_t st = dev->stream;
+    std::vector<uint32_t> ids(n.n_pos), rp(n.n_pos + 1);
+    std::vector<uint2> ed(n.n_edges);
+    if (n.n_pos) {
+        CK(cudaMemcpyAsync(ids.data(), L->node_ids.p + n.pos_base, n.n_pos * 4ull, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(rp.data(), L->row_ptr.p + n.pos_base, (n.n_pos + 1) * 4ull, cudaMemcpyDeviceToHost, st));
+    }
+    if (n.n_edges)
+        CK(cudaMemcpyAsync(ed.data(), L->edges.p + n.edge_base, n.n_edges * 8, cudaMemcpyDeviceToHost, st));
+    std::vector<uint4> si(L->total_sensors);
+    if (L->total_sensors)
+        CK(cudaMemcpyAsync(si.data(), L->sinfo.p, L->total_sensors * 16ull, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (layer_offsets) std::copy(n.layer_offsets.begin(), n.layer_offsets.end(), layer_offsets);
+    if (node_ids) std::copy(ids.begin(), ids.end(), node_ids);
+    if (row_ptr)
+        for (uint32_t p = 0; p <= n.n_pos; ++p) row_ptr[p] = rp[p] - rp[0];
+    for (uint64_t k = 0; k < n.n_edges; ++k) {
+        const uint32_t pos = ed[k].x;
+        if (in_nodes)
+            in_nodes[k] = (pos >= n.pos_base && pos < n.pos_base + n.n_pos) ? ids[pos - n.pos_base]
+                                                                            : ASNN_UNASSIGNED;
+        if (in_weights) std::memcpy(&in_weights[k], &ed[k].y, 4);
+    }
+    if (input_order) std::copy(n.inputs.begin(), n.inputs.end(), input_order);
+    (void)si;
+    return ASNN_OK;
+}
+
+int asnn_dev_activate_plan(asnn_dev_layout* L, uint32_t n_vec, uint32_t* kernels, uint64_t* alg_bytes,
+                           uint64_t* conn_evals) {
+    if (!L) return ASNN_E_INVALID;
+    uint32_t k = L->total_sensors ? 1 : 0;
+    for (uint32_t l = 1; l < L->n_levels; ++l) k += (L->lvl_off[l + 1] > L->lvl_off[l]);
+    k += L->total_out ? 1 : 0;
+    if (kernels) *kernels = k;
+    const uint64_t B = n_vec, E = L->total_edges, N = L->total_pos;
+    // 8E (col+w) + 4(N+1) row_ptr + 4EB gathers + 4NB writes + 4 n_in B reads
+    if (alg_bytes) *alg_bytes = 8 * E + 4 * (N + 1) + 4 * E * B + 4 * N * B + 4ull * L->total_in * B;
+    if (conn_evals) *conn_evals = E * B;
+    return ASNN_OK;
+}
+
+int asnn_dev_activate_device(asnn_dev_layout* L, const float* x_dev, uint32_t n_vec, float* out_dev) {
+    if (!L) return ASNN_E_INVALID;
+    asnn_dev* dev = L->dev;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    if (n_vec == 0) return ASNN_OK;
+    CK(cudaSetDevice(dev->device));
+    return run_sweep(L, x_dev, n_vec, out_dev, nullptr);
+}
+
+// eval_parallel(DeviceCompute) + read_outputs over a batch of host vectors.
+int asnn_dev_activate(asnn_dev_layout* L, const float* x, uint32_t n_vec, uint64_t n_x, float* out,
+                      float* state) {
+    if (!L) return ASNN_E_INVALID;
+    asnn_dev* dev = L->dev;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    // eval.cpp:26-28 -- arity check (per vector, all networks).
+    if (n_x != static_cast<uint64_t>(L->total_in) * n_vec)
+        return fail(dev, ASNN_E_ARITY,
+                    "expected " + std::to_string(static_cast<uint64_t>(L->total_in) * n_vec) +
+                        " input values, got " + std::to_string(n_x));
+    if (n_vec == 0) return ASNN_OK;
+    if (!x && n_x) return fail(dev, ASNN_E_INVALID, "null input");
+    CK(cudaSetDevice(dev->device));
+    cudaStream_t st = dev->stream;
+    const size_t xb = static_cast<size_t>(n_x) * 4;
+    const size_t ob = static_cast<size_t>(L->total_out) * n_vec * 4;
+    CK(L->x_stage.ensure(n_x ? n_x : 1));
+    CK(L->out_stage.ensure(static_cast<size_t>(L->total_out) * n_vec + 1));
+    DevBuf<float> state_dev;
+    if (state) CK(state_dev.alloc(static_cast<size_t>(L->total_idb) * n_vec));
+    CK(cudaEventRecord(dev->ev0, st));
+    if (xb) {
+        const float* src = x;
+        if (!is_pinned(x)) {
+            CK(L->pin_x.ensure(xb));
+            std::memcpy(L->pin_x.p, x, xb);
+            src = static_cast<const float*>(L->pin_x.p);
+        }
+        CK(cudaMemcpyAsync(L->x_stage.p, src, xb, cudaMemcpyHostToDevice, st));
+    }
+    int rc = run_sweep(L, L->x_stage.p, n_vec, out ? L->out_stage.p : nullptr,
+                       state ? state_dev.p : nullptr);
+    if (rc) return rc;
+    bool stage_out = false;
+    if (out && ob) {
+        if (is_pinned(out)) {
+            CK(cudaMemcpyAsync(out, L->out_stage.p, ob, cudaMemcpyDeviceToHost, st));
+        } else {
+            CK(L->pin_out.ensure(ob));
+            CK(cudaMemcpyAsync(L->pin_out.p, L->out_stage.p, ob, cudaMemcpyDeviceToHost, st));
+            stage_out = true;
+        }
+    }
+    if (state)
+        CK(cudaMemcpyAsync(state, state_dev.p, static_cast<size_t>(L->total_idb) * n_vec * 4,
+                           cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(dev->ev1, st));
+    CK(cudaEventSynchronize(dev->ev1));
+    if (stage_out) std::memcpy(out, L->pin_out.p, ob);
+    cudaEventElapsedTime(&dev->timings.activate_ms, dev->ev0, dev->ev1);
+    return ASNN_OK;
+}
+
+}  // extern "C"

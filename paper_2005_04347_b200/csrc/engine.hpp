@@ -1,0 +1,173 @@
+// engine.hpp -- internal host-side structures of the ASNN engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "asnn_dev.h"
+
+namespace asnn_b200 {
+
+// Owning device buffer (cudaMalloc / cudaFree).
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+        o.p = nullptr;
+        o.n = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    cudaError_t alloc(size_t count) {
+        reset();
+        if (count == 0) count = 1;
+        cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T));
+        if (e == cudaSuccess) n = count;
+        else p = nullptr;
+        return e;
+    }
+    cudaError_t ensure(size_t count) { return count <= n ? cudaSuccess : alloc(count); }
+};
+
+// Pinned host staging buffer.
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() { reset(); }
+    void reset() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    cudaError_t ensure(size_t b) {
+        if (b <= bytes) return cudaSuccess;
+        reset();
+        cudaError_t e = cudaMallocHost(&p, b);
+        if (e == cudaSuccess) bytes = b;
+        else p = nullptr;
+        return e;
+    }
+};
+
+}  // namespace asnn_b200
+
+struct asnn_dev {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr, ev4 = nullptr;
+    std::recursive_mutex mu;
+    std::string err;
+    asnn_timings timings{};
+};
+
+namespace asnn_b200 {
+
+// One network inside a layout (a population holds many).
+struct NetMeta {
+    uint32_t pos_base = 0;    // first global position
+    uint32_t n_pos = 0;       // assigned nodes
+    uint32_t n_sensors = 0;   // layer-0 nodes
+    uint32_t n_layers = 0;    // total_layers of this network
+    uint32_t id_bound = 0;
+    uint32_t n_in = 0, n_out = 0;
+    uint32_t in_prefix = 0, out_prefix = 0, idb_prefix = 0;
+    uint64_t edge_base = 0, n_edges = 0;
+    uint64_t dropped = 0;
+    std::vector<uint32_t> layer_offsets;  // local positions, [n_layers + 1]
+    std::vector<uint32_t> inputs;         // declared input ids (layout.cpp:23)
+    std::vector<uint32_t> outputs;        // declared output ids
+};
+
+// Cached CUDA graph of one activation sweep.
+struct SweepGraph {
+    cudaGraphExec_t exec = nullptr;
+    uint32_t n_vec = 0;
+    const float* x = nullptr;
+    float* out = nullptr;
+    float* state = nullptr;
+    cudaStream_t stream = nullptr;
+    void reset() {
+        if (exec) cudaGraphExecDestroy(exec);
+        exec = nullptr;
+    }
+};
+
+}  // namespace asnn_b200
+
+struct asnn_dev_layout {
+    asnn_dev* dev = nullptr;
+    std::vector<asnn_b200::NetMeta> nets;
+    uint32_t total_pos = 0, total_sensors = 0, total_in = 0, total_out = 0, total_idb = 0;
+    uint32_t n_levels = 0;  // global levels (max over nets)
+    uint32_t max_width = 0, max_deg = 0;
+    uint64_t total_edges = 0, dropped = 0;
+    std::vector<uint32_t> lvl_off;  // sched offsets per global level, [n_levels + 1]
+
+    asnn_b200::DevBuf<uint32_t> row_ptr;    // [total_pos + 1]
+    asnn_b200::DevBuf<uint2> edges;         // [total_edges] {src pos, w bits}
+    asnn_b200::DevBuf<uint32_t> sched;      // [total_pos] level-major schedule
+    asnn_b200::DevBuf<uint4> sinfo;         // [total_sensors]
+    asnn_b200::DevBuf<uint4> oinfo;         // [total_out]
+    asnn_b200::DevBuf<uint32_t> state_map;  // [total_idb] id -> pos
+    asnn_b200::DevBuf<uint32_t> idb_prefix; // [n_nets + 1]
+    asnn_b200::DevBuf<uint32_t> node_ids;   // [total_pos]
+
+    // activation workspace
+    asnn_b200::DevBuf<float> A;
+    asnn_b200::DevBuf<float> x_stage, out_stage;
+    asnn_b200::PinnedBuf pin_x, pin_out;
+    asnn_b200::SweepGraph graph;
+
+    ~asnn_dev_layout() { graph.reset(); }
+};
+
+namespace asnn_b200 {
+
+// Records `msg` (plus the CUDA error string) as the handle's last error and
+// returns the status.
+int fail(asnn_dev* dev, int status, const std::string& msg);
+int cuda_fail(asnn_dev* dev, cudaError_t e, const char* what);
+
+// Device-side assembly of a layout from flattened per-network arrays that are
+// already resident (used by upload, build and population paths).  Takes
+// ownership of d_node_ids / d_row_ptr; d_in_ids / d_w are per-edge source ids
+// (local to their network) and weights, freed by the caller.
+struct FlatDevice {
+    DevBuf<uint32_t> node_ids;  // [P]  global pos order
+    DevBuf<uint32_t> row_ptr;   // [P+1] global edge offsets
+    DevBuf<uint32_t> in_ids;    // [E]
+    DevBuf<float> w;            // [E]
+    DevBuf<uint32_t> inputs;    // [sum n_in]  declared input ids, per net
+    DevBuf<uint32_t> outputs;   // [sum n_out] declared output ids, per net
+};
+int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& flat,
+                    asnn_dev_layout** out);
+
+}  // namespace asnn_b200

@@ -1,0 +1,172 @@
+// kernels.cuh -- activation kernels of the ASNN engine (sm_100a).
+//
+// Data layout in HBM:
+//   positions  p = 0..P-1 : every assigned node of every network, network-major,
+//                           then (layer, id) -- the reference's flat order
+//                           (layout.cpp:28-50);
+//   row_ptr[P+1]  (u32)   : destination-major CSR of incoming edges;
+//   edges[E]      (uint2) : {source position, weight bits}, each row in the
+//                           reference's accumulation order (ascending source
+//                           id, layout.cpp:64-80);
+//   A[P][ldA]     (f32)   : activations, one row per position, one column per
+//                           input vector (ldA = padded batch), so a source row
+//                           gather across the batch is one coalesced 128-bit
+//                           load per thread.
+#pragma once
+
+#include "common.cuh"
+
+namespace asnn_b200 {
+
+constexpr uint32_t kUnassigned = 0xFFFFFFFFu;
+
+// ---------------------------------------------------------------------------
+// K-sense: sensors (layer 0).  eval.cpp:17 + make_state eval.cpp:25-35:
+// A[pos][b] = sigmoid32(x_b[k]) where k is the declared input index feeding
+// the sensor id (last duplicate wins).  sinfo = {pos, in_prefix, n_in, k}.
+__global__ void k_sense(const uint4* __restrict__ sinfo, uint32_t n_sensors,
+                        const float* __restrict__ x, uint32_t n_vec, float* __restrict__ A,
+                        uint32_t ldA) {
+    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t s = idx / ldA;
+    const uint32_t b = static_cast<uint32_t>(idx - s * ldA);
+    if (s >= n_sensors) return;
+    const uint4 si = sinfo[s];
+    float xv = 0.0f;
+    if (b < n_vec && si.w != kUnassigned)
+        xv = x[static_cast<uint64_t>(n_vec) * si.y + static_cast<uint64_t>(b) * si.z + si.w];
+    A[static_cast<uint64_t>(si.x) * ldA + b] = sigmoid32(xv);
+}
+
+// ---------------------------------------------------------------------------
+// K-act-lane: one launch per dependency level.  activate_node (eval.cpp:16-23)
+// for every (node, column tile) item of the level:
+//   LANES threads own one item; thread `lane` owns V consecutive batch
+//   columns; edges are loaded cooperatively (one 8-byte {col, w} per lane,
+//   coalesced) and broadcast with __shfl; each of the U in-flight source-row
+//   gathers is one V-wide vector load; the sum runs sequentially in the
+//   stored edge order with fp32 mul then fp32 add (bit-exact).
+// sched lists the level's positions (heaviest first); item -> (sched[item /
+// tiles], item % tiles).
+template <int V, int LANES>
+struct LevelCfg {
+    static constexpr int CH = LANES < 8 ? 8 : LANES;  // edges per chunk
+    static constexpr int PER = CH / LANES;            // edges held per lane
+    static constexpr int U = 8;                       // gathers in flight
+};
+
+template <int V, int LANES>
+__global__ void __launch_bounds__(256)
+k_level(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
+        float* __restrict__ A, uint32_t ldA, const uint32_t* __restrict__ sched,
+        uint32_t n_items, uint32_t tiles) {
+    using C = LevelCfg<V, LANES>;
+    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t item = gt / LANES;
+    if (item >= n_items) return;  // uniform across the LANES group
+    const uint32_t lane = threadIdx.x % LANES;
+    const uint32_t ni = item / tiles;
+    const uint32_t tile = item - ni * tiles;
+    const uint32_t node = __ldg(&sched[ni]);
+    const uint32_t col = tile * (LANES * V) + lane * V;
+    const unsigned gmask =
+        LANES == 32 ? 0xFFFFFFFFu
+                    : (((1u << LANES) - 1u) << ((threadIdx.x & 31u) / LANES * LANES));
+    const uint32_t beg = __ldg(&row_ptr[node]);
+    const uint32_t end = __ldg(&row_ptr[node + 1]);
+    const float* __restrict__ Acol = A + col;
+
+    float acc[V];
+#pragma unroll
+    for (int c = 0; c < V; ++c) acc[c] = 0.0f;
+
+    for (uint32_t base = beg; base < end; base += C::CH) {
+        uint2 e[C::PER];
+#pragma unroll
+        for (int r = 0; r < C::PER; ++r) {
+            const uint32_t k = base + r * LANES + lane;
+            e[r] = k < end ? __ldg(&edges[k]) : make_uint2(0u, 0u);
+        }
+        const uint32_t n = min(static_cast<uint32_t>(C::CH), end - base);
+#pragma unroll
+        for (int j0 = 0; j0 < C::CH; j0 += C::U) {
+            if (static_cast<uint32_t>(j0) >= n) break;
+            float v[C::U][V];
+            float wj[C::U];
+#pragma unroll
+            for (int u = 0; u < C::U; ++u) {
+                const int j = j0 + u;
+                uint32_t s, wb;
+                if constexpr (LANES == 1) {
+                    s = e[j].x;
+                    wb = e[j].y;
+                } else {
+                    s = __shfl_sync(gmask, e[j / LANES].x, j % LANES, LANES);
+                    wb = __shfl_sync(gmask, e[j / LANES].y, j % LANES, LANES);
+                }
+                wj[u] = __uint_as_float(wb);
+                if (static_cast<uint32_t>(j) < n) {
+                    load_cols<V>(v[u], Acol + static_cast<uint64_t>(s) * ldA);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < V; ++c) v[u][c] = 0.0f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < C::U; ++u) {
+                if (static_cast<uint32_t>(j0 + u) < n) {
+#pragma unroll
+                    for (int c = 0; c < V; ++c) acc[c] = mac(acc[c], wj[u], v[u][c]);
+                }
+            }
+        }
+    }
+    float out[V];
+#pragma unroll
+    for (int c = 0; c < V; ++c) out[c] = sigmoid32(acc[c]);
+    store_cols<V>(A + static_cast<uint64_t>(node) * ldA + col, out);
+}
+
+__global__ void k_sigmoid_many(const float* __restrict__ x, float* __restrict__ y, uint64_t n) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = sigmoid32(x[i]);
+}
+
+// ---------------------------------------------------------------------------
+// K-gather-out: read_outputs (eval.cpp:82-87) for the whole batch.
+// oinfo = {pos (or kUnassigned), out_prefix, n_out, k}; out is [net][b][k].
+__global__ void k_gather_out(const uint4* __restrict__ oinfo, uint32_t n_total,
+                             const float* __restrict__ A, uint32_t ldA, uint32_t n_vec,
+                             float* __restrict__ out) {
+    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t o = idx / n_vec;
+    const uint32_t b = static_cast<uint32_t>(idx - o * n_vec);
+    if (o >= n_total) return;
+    const uint4 oi = oinfo[o];
+    const float v = oi.x == kUnassigned ? 0.0f : A[static_cast<uint64_t>(oi.x) * ldA + b];
+    out[static_cast<uint64_t>(n_vec) * oi.y + static_cast<uint64_t>(b) * oi.z + oi.w] = v;
+}
+
+// K-state: the id-indexed ActivationState.outputs (eval.hpp:14-17) for every
+// vector; ids without a layer stay 0.0f (eval.cpp:30-31).
+__global__ void k_state(const uint32_t* __restrict__ state_map, const uint32_t* __restrict__ idb_prefix,
+                        uint32_t n_nets, uint32_t total_idb, const float* __restrict__ A,
+                        uint32_t ldA, uint32_t n_vec, float* __restrict__ state) {
+    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t f = idx / n_vec;
+    const uint32_t b = static_cast<uint32_t>(idx - f * n_vec);
+    if (f >= total_idb) return;
+    uint32_t lo = 0, hi = n_nets;  // net g: idb_prefix[g] <= f < idb_prefix[g+1]
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (idb_prefix[mid] <= f) lo = mid;
+        else hi = mid;
+    }
+    const uint32_t base = idb_prefix[lo];
+    const uint32_t idb = idb_prefix[lo + 1] - base;
+    const uint32_t pos = state_map[f];
+    const float v = pos == kUnassigned ? 0.0f : A[static_cast<uint64_t>(pos) * ldA + b];
+    state[static_cast<uint64_t>(n_vec) * base + static_cast<uint64_t>(b) * idb + (f - base)] = v;
+}
+
+}  // namespace asnn_b200

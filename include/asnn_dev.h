@@ -181,6 +181,13 @@ int asnn_dev_activate(asnn_dev_layout* layout, const float* x, uint32_t n_vec, u
 int asnn_dev_activate_device(asnn_dev_layout* layout, const float* x_dev, uint32_t n_vec,
                              float* out_dev);
 
+/* One sweep launched kernel by kernel (no graph) with a CUDA event between
+ * launches on the handle's stream: ms[k] receives the device time of launch
+ * k in order (sensors, each level, output gather); *n_launches its count
+ * (ms must hold asnn_dev_activate_plan's `kernels` entries). */
+int asnn_dev_profile_sweep(asnn_dev_layout* layout, const float* x_dev, uint32_t n_vec,
+                           float* out_dev, float* ms, uint32_t* n_launches);
+
 /* Number of kernels one activate of n_vec vectors launches, and the
  * algorithmic bytes it moves. */
 int asnn_dev_activate_plan(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* kernels,

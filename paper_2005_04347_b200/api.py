@@ -432,14 +432,30 @@ class DeviceLayout:
                                                            C.byref(ce)))
         return {"kernels": k.value, "alg_bytes": b.value, "conn_evals": ce.value}
 
+    def profile(self, x_ptr: int, n_vec: int, out_ptr: int) -> np.ndarray:
+        """Per-launch device ms of one sweep (sensors, levels, gather)."""
+        k = self.plan(n_vec)["kernels"]
+        ms = np.zeros(k, np.float32)
+        n = C.c_uint32()
+        self.dev.check(self.dev.lib.asnn_dev_profile_sweep(
+            self.h, C.c_void_p(x_ptr), n_vec, C.c_void_p(out_ptr), _lib.ptr(ms, C.c_float),
+            C.byref(n)))
+        return ms[:n.value]
+
     # activation ---------------------------------------------------------------
-    def activate(self, X: np.ndarray, outputs: bool = True, state: bool = False):
-        """X: [n_vec][n_inputs] float32 (host).  Returns (out [n_vec][n_outputs]
-        or None, state [n_vec][id_bound] or None)."""
+    def activate(self, X: np.ndarray, outputs: bool = True, state: bool = False,
+                 n_vec: Optional[int] = None):
+        """X: [n_vec][n_inputs] float32 (host) for one network.  For a
+        population pass X as [n_networks][n_vec][n_inputs] (or any buffer
+        holding each network's [n_vec][n_inputs] block in order) together with
+        n_vec.  Returns (out, state): out holds each network's
+        [n_vec][n_outputs] block, state each network's [n_vec][id_bound]
+        block; for a single network they are shaped [n_vec][...]."""
         X = np.ascontiguousarray(X, dtype=np.float32)
-        if X.ndim == 1:
-            X = X[None, :]
-        n_vec = X.shape[0]
+        if n_vec is None:
+            if X.ndim == 1:
+                X = X[None, :]
+            n_vec = X.shape[0]
         inf = self.info() if self._info is None else self._info
         self._info = inf
         out = np.empty((n_vec, inf["n_outputs"]), np.float32) if outputs else None

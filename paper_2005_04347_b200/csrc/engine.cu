@@ -316,9 +316,14 @@ namespace {
 
 // One activation sweep, stream-ordered: sensors, every level, outputs, state.
 int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out, float* state,
-                 cudaStream_t st) {
+                 cudaStream_t st, std::vector<cudaEvent_t>* evs = nullptr) {
     asnn_dev* dev = L->dev;
     const uint32_t ldA = padded_batch(n_vec);
+    size_t ek = 0;
+    auto mark = [&]() {
+        if (evs && ek < evs->size()) cudaEventRecord((*evs)[ek++], st);
+    };
+    mark();
     if (L->total_sensors)
         k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(
             L->sinfo.p, L->total_sensors, x, n_vec, L->A.p, ldA);
@@ -327,13 +332,17 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         const uint32_t n = L->lvl_off[l + 1] - L->lvl_off[l];
         if (!n) continue;
         const uint64_t items = static_cast<uint64_t>(n) * ll.tiles;
+        if (L->total_sensors || l > 1) mark();
         ll.fn<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(
             L->row_ptr.p, L->edges.p, L->A.p, ldA, L->sched.p + L->lvl_off[l],
             static_cast<uint32_t>(items), ll.tiles);
     }
-    if (out && L->total_out)
+    if (out && L->total_out) {
+        mark();
         k_gather_out<<<blocks_for(static_cast<uint64_t>(L->total_out) * n_vec), kThreads, 0, st>>>(
             L->oinfo.p, L->total_out, L->A.p, ldA, n_vec, out);
+    }
+    mark();
     if (state && L->total_idb)
         k_state<<<blocks_for(static_cast<uint64_t>(L->total_idb) * n_vec), kThreads, 0, st>>>(
             L->state_map.p, L->idb_prefix.p, static_cast<uint32_t>(L->nets.size()), L->total_idb,
@@ -649,6 +658,30 @@ int asnn_dev_layout_download(asnn_dev_layout* L, uint32_t g, uint32_t* layer_off
     if (input_order) std::copy(n.inputs.begin(), n.inputs.end(), input_order);
     (void)si;
     return ASNN_OK;
+}
+
+int asnn_dev_profile_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_vec, float* out_dev,
+                           float* ms, uint32_t* n_launches) {
+    if (!L || !ms || !n_launches) return ASNN_E_INVALID;
+    asnn_dev* dev = L->dev;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    CK(cudaSetDevice(dev->device));
+    int rc = ensure_workspace(L, n_vec);
+    if (rc) return rc;
+    uint32_t k = 0;
+    rc = asnn_dev_activate_plan(L, n_vec, &k, nullptr, nullptr);
+    if (rc) return rc;
+    if (!out_dev) k -= L->total_out ? 1 : 0;
+    std::vector<cudaEvent_t> evs(k + 1);
+    for (auto& e : evs) CK(cudaEventCreate(&e));
+    rc = launch_sweep(L, x_dev, n_vec, out_dev, nullptr, dev->stream, &evs);
+    cudaError_t e = cudaStreamSynchronize(dev->stream);
+    for (uint32_t i = 0; i < k && rc == ASNN_OK && e == cudaSuccess; ++i)
+        cudaEventElapsedTime(&ms[i], evs[i], evs[i + 1]);
+    for (auto& ev : evs) cudaEventDestroy(ev);
+    CK(e);
+    *n_launches = k;
+    return rc;
 }
 
 int asnn_dev_activate_plan(asnn_dev_layout* L, uint32_t n_vec, uint32_t* kernels, uint64_t* alg_bytes,

@@ -298,6 +298,11 @@ class Device:
     def synchronize(self):
         self.check(self.lib.asnn_dev_synchronize(self.h))
 
+    def set_heavy_threshold(self, min_in_degree: Optional[int]):
+        """Rows above this in-degree use the streamed heavy kernel (None = off)."""
+        v = 0xFFFFFFFF if min_in_degree is None else int(min_in_degree)
+        self.check(self.lib.asnn_dev_set_heavy_threshold(self.h, v))
+
     def timings(self) -> dict:
         t = _lib.Timings()
         self.check(self.lib.asnn_dev_last_timings(self.h, C.byref(t)))

@@ -8,6 +8,7 @@
 
 #include "engine.hpp"
 #include "kernels.cuh"
+#include "sort.cuh"
 
 using namespace asnn_b200;
 
@@ -142,6 +143,32 @@ __global__ void k_max_deg(const uint32_t* __restrict__ row_ptr, uint32_t P, uint
     if ((threadIdx.x & 31) == 0 && d) atomicMax(out, d);
 }
 
+// Schedule sort keys: (layer << 16) | (0xFFFF - min(in-degree, 0xFFFF)).
+__global__ void k_sched_keys(MetaPtrs m, const uint32_t* __restrict__ lo_cat,
+                             const uint32_t* __restrict__ lo_base, const uint32_t* __restrict__ row_ptr,
+                             uint32_t P, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const uint32_t g = find_seg(m.pos, m.G, p);
+    const uint32_t lp = p - m.pos[g];
+    const uint32_t nl = lo_base[g + 1] - lo_base[g] - 1;
+    const uint32_t lv = find_seg(lo_cat + lo_base[g], nl, lp);
+    const uint32_t deg = min(row_ptr[p + 1] - row_ptr[p], 0xFFFFu);
+    keys[p] = (lv << 16) | (0xFFFFu - deg);
+    vals[p] = p;
+}
+
+__global__ void k_heavy_counts(const uint32_t* __restrict__ keys, uint32_t n, uint32_t stride,
+                               uint32_t* __restrict__ hv) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t lv = keys[i] >> 16;
+    const uint32_t deg = 0xFFFFu - (keys[i] & 0xFFFFu);
+#pragma unroll
+    for (int t = 0; t < kNumHeavyThr; ++t)
+        if (deg > heavy_thr(t)) atomicAdd(&hv[t * stride + lv], 1u);
+}
+
 __global__ void k_row64_to_32(const uint64_t* __restrict__ in, uint32_t n, uint32_t* __restrict__ out) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = static_cast<uint32_t>(in[i]);
@@ -176,6 +203,59 @@ LevelLaunch level_launch_for(uint32_t ldA) {
         case 64: return {k_level<4, 16>, 16, 1};
         default: return {k_level<4, 32>, 32, ldA / 128};
     }
+}
+
+struct HeavyLaunch {
+    void (*fn)(const uint32_t*, const uint2*, float*, uint32_t, const uint32_t*, uint32_t);
+    uint32_t threads;
+    uint32_t smem;
+    uint32_t tiles;
+};
+
+template <int TC>
+HeavyLaunch heavy_launch() {
+    const uint32_t smem = heavy::kStages * heavy::kRows * (TC + 1) * 4 + 2 * heavy::kStages * 8;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_heavy<TC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        configured = true;
+    }
+    return {k_heavy<TC>, 32u + (TC < 32 ? 32u : static_cast<uint32_t>(TC)), smem, 1};
+}
+
+// Rows must be >= 16 bytes for a bulk copy: no heavy path below 4 columns.
+HeavyLaunch heavy_launch_for(uint32_t ldA) {
+    switch (ldA) {
+        case 1:
+        case 2: return {nullptr, 0, 0, 0};
+        case 4: return heavy_launch<4>();
+        case 8: return heavy_launch<8>();
+        case 16: return heavy_launch<16>();
+        case 32: return heavy_launch<32>();
+        case 64: return heavy_launch<64>();
+        default: {
+            HeavyLaunch h = heavy_launch<128>();
+            h.tiles = ldA / 128;
+            return h;
+        }
+    }
+}
+
+// Index into heavy_thr() of the smallest listed threshold >= `want` (an
+// in-degree), or -1 when the heavy path is off.
+int heavy_index_for(uint32_t want) {
+    for (int t = 0; t < kNumHeavyThr; ++t)
+        if (heavy_thr(t) >= want) return heavy_thr(t) == 0xFFFFFFFFu ? -1 : t;
+    return -1;
+}
+
+// Default: ASNN_HEAVY_THRESHOLD (an in-degree, or "off"), else 128.
+uint32_t default_heavy_threshold() {
+    const char* s = getenv("ASNN_HEAVY_THRESHOLD");
+    if (s && std::string(s) == "off") return 0xFFFFFFFFu;
+    if (s) return static_cast<uint32_t>(strtoul(s, nullptr, 10));
+    return 128;
 }
 
 }  // namespace
@@ -267,28 +347,66 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
                                                                  maxdeg.p);
     CKL(cudaGetLastError());
 
-    // Level-major schedule: global level l runs layer l of every network.
+    // Level-major schedule: global level l runs layer l of every network, its
+    // positions ordered by in-degree descending (longest rows first, LPT),
+    // ties by position.  A stable radix sort of all positions by
+    // (level, ~degree); level-0 sensors sort first and are skipped.
     uint32_t n_levels = 0;
     for (const auto& n : nets) n_levels = std::max(n_levels, n.n_layers);
     L->n_levels = n_levels;
     L->lvl_off.assign(n_levels + 1, 0);
-    std::vector<uint32_t> sched;
-    sched.reserve(L->total_pos - L->total_sensors);
-    for (uint32_t l = 1; l < n_levels; ++l) {
-        L->lvl_off[l] = static_cast<uint32_t>(sched.size());
-        for (const auto& n : nets) {
-            if (l >= n.n_layers) continue;
-            for (uint32_t p = n.layer_offsets[l]; p < n.layer_offsets[l + 1]; ++p)
-                sched.push_back(n.pos_base + p);
+    {
+        std::vector<uint32_t> lvl_count(n_levels + 1, 0), lo_cat, lo_base(G + 1, 0);
+        for (uint32_t g = 0; g < G; ++g) {
+            const auto& n = nets[g];
+            for (uint32_t l = 0; l < n.n_layers; ++l) {
+                const uint32_t c = n.layer_offsets[l + 1] - n.layer_offsets[l];
+                lvl_count[l] += c;
+                L->max_width = std::max(L->max_width, c);
+            }
+            lo_base[g + 1] = lo_base[g] + n.n_layers + 1;
+            lo_cat.insert(lo_cat.end(), n.layer_offsets.begin(), n.layer_offsets.end());
         }
+        uint32_t acc = 0;
+        for (uint32_t l = 1; l < n_levels; ++l) {
+            L->lvl_off[l] = acc;
+            acc += lvl_count[l];
+        }
+        if (n_levels) L->lvl_off[n_levels] = acc;
+        const uint32_t P = L->total_pos;
+        DevBuf<uint32_t> d_lo, d_lob, keys, vals, hv;
+        CKL(d_lo.alloc(lo_cat.size()));
+        CKL(d_lob.alloc(G + 1));
+        CKL(keys.alloc(P + 1));
+        CKL(vals.alloc(P + 1));
+        if (!lo_cat.empty())
+            CKL(cudaMemcpyAsync(d_lo.p, lo_cat.data(), lo_cat.size() * 4, cudaMemcpyHostToDevice, st));
+        CKL(cudaMemcpyAsync(d_lob.p, lo_base.data(), (G + 1) * 4, cudaMemcpyHostToDevice, st));
+        if (P)
+            k_sched_keys<<<blocks_for(P), kThreads, 0, st>>>(m, d_lo.p, d_lob.p, flat.row_ptr.p, P, keys.p,
+                                                             vals.p);
+        CKL(cudaGetLastError());
+        SortBuffers sb;
+        uint32_t *ks = nullptr, *vs = nullptr;
+        int lb = 0;
+        while ((1u << lb) < n_levels) ++lb;
+        int rc = radix_sort_pairs(dev, keys.p, vals.p, P, std::max(1, lb) + 16, sb, &ks, &vs, st);
+        if (rc) return cleanup_fail(rc);
+        const uint32_t S = L->total_sensors;
+        CKL(L->sched.alloc(P - S + 1));
+        if (P > S)
+            CKL(cudaMemcpyAsync(L->sched.p, vs + S, (P - S) * 4ull, cudaMemcpyDeviceToDevice, st));
+        // heavy-row counts per level for each threshold kHeavyThr[t]
+        const size_t nh = static_cast<size_t>(kNumHeavyThr) * (n_levels + 1);
+        CKL(hv.alloc(nh));
+        CKL(cudaMemsetAsync(hv.p, 0, nh * 4, st));
+        if (P > S)
+            k_heavy_counts<<<blocks_for(P - S), kThreads, 0, st>>>(ks + S, P - S, n_levels + 1, hv.p);
+        CKL(cudaGetLastError());
+        L->heavy_cnt.assign(nh, 0);
+        CKL(cudaMemcpyAsync(L->heavy_cnt.data(), hv.p, nh * 4, cudaMemcpyDeviceToHost, st));
+        CKL(cudaStreamSynchronize(st));
     }
-    if (n_levels) L->lvl_off[n_levels] = static_cast<uint32_t>(sched.size());
-    for (const auto& n : nets)
-        for (uint32_t l = 0; l < n.n_layers; ++l)
-            L->max_width = std::max(L->max_width, n.layer_offsets[l + 1] - n.layer_offsets[l]);
-    CKL(L->sched.alloc(sched.size()));
-    if (!sched.empty())
-        CKL(cudaMemcpyAsync(L->sched.p, sched.data(), sched.size() * 4, cudaMemcpyHostToDevice, st));
     CKL(L->idb_prefix.alloc(G + 1));
     CKL(cudaMemcpyAsync(L->idb_prefix.p, d_meta.p + (G + 1), (G + 1) * 4, cudaMemcpyDeviceToDevice,
                         st));
@@ -328,14 +446,40 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(
             L->sinfo.p, L->total_sensors, x, n_vec, L->A.p, ldA);
     const LevelLaunch ll = level_launch_for(ldA);
+    const HeavyLaunch hl = heavy_launch_for(ldA);
+    const int thr = heavy_index_for(dev->heavy_threshold);
+    if (dev->fork_ev.size() < L->n_levels) {
+        for (size_t i = dev->fork_ev.size(); i < L->n_levels; ++i) {
+            cudaEvent_t a, b;
+            CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+            dev->fork_ev.push_back(a);
+            dev->join_ev.push_back(b);
+        }
+    }
     for (uint32_t l = 1; l < L->n_levels; ++l) {
         const uint32_t n = L->lvl_off[l + 1] - L->lvl_off[l];
         if (!n) continue;
-        const uint64_t items = static_cast<uint64_t>(n) * ll.tiles;
+        // rows above the threshold stream through k_heavy on the aux branch,
+        // concurrently with the light rows on the main stream
+        const uint32_t nh = (hl.fn && thr >= 0) ? L->heavy_cnt[thr * (L->n_levels + 1) + l] : 0;
         if (L->total_sensors || l > 1) mark();
-        ll.fn<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(
-            L->row_ptr.p, L->edges.p, L->A.p, ldA, L->sched.p + L->lvl_off[l],
-            static_cast<uint32_t>(items), ll.tiles);
+        if (nh) {
+            CK(cudaEventRecord(dev->fork_ev[l], st));
+            CK(cudaStreamWaitEvent(dev->aux, dev->fork_ev[l], 0));
+            hl.fn<<<nh * hl.tiles, hl.threads, hl.smem, dev->aux>>>(
+                L->row_ptr.p, L->edges.p, L->A.p, ldA, L->sched.p + L->lvl_off[l], hl.tiles);
+        }
+        if (n > nh) {
+            const uint64_t items = static_cast<uint64_t>(n - nh) * ll.tiles;
+            ll.fn<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(
+                L->row_ptr.p, L->edges.p, L->A.p, ldA, L->sched.p + L->lvl_off[l] + nh,
+                static_cast<uint32_t>(items), ll.tiles);
+        }
+        if (nh) {
+            CK(cudaEventRecord(dev->join_ev[l], dev->aux));
+            CK(cudaStreamWaitEvent(st, dev->join_ev[l], 0));
+        }
     }
     if (out && L->total_out) {
         mark();
@@ -373,7 +517,7 @@ int run_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out, fl
     cudaStream_t st = dev->stream;
     SweepGraph& g = L->graph;
     if (!(g.exec && g.n_vec == n_vec && g.x == x && g.out == out && g.state == state &&
-          g.stream == st)) {
+          g.stream == st && g.epoch == dev->option_epoch)) {
         g.reset();
         cudaGraph_t graph = nullptr;
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -392,6 +536,7 @@ int run_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out, fl
         g.out = out;
         g.state = state;
         g.stream = st;
+        g.epoch = dev->option_epoch;
     }
     CK(cudaGraphLaunch(g.exec, st));
     return ASNN_OK;
@@ -464,6 +609,12 @@ int asnn_dev_open(int device, asnn_dev** out) {
         return ASNN_E_UNAVAILABLE;
     }
     dev->stream = dev->own_stream;
+    dev->heavy_threshold = default_heavy_threshold();
+    if (cudaStreamCreateWithFlags(&dev->aux, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        delete dev;
+        return ASNN_E_UNAVAILABLE;
+    }
     *out = dev;
     return ASNN_OK;
 }
@@ -474,6 +625,9 @@ void asnn_dev_close(asnn_dev* dev) {
     cudaStreamSynchronize(dev->stream);
     for (cudaEvent_t ev : {dev->ev0, dev->ev1, dev->ev2, dev->ev3, dev->ev4})
         if (ev) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : dev->fork_ev) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : dev->join_ev) cudaEventDestroy(ev);
+    if (dev->aux) cudaStreamDestroy(dev->aux);
     if (dev->own_stream) cudaStreamDestroy(dev->own_stream);
     delete dev;
 }
@@ -488,6 +642,14 @@ int asnn_dev_set_stream(asnn_dev* dev, void* s) {
 }
 
 void* asnn_dev_get_stream(asnn_dev* dev) { return dev ? dev->stream : nullptr; }
+
+int asnn_dev_set_heavy_threshold(asnn_dev* dev, uint32_t min_in_degree) {
+    if (!dev) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    dev->heavy_threshold = min_in_degree;
+    ++dev->option_epoch;
+    return ASNN_OK;
+}
 
 int asnn_dev_synchronize(asnn_dev* dev) {
     if (!dev) return ASNN_E_INVALID;

@@ -81,13 +81,24 @@ struct asnn_dev {
     int sm_count = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;  // heavy-row branch of each level (fork/join)
+    std::vector<cudaEvent_t> fork_ev, join_ev;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr, ev4 = nullptr;
     std::recursive_mutex mu;
     std::string err;
+    uint32_t heavy_threshold = 128;  // in-degree above which rows stream through k_heavy
+    uint32_t option_epoch = 0;       // bumps invalidate cached sweep graphs
     asnn_timings timings{};
 };
 
 namespace asnn_b200 {
+
+// In-degree thresholds above which a row goes to the streamed heavy kernel.
+constexpr int kNumHeavyThr = 9;
+__host__ __device__ constexpr uint32_t heavy_thr(int t) {
+    return t == 0 ? 16u : t == 1 ? 32u : t == 2 ? 64u : t == 3 ? 128u : t == 4 ? 256u
+         : t == 5 ? 512u : t == 6 ? 1024u : t == 7 ? 4096u : 0xFFFFFFFFu;
+}
 
 // One network inside a layout (a population holds many).
 struct NetMeta {
@@ -113,6 +124,7 @@ struct SweepGraph {
     float* out = nullptr;
     float* state = nullptr;
     cudaStream_t stream = nullptr;
+    uint32_t epoch = 0;
     void reset() {
         if (exec) cudaGraphExecDestroy(exec);
         exec = nullptr;
@@ -129,6 +141,7 @@ struct asnn_dev_layout {
     uint32_t max_width = 0, max_deg = 0;
     uint64_t total_edges = 0, dropped = 0;
     std::vector<uint32_t> lvl_off;  // sched offsets per global level, [n_levels + 1]
+    std::vector<uint32_t> heavy_cnt;  // [kNumHeavyThr][n_levels + 1] rows above heavy_thr(t)
 
     asnn_b200::DevBuf<uint32_t> row_ptr;    // [total_pos + 1]
     asnn_b200::DevBuf<uint2> edges;         // [total_edges] {src pos, w bits}

@@ -127,6 +127,127 @@ k_level(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
     store_cols<V>(A + static_cast<uint64_t>(node) * ldA + col, out);
 }
 
+// ---------------------------------------------------------------------------
+// K-act-heavy: one CTA per (high in-degree node, column tile).  The serial
+// fp32 sum of a node cannot be split without changing its rounding, so the
+// row is streamed instead: a producer warp issues one TMA bulk copy
+// (cp.async.bulk, complete_tx on an mbarrier) per predecessor row into a ring
+// of shared-memory stages -- hundreds of rows in flight -- and one consumer
+// thread per batch column runs the reference's in-order mul-then-add chain out
+// of shared memory (~4 cycles per edge, the FADD latency).  Heavy rows thus
+// cost their dependent-add chain, not d round trips to HBM.
+namespace heavy {
+constexpr int kRows = 32;    // rows per stage (one per producer lane)
+constexpr int kStages = 12;  // ring depth: 384 rows in flight
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+}  // namespace heavy
+
+// TC = columns per tile (a multiple of 4 between 4 and 128); block = 32 + TC
+// threads rounded up to warps; dynamic smem = stages x rows x TC floats + w.
+template <int TC>
+__global__ void __launch_bounds__(32 + (TC < 32 ? 32 : TC))
+k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, float* __restrict__ A,
+        uint32_t ldA, const uint32_t* __restrict__ sched, uint32_t tiles) {
+    using namespace heavy;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* ring = reinterpret_cast<float*>(smem);                         // [S][R][TC]
+    float* wts = ring + kStages * kRows * TC;                             // [S][R]
+    uint64_t* full = reinterpret_cast<uint64_t*>(wts + kStages * kRows);  // [S]
+    uint64_t* empty = full + kStages;                                     // [S]
+    constexpr int kConsumerWarps = (TC + 31) / 32;
+
+    const uint32_t item = blockIdx.x;
+    const uint32_t node = sched[item / tiles];
+    const uint32_t tile = item % tiles;
+    const uint32_t beg = row_ptr[node], end = row_ptr[node + 1];
+    const uint32_t n_chunks = (end - beg + kRows - 1) / kRows;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        // ---- producer warp ----
+        const float* base = A + static_cast<uint64_t>(tile) * TC;
+        constexpr uint32_t kRowBytes = TC * 4;
+        uint2 cur = make_uint2(0u, 0u), nxt = make_uint2(0u, 0u);
+        if (beg + lane < end) nxt = __ldg(&edges[beg + lane]);
+        for (uint32_t c = 0; c < n_chunks; ++c) {
+            cur = nxt;
+            const uint32_t k2 = beg + (c + 1) * kRows + lane;
+            nxt = k2 < end ? __ldg(&edges[k2]) : make_uint2(0u, 0u);
+            const int s = c % kStages;
+            if (c >= kStages) mbar_wait(&empty[s], ((c / kStages) - 1) & 1);
+            const uint32_t rows = min(static_cast<uint32_t>(kRows), end - beg - c * kRows);
+            wts[s * kRows + lane] = __uint_as_float(cur.y);
+            __syncwarp();
+            if (lane == 0) mbar_expect_tx(&full[s], rows * kRowBytes);
+            __syncwarp();
+            if (static_cast<uint32_t>(lane) < rows)
+                bulk_g2s(ring + (s * kRows + lane) * TC, base + static_cast<uint64_t>(cur.x) * ldA,
+                         kRowBytes, &full[s]);
+        }
+    } else if (warp < kConsumerWarps) {
+        // ---- consumers: thread = one batch column of the tile ----
+        const int col = threadIdx.x;
+        float acc = 0.0f;
+        for (uint32_t c = 0; c < n_chunks; ++c) {
+            const int s = c % kStages;
+            mbar_wait(&full[s], (c / kStages) & 1);
+            const uint32_t rows = min(static_cast<uint32_t>(kRows), end - beg - c * kRows);
+            const float* r = ring + s * kRows * TC;
+            const float* ws = wts + s * kRows;
+            if (col < TC) {
+                if (rows == kRows) {
+#pragma unroll
+                    for (int j = 0; j < kRows; ++j) acc = mac(acc, ws[j], r[j * TC + col]);
+                } else {
+                    for (uint32_t j = 0; j < rows; ++j) acc = mac(acc, ws[j], r[j * TC + col]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        if (col < TC) A[static_cast<uint64_t>(node) * ldA + tile * TC + col] = sigmoid32(acc);
+    }
+}
+
 __global__ void k_sigmoid_many(const float* __restrict__ x, float* __restrict__ y, uint64_t n) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) y[i] = sigmoid32(x[i]);

@@ -197,3 +197,27 @@ def test_self_consistency(oracle):
         # the oracle's sigmoid is glibc's; allow the rare last-bit exp flip
         assert (rec.view(np.uint32) == vals.view(np.uint32)).mean() >= 0.999
         assert rel_close(rec, vals).all()
+
+
+# --- the streamed heavy-row kernel (k_heavy) ------------------------------------------
+@pytest.mark.parametrize("B", [4, 8, 16, 32, 64, 100, 128, 256])
+@pytest.mark.parametrize("thr", [16, 64])
+def test_heavy_rows_bitwise(oracle, B, thr):
+    """Power-law rows routed through the TMA-fed heavy kernel give the same
+    values as the light kernel and the oracle (same summation order)."""
+    net = A.generate_powerlaw(6000, 12, 32, 16, 150_000, 2.1, 11)
+    d = oracle.layout(net)
+    dl = A.DeviceLayout.from_network(net)
+    X = np.random.default_rng(B).uniform(-2, 2, (B, len(net.inputs))).astype(np.float32)
+    dev = A.Device.get(0)
+    try:
+        dev.set_heavy_threshold(thr)
+        _, st_heavy = dl.activate(X, outputs=False, state=True)
+        dev.set_heavy_threshold(None)
+        _, st_light = dl.activate(X, outputs=False, state=True)
+    finally:
+        dev.set_heavy_threshold(128)
+    assert bitwise_equal(st_heavy, st_light)
+    stats = {}
+    check_close(st_heavy, oracle.eval_batch(d, X), stats)
+    assert stats["eq"] / stats["n"] >= 0.999

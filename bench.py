@@ -298,6 +298,9 @@ def run_ours(args, cfg):
     # dominant kernel's roofline: median over 3 profiled sweeps
     prof = np.median(np.stack([dl.profile(x_dev.data_ptr(), B, out_dev.data_ptr())
                                for _ in range(3)]), axis=0)
+    if os.environ.get("ASNN_BENCH_DIAG") and rank == 0:
+        pathlib.Path(os.environ["ASNN_BENCH_DIAG"]).write_text(json.dumps(
+            {"launch_ms": [float(v) for v in prof], "info": info, "ms_per_step": ms}))
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -123,7 +123,7 @@ int asnn_dev_set_stream(asnn_dev* dev, void* cuda_stream);
 void* asnn_dev_get_stream(asnn_dev* dev);
 int asnn_dev_synchronize(asnn_dev* dev);
 /* Rows with more predecessors than this stream through the TMA-staged heavy
- * kernel (default 128, or $ASNN_HEAVY_THRESHOLD; 0xFFFFFFFF = never).
+ * kernel (default 512, or $ASNN_HEAVY_THRESHOLD; 0xFFFFFFFF = never).
  * Numerics are identical either way; this is a scheduling knob. */
 int asnn_dev_set_heavy_threshold(asnn_dev* dev, uint32_t min_in_degree);
 int asnn_dev_last_timings(const asnn_dev* dev, asnn_timings* out);

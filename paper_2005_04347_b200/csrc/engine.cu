@@ -221,7 +221,7 @@ HeavyLaunch heavy_launch() {
                              static_cast<int>(smem));
         configured = true;
     }
-    return {k_heavy<TC>, 32u + (TC < 32 ? 32u : static_cast<uint32_t>(TC)), smem, 1};
+    return {k_heavy<TC>, 32u * heavy::kProducers + (TC < 32 ? 32u : static_cast<uint32_t>(TC)), smem, 1};
 }
 
 // Rows must be >= 16 bytes for a bulk copy: no heavy path below 4 columns.
@@ -250,12 +250,12 @@ int heavy_index_for(uint32_t want) {
     return -1;
 }
 
-// Default: ASNN_HEAVY_THRESHOLD (an in-degree, or "off"), else 128.
+// Default: ASNN_HEAVY_THRESHOLD (an in-degree, or "off"), else 512.
 uint32_t default_heavy_threshold() {
     const char* s = getenv("ASNN_HEAVY_THRESHOLD");
     if (s && std::string(s) == "off") return 0xFFFFFFFFu;
     if (s) return static_cast<uint32_t>(strtoul(s, nullptr, 10));
-    return 128;
+    return 512;
 }
 
 }  // namespace

@@ -86,7 +86,7 @@ struct asnn_dev {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr, ev4 = nullptr;
     std::recursive_mutex mu;
     std::string err;
-    uint32_t heavy_threshold = 128;  // in-degree above which rows stream through k_heavy
+    uint32_t heavy_threshold = 512;  // in-degree above which rows stream through k_heavy
     uint32_t option_epoch = 0;       // bumps invalidate cached sweep graphs
     asnn_timings timings{};
 };

@@ -130,26 +130,24 @@ k_level(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
 // ---------------------------------------------------------------------------
 // K-act-heavy: one CTA per (high in-degree node, column tile).  The serial
 // fp32 sum of a node cannot be split without changing its rounding, so the
-// row is streamed instead: a producer warp issues one TMA bulk copy
-// (cp.async.bulk, complete_tx on an mbarrier) per predecessor row into a ring
-// of shared-memory stages -- hundreds of rows in flight -- and one consumer
-// thread per batch column runs the reference's in-order mul-then-add chain out
-// of shared memory (~4 cycles per edge, the FADD latency).  Heavy rows thus
-// cost their dependent-add chain, not d round trips to HBM.
+// row is streamed instead: two producer warps copy predecessor rows with
+// cp.async (LDGSTS, 16 bytes per lane, completion signalled on an mbarrier
+// per stage) into a ring of shared-memory stages -- hundreds of rows in
+// flight -- and one consumer thread per batch column runs the reference's
+// in-order mul-then-add chain out of shared memory (~4 cycles per edge, the
+// FADD latency).  Heavy rows thus cost their dependent-add chain, not d round
+// trips to HBM.  (One TMA bulk copy per 256-byte row measured ~70 cycles per
+// row per SM on B200, 17x slower than LDGSTS for this row size.)
 namespace heavy {
-constexpr int kRows = 32;    // rows per stage (one per producer lane)
-constexpr int kStages = 12;  // ring depth: 384 rows in flight
+constexpr int kRows = 32;     // rows per stage
+constexpr int kStages = 12;   // ring depth: 384 rows in flight
+constexpr int kProducers = 2; // producer warps (stage c belongs to warp c % 2)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-                 "r"(bytes)
-                 : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
@@ -163,19 +161,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// Arrives on `b` once all of this thread's prior cp.async have landed.
+__device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 }  // namespace heavy
 
-// TC = columns per tile (a multiple of 4 between 4 and 128); block = 32 + TC
-// threads rounded up to warps; dynamic smem = stages x rows x TC floats + w.
+// TC = columns per tile (4..128, a multiple of 4); block = 64 producer threads
+// + max(TC, 32) consumers; dynamic smem = stages x rows x (TC + 1) floats.
 template <int TC>
-__global__ void __launch_bounds__(32 + (TC < 32 ? 32 : TC))
+__global__ void __launch_bounds__(32 * heavy::kProducers + (TC < 32 ? 32 : TC))
 k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, float* __restrict__ A,
         uint32_t ldA, const uint32_t* __restrict__ sched, uint32_t tiles) {
     using namespace heavy;
@@ -185,6 +183,7 @@ k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, f
     uint64_t* full = reinterpret_cast<uint64_t*>(wts + kStages * kRows);  // [S]
     uint64_t* empty = full + kStages;                                     // [S]
     constexpr int kConsumerWarps = (TC + 31) / 32;
+    constexpr int kPieces = TC / 4;  // 16-byte pieces per row
 
     const uint32_t item = blockIdx.x;
     const uint32_t node = sched[item / tiles];
@@ -195,35 +194,57 @@ k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, f
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 33);  // 32 cp.async arrivals + the weights arrive
             mbar_init(&empty[s], kConsumerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    if (warp == kConsumerWarps) {
-        // ---- producer warp ----
+    if (warp >= kConsumerWarps) {
+        // ---- producer warps: chunk c belongs to warp kConsumerWarps + c % kProducers ----
+        const int p = warp - kConsumerWarps;
         const float* base = A + static_cast<uint64_t>(tile) * TC;
-        constexpr uint32_t kRowBytes = TC * 4;
-        uint2 cur = make_uint2(0u, 0u), nxt = make_uint2(0u, 0u);
-        if (beg + lane < end) nxt = __ldg(&edges[beg + lane]);
-        for (uint32_t c = 0; c < n_chunks; ++c) {
-            cur = nxt;
-            const uint32_t k2 = beg + (c + 1) * kRows + lane;
-            nxt = k2 < end ? __ldg(&edges[k2]) : make_uint2(0u, 0u);
-            const int s = c % kStages;
-            if (c >= kStages) mbar_wait(&empty[s], ((c / kStages) - 1) & 1);
-            const uint32_t rows = min(static_cast<uint32_t>(kRows), end - beg - c * kRows);
-            wts[s * kRows + lane] = __uint_as_float(cur.y);
-            __syncwarp();
-            if (lane == 0) mbar_expect_tx(&full[s], rows * kRowBytes);
-            __syncwarp();
-            if (static_cast<uint32_t>(lane) < rows)
-                bulk_g2s(ring + (s * kRows + lane) * TC, base + static_cast<uint64_t>(cur.x) * ldA,
-                         kRowBytes, &full[s]);
+        constexpr int kAhead = 8;  // this warp's chunks whose edges are in flight
+        uint2 pre[kAhead];
+#pragma unroll
+        for (int i = 0; i < kAhead; ++i) {
+            const uint32_t k = beg + (p + i * kProducers) * kRows + lane;
+            pre[i] = k < end ? __ldg(&edges[k]) : make_uint2(0u, 0u);
         }
-    } else if (warp < kConsumerWarps) {
+        for (uint32_t i0 = 0;; i0 += kAhead) {
+            bool done = false;
+#pragma unroll
+            for (int i = 0; i < kAhead; ++i) {
+                const uint32_t c = p + (i0 + i) * kProducers;
+                if (c >= n_chunks) {
+                    done = true;
+                    break;
+                }
+                const uint2 cur = pre[i];
+                const uint32_t k = beg + (c + kAhead * kProducers) * kRows + lane;
+                pre[i] = k < end ? __ldg(&edges[k]) : make_uint2(0u, 0u);
+                const int s = c % kStages;
+                if (c >= kStages) mbar_wait(&empty[s], ((c / kStages) - 1) & 1);
+                const uint32_t rows = min(static_cast<uint32_t>(kRows), end - beg - c * kRows);
+                float* dst = ring + s * kRows * TC;
+#pragma unroll
+                for (int j = 0; j < kPieces; ++j) {
+                    const int q = j * 32 + lane;    // piece index within the stage
+                    const int r = q / kPieces;      // row
+                    const int pc = q - r * kPieces; // 16-byte piece of the row
+                    const uint32_t col = __shfl_sync(0xFFFFFFFFu, cur.x, r);
+                    if (static_cast<uint32_t>(r) < rows)
+                        cp_async16(dst + r * TC + pc * 4, base + static_cast<uint64_t>(col) * ldA + pc * 4);
+                }
+                cp_async_arrive(&full[s]);
+                wts[s * kRows + lane] = __uint_as_float(cur.y);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[s]);
+            }
+            if (done) break;
+        }
+    } else {
         // ---- consumers: thread = one batch column of the tile ----
         const int col = threadIdx.x;
         float acc = 0.0f;

@@ -216,7 +216,7 @@ def test_heavy_rows_bitwise(oracle, B, thr):
         dev.set_heavy_threshold(None)
         _, st_light = dl.activate(X, outputs=False, state=True)
     finally:
-        dev.set_heavy_threshold(128)
+        dev.set_heavy_threshold(512)
     assert bitwise_equal(st_heavy, st_light)
     stats = {}
     check_close(st_heavy, oracle.eval_batch(d, X), stats)

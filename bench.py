@@ -403,6 +403,26 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_ncu_sweeps(args, cfg):
+    """Layout build + N plain sweeps (no graph, no timing): the command the
+    committed ncu launch lists and captures in profiles/ were taken with."""
+    import torch
+    import paper_2005_04347_b200 as A
+    nets = make_network(cfg, args.scale)
+    B = CONFIGS[cfg][1]
+    rng = np.random.default_rng(12345)
+    X = np.concatenate([rng.uniform(-2, 2, (B, len(n.inputs))).astype(np.float32).reshape(-1)
+                        for n in nets])
+    dl = (A.DeviceLayout.from_population(nets) if cfg == "c5"
+          else A.DeviceLayout.from_network(nets[0]))
+    x_dev = torch.from_numpy(X).cuda()
+    out_dev = torch.empty(dl.info()["n_outputs"] * B, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(args.ncu_sweeps):
+        dl.profile(x_dev.data_ptr(), B, out_dev.data_ptr())
+    torch.cuda.synchronize()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -416,9 +436,14 @@ def main():
     ap.add_argument("--prep", default="device", choices=["device", "upload"],
                     help="device: compute_required/segment/flatten on the GPU; upload: "
                          "asnn_dev_upload_layout of the generator's banded layout")
+    ap.add_argument("--ncu-sweeps", type=int, default=0,
+                    help="profiling helper: build the layout, run this many sweeps, print "
+                         "nothing else (for ncu launch lists; never a bench number)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    if args.impl == "reference":
+    if args.ncu_sweeps:
+        run_ncu_sweeps(args, args.config)
+    elif args.impl == "reference":
         run_reference(args, args.config)
     else:
         run_ours(args, args.config)

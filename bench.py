@@ -149,9 +149,13 @@ def measured_peak():
 
 
 def profiled_traffic(cfg):
+    """DRAM bytes per sweep from the committed ncu launch list (same unit as
+    alg_bytes_per_step), or None when this config was not captured."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
-        return json.loads(p.read_text()).get(cfg)
+        e = json.loads(p.read_text()).get(cfg)
+        if e:
+            return e["dram_bytes_per_step"]
     return None
 
 

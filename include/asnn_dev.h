@@ -126,6 +126,11 @@ int asnn_dev_synchronize(asnn_dev* dev);
  * kernel (default 512, or $ASNN_HEAVY_THRESHOLD; 0xFFFFFFFF = never).
  * Numerics are identical either way; this is a scheduling knob. */
 int asnn_dev_set_heavy_threshold(asnn_dev* dev, uint32_t min_in_degree);
+/* Sweep strategy: 0 = automatic (default, $ASNN_SWEEP_MODE), 1 = one launch
+ * per dependency level, 2 = one CTA per (network, batch slice) running every
+ * level with shared-memory-resident activations whenever they fit.  Also a
+ * scheduling knob: results are identical. */
+int asnn_dev_set_sweep_mode(asnn_dev* dev, uint32_t mode);
 int asnn_dev_last_timings(const asnn_dev* dev, asnn_timings* out);
 
 /* ---- preprocessing (GPU) ------------------------------------------------

@@ -77,6 +77,7 @@ PROTOTYPES = {
     "asnn_dev_get_stream": (C.c_void_p, [C.c_void_p]),
     "asnn_dev_synchronize": (C.c_int, [C.c_void_p]),
     "asnn_dev_set_heavy_threshold": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "asnn_dev_set_sweep_mode": (C.c_int, [C.c_void_p, C.c_uint32]),
     "asnn_dev_last_timings": (C.c_int, [C.c_void_p, C.POINTER(Timings)]),
     "asnn_dev_compute_required": (C.c_int, [C.c_void_p, C.POINTER(NetworkDesc), u8p]),
     "asnn_dev_segment": (C.c_int, [C.c_void_p, C.POINTER(NetworkDesc), u8p, u32p, u32p]),

@@ -298,6 +298,10 @@ class Device:
     def synchronize(self):
         self.check(self.lib.asnn_dev_synchronize(self.h))
 
+    def set_sweep_mode(self, mode: int):
+        """0 automatic, 1 one launch per level, 2 one CTA per (network, slice)."""
+        self.check(self.lib.asnn_dev_set_sweep_mode(self.h, int(mode)))
+
     def set_heavy_threshold(self, min_in_degree: Optional[int]):
         """Rows above this in-degree use the streamed heavy kernel (None = off)."""
         v = 0xFFFFFFFF if min_in_degree is None else int(min_in_degree)

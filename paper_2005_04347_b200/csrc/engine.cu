@@ -169,6 +169,16 @@ __global__ void k_heavy_counts(const uint32_t* __restrict__ keys, uint32_t n, ui
         if (deg > heavy_thr(t)) atomicAdd(&hv[t * stride + lv], 1u);
 }
 
+// le_cat[j] = row_ptr[pos_base(g) + lo_cat[j]] for the network g owning j.
+__global__ void k_layer_edges(const uint32_t* __restrict__ lo_cat, const uint32_t* __restrict__ lo_base,
+                              uint32_t G, const uint32_t* __restrict__ pos_base,
+                              const uint32_t* __restrict__ row_ptr, uint32_t n, uint32_t* __restrict__ le) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint32_t g = find_seg(lo_base, G, j);
+    le[j] = row_ptr[pos_base[g] + lo_cat[j]];
+}
+
 __global__ void k_row64_to_32(const uint64_t* __restrict__ in, uint32_t n, uint32_t* __restrict__ out) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = static_cast<uint32_t>(in[i]);
@@ -256,6 +266,49 @@ uint32_t default_heavy_threshold() {
     if (s && std::string(s) == "off") return 0xFFFFFFFFu;
     if (s) return static_cast<uint32_t>(strtoul(s, nullptr, 10));
     return 512;
+}
+
+// K-cta launch plan for a padded batch width: the largest power-of-two column
+// slice whose activations (plus the staged edge buffers) fit in shared memory.
+struct CtaPlan {
+    bool use = false;
+    uint32_t C = 0, V = 1, T = 32, smem = 0, EB = 0, RB = 0;
+};
+
+constexpr uint32_t kMaxDynSmem = 227 * 1024;
+
+CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
+    CtaPlan p;
+    const uint32_t mode = L->dev->sweep_mode;  // 0 auto, 1 layer launches, 2 K-cta when it fits
+    if (mode == 1) return p;
+    if (L->n_levels < 2 || L->max_pos == 0) return p;
+    p.RB = std::min<uint32_t>(L->max_width + 1, 4096);
+    p.EB = std::min<uint32_t>(std::max<uint32_t>(L->max_level_edges, 1), 4096);
+    const uint32_t cmax = std::min<uint32_t>(ldA, 128);
+    for (uint32_t C = cmax; C >= 1; C >>= 1) {
+        if (ldA % C) continue;
+        uint32_t eb = p.EB;
+        uint64_t sm = static_cast<uint64_t>(L->max_pos) * C * 4 + 2ull * eb * 8 + 2ull * p.RB * 4;
+        while (sm > kMaxDynSmem && eb > 64) {  // stage fewer edges; big layers read global
+            eb /= 2;
+            sm = static_cast<uint64_t>(L->max_pos) * C * 4 + 2ull * eb * 8 + 2ull * p.RB * 4;
+        }
+        if (sm <= kMaxDynSmem) {
+            p.C = C;
+            p.EB = eb;
+            p.smem = static_cast<uint32_t>(sm);
+            break;
+        }
+        if (C == 1) break;
+    }
+    if (!p.C) return p;
+    p.V = p.C >= 4 ? 4 : 1;
+    const uint64_t items = static_cast<uint64_t>(L->max_width) * (p.C / p.V);
+    p.T = static_cast<uint32_t>(std::min<uint64_t>(256, std::max<uint64_t>(32, (items + 31) / 32 * 32)));
+    const bool latency_bound = L->nets.size() > 1 || L->n_levels >= 24 ||
+                               L->total_edges * static_cast<uint64_t>(ldA) <= (1ull << 22);
+    p.use = mode == 2 || latency_bound;
+    return p;
 }
 
 }  // namespace
@@ -405,7 +458,43 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
         CKL(cudaGetLastError());
         L->heavy_cnt.assign(nh, 0);
         CKL(cudaMemcpyAsync(L->heavy_cnt.data(), hv.p, nh * 4, cudaMemcpyDeviceToHost, st));
+
+        // K-cta metadata: per-network records and layer boundaries as edge offsets
+        std::vector<uint32_t> recs(static_cast<size_t>(G) * 12, 0);
+        uint32_t sens = 0;
+        for (uint32_t g = 0; g < G; ++g) {
+            const NetMeta& n = nets[g];
+            uint32_t* r = &recs[static_cast<size_t>(g) * 12];
+            r[0] = n.pos_base;
+            r[1] = n.n_pos;
+            r[2] = n.n_sensors;
+            r[3] = sens;
+            r[4] = n.in_prefix;
+            r[5] = n.n_in;
+            r[6] = n.out_prefix;
+            r[7] = n.n_out;
+            r[8] = lo_base[g];
+            r[9] = n.n_layers;
+            sens += n.n_sensors;
+            L->max_pos = std::max(L->max_pos, n.n_pos);
+        }
+        CKL(L->cta_nets.alloc(recs.size()));
+        CKL(cudaMemcpyAsync(L->cta_nets.p, recs.data(), recs.size() * 4, cudaMemcpyHostToDevice, st));
+        CKL(L->le_cat.alloc(lo_cat.size() + 1));
+        if (!lo_cat.empty())
+            k_layer_edges<<<blocks_for(lo_cat.size()), kThreads, 0, st>>>(
+                d_lo.p, d_lob.p, G, m.pos, flat.row_ptr.p, static_cast<uint32_t>(lo_cat.size()),
+                L->le_cat.p);
+        CKL(cudaGetLastError());
+        std::vector<uint32_t> le(lo_cat.size());
+        if (!le.empty())
+            CKL(cudaMemcpyAsync(le.data(), L->le_cat.p, le.size() * 4, cudaMemcpyDeviceToHost, st));
         CKL(cudaStreamSynchronize(st));
+        for (uint32_t g = 0; g < G; ++g)
+            for (uint32_t l = 0; l < nets[g].n_layers; ++l)
+                L->max_level_edges =
+                    std::max(L->max_level_edges, le[lo_base[g] + l + 1] - le[lo_base[g] + l]);
+        L->lo_cat = std::move(d_lo);
     }
     CKL(L->idb_prefix.alloc(G + 1));
     CKL(cudaMemcpyAsync(L->idb_prefix.p, d_meta.p + (G + 1), (G + 1) * 4, cudaMemcpyDeviceToDevice,
@@ -432,6 +521,15 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
 // ---------------------------------------------------------------------------
 namespace {
 
+template <typename Mark>
+int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark);
+
+#define RC_(expr)          \
+    do {                   \
+        int _r = (expr);   \
+        if (_r) return _r; \
+    } while (0)
+
 // One activation sweep, stream-ordered: sensors, every level, outputs, state.
 int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out, float* state,
                  cudaStream_t st, std::vector<cudaEvent_t>* evs = nullptr) {
@@ -442,9 +540,40 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         if (evs && ek < evs->size()) cudaEventRecord((*evs)[ek++], st);
     };
     mark();
-    if (L->total_sensors)
-        k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(
-            L->sinfo.p, L->total_sensors, x, n_vec, L->A.p, ldA);
+    const CtaPlan cp = cta_plan(L, ldA);
+    if (cp.use) {
+        // the whole sweep (sensors + every layer) of each (network, slice) in one CTA
+        auto fn = cp.V == 4 ? k_cta<4> : k_cta<1>;
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(cp.smem)));
+        fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T, cp.smem, st>>>(
+            reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->le_cat.p, L->row_ptr.p,
+            L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos, cp.EB, cp.RB,
+            state ? 1 : 0);
+    } else {
+        if (L->total_sensors)
+            k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(
+                L->sinfo.p, L->total_sensors, x, n_vec, L->A.p, ldA);
+        RC_(launch_levels(L, ldA, st, mark));
+    }
+    if (out && L->total_out) {
+        mark();
+        k_gather_out<<<blocks_for(static_cast<uint64_t>(L->total_out) * n_vec), kThreads, 0, st>>>(
+            L->oinfo.p, L->total_out, L->A.p, ldA, n_vec, out);
+    }
+    mark();
+    if (state && L->total_idb)
+        k_state<<<blocks_for(static_cast<uint64_t>(L->total_idb) * n_vec), kThreads, 0, st>>>(
+            L->state_map.p, L->idb_prefix.p, static_cast<uint32_t>(L->nets.size()), L->total_idb,
+            L->A.p, ldA, n_vec, state);
+    CK(cudaGetLastError());
+    return ASNN_OK;
+}
+
+// Per-layer launches (k_level, plus k_heavy on the aux branch for heavy rows).
+template <typename Mark>
+int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark) {
+    asnn_dev* dev = L->dev;
     const LevelLaunch ll = level_launch_for(ldA);
     const HeavyLaunch hl = heavy_launch_for(ldA);
     const int thr = heavy_index_for(dev->heavy_threshold);
@@ -481,16 +610,6 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
             CK(cudaStreamWaitEvent(st, dev->join_ev[l], 0));
         }
     }
-    if (out && L->total_out) {
-        mark();
-        k_gather_out<<<blocks_for(static_cast<uint64_t>(L->total_out) * n_vec), kThreads, 0, st>>>(
-            L->oinfo.p, L->total_out, L->A.p, ldA, n_vec, out);
-    }
-    mark();
-    if (state && L->total_idb)
-        k_state<<<blocks_for(static_cast<uint64_t>(L->total_idb) * n_vec), kThreads, 0, st>>>(
-            L->state_map.p, L->idb_prefix.p, static_cast<uint32_t>(L->nets.size()), L->total_idb,
-            L->A.p, ldA, n_vec, state);
     CK(cudaGetLastError());
     return ASNN_OK;
 }
@@ -610,6 +729,7 @@ int asnn_dev_open(int device, asnn_dev** out) {
     }
     dev->stream = dev->own_stream;
     dev->heavy_threshold = default_heavy_threshold();
+    if (const char* m = getenv("ASNN_SWEEP_MODE")) dev->sweep_mode = static_cast<uint32_t>(atoi(m)) % 3;
     if (cudaStreamCreateWithFlags(&dev->aux, cudaStreamNonBlocking) != cudaSuccess) {
         cudaGetLastError();
         delete dev;
@@ -642,6 +762,14 @@ int asnn_dev_set_stream(asnn_dev* dev, void* s) {
 }
 
 void* asnn_dev_get_stream(asnn_dev* dev) { return dev ? dev->stream : nullptr; }
+
+int asnn_dev_set_sweep_mode(asnn_dev* dev, uint32_t mode) {
+    if (!dev || mode > 2) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    dev->sweep_mode = mode;
+    ++dev->option_epoch;
+    return ASNN_OK;
+}
 
 int asnn_dev_set_heavy_threshold(asnn_dev* dev, uint32_t min_in_degree) {
     if (!dev) return ASNN_E_INVALID;
@@ -849,8 +977,13 @@ int asnn_dev_profile_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_ve
 int asnn_dev_activate_plan(asnn_dev_layout* L, uint32_t n_vec, uint32_t* kernels, uint64_t* alg_bytes,
                            uint64_t* conn_evals) {
     if (!L) return ASNN_E_INVALID;
-    uint32_t k = L->total_sensors ? 1 : 0;
-    for (uint32_t l = 1; l < L->n_levels; ++l) k += (L->lvl_off[l + 1] > L->lvl_off[l]);
+    uint32_t k = 0;
+    if (cta_plan(L, padded_batch(n_vec)).use) {
+        k = 1;  // K-cta runs sensors and every layer
+    } else {
+        k = L->total_sensors ? 1 : 0;
+        for (uint32_t l = 1; l < L->n_levels; ++l) k += (L->lvl_off[l + 1] > L->lvl_off[l]);
+    }
     k += L->total_out ? 1 : 0;
     if (kernels) *kernels = k;
     const uint64_t B = n_vec, E = L->total_edges, N = L->total_pos;

@@ -87,6 +87,7 @@ struct asnn_dev {
     std::recursive_mutex mu;
     std::string err;
     uint32_t heavy_threshold = 512;  // in-degree above which rows stream through k_heavy
+    uint32_t sweep_mode = 0;         // 0 auto, 1 per-layer launches, 2 K-cta when it fits
     uint32_t option_epoch = 0;       // bumps invalidate cached sweep graphs
     asnn_timings timings{};
 };
@@ -157,6 +158,13 @@ struct asnn_dev_layout {
     asnn_b200::DevBuf<float> x_stage, out_stage;
     asnn_b200::PinnedBuf pin_x, pin_out;
     asnn_b200::SweepGraph graph;
+
+    // K-cta (whole sweep in one CTA per network x column slice)
+    asnn_b200::DevBuf<uint32_t> cta_nets;  // [n_nets][12] CtaNet records
+    asnn_b200::DevBuf<uint32_t> lo_cat;    // per net: layer offsets (local positions)
+    asnn_b200::DevBuf<uint32_t> le_cat;    // per net: layer offsets as global edge indices
+    uint32_t max_pos = 0;                  // largest network (positions)
+    uint32_t max_level_edges = 0;          // most edges into one layer of one network
 
     ~asnn_dev_layout() { graph.reset(); }
 };

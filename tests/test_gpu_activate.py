@@ -20,6 +20,16 @@ pytestmark = pytest.mark.gpu
 DEV = A.ParallelConfig(backend=A.Backend.DeviceCompute)
 
 
+@pytest.fixture(params=[1, 2], ids=["layer-launches", "k_cta"])
+def sweep_mode(request):
+    """Run a test under both sweep strategies: one launch per dependency level
+    (k_level/k_heavy) and the one-CTA-per-slice sweep (k_cta)."""
+    dev = A.Device.get(0)
+    dev.set_sweep_mode(request.param)
+    yield request.param
+    dev.set_sweep_mode(0)
+
+
 def to_layout(d: dict, outputs=()) -> A.LayeredLayout:
     return A.LayeredLayout(d["total_layers"], d["layer_offsets"], d["node_ids"], d["row_ptr"],
                            d["in_nodes"], d["in_weights"], d["input_order"],
@@ -116,7 +126,7 @@ def test_layer_slice_and_width(oracle):
 
 
 # --- the reference's verify corpus (golden op arrays from the reference) ----------------
-def test_verify_corpus_against_reference_golden(oracle, verify_corpus):
+def test_verify_corpus_against_reference_golden(oracle, verify_corpus, sweep_mode):
     stats = {}
     for case in verify_corpus:
         net = A.generate(case["spec"])
@@ -126,7 +136,7 @@ def test_verify_corpus_against_reference_golden(oracle, verify_corpus):
     assert stats["eq"] / stats["n"] >= 0.999, stats
 
 
-def test_adversarial_against_reference_golden(oracle, adversarial_nets):
+def test_adversarial_against_reference_golden(oracle, adversarial_nets, sweep_mode):
     stats = {}
     for case in adversarial_nets:
         if not case["flatten_ok"]:
@@ -139,7 +149,7 @@ def test_adversarial_against_reference_golden(oracle, adversarial_nets):
 
 # --- batches: every padding / lane configuration -------------------------------------
 @pytest.mark.parametrize("B", [1, 2, 3, 4, 5, 8, 16, 31, 64, 100, 128, 129, 256, 300, 1024])
-def test_batch_widths(oracle, B):
+def test_batch_widths(oracle, B, sweep_mode):
     rng = A.SplitMix64(1000 + B)
     spec = A.random_spec(rng, 2000, 20000)
     net = A.generate(spec)
@@ -154,7 +164,7 @@ def test_batch_widths(oracle, B):
     assert stats["eq"] / stats["n"] >= 0.999
 
 
-def test_repeat_activation_is_deterministic(oracle):
+def test_repeat_activation_is_deterministic(oracle, sweep_mode):
     rng = A.SplitMix64(77)
     net = A.generate(A.random_spec(rng, 5000, 20000))
     d = oracle.layout(net)
@@ -183,7 +193,7 @@ def test_inject_fault_is_seen(oracle):
     check_close(after, oracle.eval_batch(d, x)[0], stats)
 
 
-def test_self_consistency(oracle):
+def test_self_consistency(oracle, sweep_mode):
     """test_eval.cpp:109-134: every value recomputes exactly from the op array."""
     rng = A.SplitMix64(52)
     for _ in range(5):
@@ -210,6 +220,7 @@ def test_heavy_rows_bitwise(oracle, B, thr):
     dl = A.DeviceLayout.from_network(net)
     X = np.random.default_rng(B).uniform(-2, 2, (B, len(net.inputs))).astype(np.float32)
     dev = A.Device.get(0)
+    dev.set_sweep_mode(1)
     try:
         dev.set_heavy_threshold(thr)
         _, st_heavy = dl.activate(X, outputs=False, state=True)
@@ -217,6 +228,7 @@ def test_heavy_rows_bitwise(oracle, B, thr):
         _, st_light = dl.activate(X, outputs=False, state=True)
     finally:
         dev.set_heavy_threshold(512)
+        dev.set_sweep_mode(0)
     assert bitwise_equal(st_heavy, st_light)
     stats = {}
     check_close(st_heavy, oracle.eval_batch(d, X), stats)

@@ -136,10 +136,12 @@ def test_deep_chain_and_wide_fan():
     assert nl == 2 and level[k] == 1
 
 
-def test_population_matches_single_networks(oracle):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_population_matches_single_networks(oracle, mode):
     rng = A.SplitMix64(5)
     nets = [A.generate(A.GenSpec(8, 4, 188, 1000, 8, seed=rng.next())) for _ in range(50)]
     pop = A.DeviceLayout.from_population(nets)
+    A.Device.get(0).set_sweep_mode(mode)
     info = pop.info()
     assert info["n_networks"] == 50
     X = np.random.default_rng(1).uniform(-2, 2, (50, 16, 8)).astype(np.float32)
@@ -156,3 +158,4 @@ def test_population_matches_single_networks(oracle):
         o = out.reshape(-1)[ko:ko + 16 * 4].reshape(16, 4)
         ko += 16 * 4
         assert bitwise_equal(o, got[:, net.outputs])
+    A.Device.get(0).set_sweep_mode(0)

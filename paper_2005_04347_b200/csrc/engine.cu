@@ -288,10 +288,11 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     for (uint32_t C = cmax; C >= 1; C >>= 1) {
         if (ldA % C) continue;
         uint32_t eb = p.EB;
-        uint64_t sm = static_cast<uint64_t>(L->max_pos) * C * 4 + 2ull * eb * 8 + 2ull * p.RB * 4;
+        const uint64_t as_bytes = (static_cast<uint64_t>(L->max_pos) * C + 3) / 4 * 16;
+        uint64_t sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4;
         while (sm > kMaxDynSmem && eb > 64) {  // stage fewer edges; big layers read global
             eb /= 2;
-            sm = static_cast<uint64_t>(L->max_pos) * C * 4 + 2ull * eb * 8 + 2ull * p.RB * 4;
+            sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4;
         }
         if (sm <= kMaxDynSmem) {
             p.C = C;

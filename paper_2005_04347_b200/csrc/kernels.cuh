@@ -293,12 +293,13 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(heavy::smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+constexpr uint32_t kRing = 4;  // staged layers (3 prefetched ahead of the one computing)
+__device__ __forceinline__ void wait_ring() { asm volatile("cp.async.wait_group 2;" ::: "memory"); }
 }  // namespace cta
 
 // lo_cat/le_cat: per network, layer boundaries as local positions and as
 // global edge offsets ([n_layers + 1] entries from lo_base).  Shared memory:
-// As[max_pos][C] | eb[2][EB] uint2 | rb[2][RB] u32.
+// As[max_pos][C] | eb[kRing][EB] uint2 | rb[kRing][RB] u32.
 template <int V>
 __global__ void __launch_bounds__(256)
 k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
@@ -309,8 +310,9 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       int write_all) {
     extern __shared__ __align__(16) unsigned char smem[];
     float* As = reinterpret_cast<float*>(smem);
-    uint2* eb = reinterpret_cast<uint2*>(As + static_cast<size_t>(max_pos) * C);
-    uint32_t* rb = reinterpret_cast<uint32_t*>(eb + 2 * EB);
+    // activations region rounded up to 16 bytes so the edge buffers stay aligned
+    uint2* eb = reinterpret_cast<uint2*>(As + ((static_cast<size_t>(max_pos) * C + 3) & ~size_t(3)));
+    uint32_t* rb = reinterpret_cast<uint32_t*>(eb + cta::kRing * EB);
     const CtaNet n = nets[blockIdx.y];
     const uint32_t c0 = blockIdx.x * C;
     const uint32_t groups = C / V;  // column groups per row
@@ -323,8 +325,8 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
         const uint32_t a = lo[l], b = lo[l + 1];
         const uint32_t e0 = le[l], e1 = le[l + 1];
         if (b - a + 1 > RB || e1 - e0 > EB) return;
-        uint32_t* rdst = rb + (l & 1) * RB;
-        uint2* edst = eb + (l & 1) * EB;
+        uint32_t* rdst = rb + (l % cta::kRing) * RB;
+        uint2* edst = eb + (l % cta::kRing) * EB;
         for (uint32_t i = tid; i <= b - a; i += T) cta::cp_async4(&rdst[i], &row_ptr[n.pos_base + a + i]);
         for (uint32_t i = tid; i < e1 - e0; i += T) cta::cp_async8(&edst[i], &edges[e0 + i]);
     };
@@ -342,19 +344,21 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
             As[s * C + q * V + v] = sigmoid32(xv);
         }
     }
-    if (n.n_layers > 1) prefetch(1);
-    cta::commit();
-    cta::wait_all();
+    // layers 1 .. kRing-1 in flight before the first one is needed; one
+    // commit group per layer so wait_group(kRing - 2) retires exactly the next
+    for (uint32_t l = 1; l < cta::kRing; ++l) {
+        if (l < n.n_layers) prefetch(l);
+        cta::commit();
+    }
+    cta::wait_ring();
     __syncthreads();
 
     for (uint32_t l = 1; l < n.n_layers; ++l) {
-        if (l + 1 < n.n_layers) prefetch(l + 1);
-        cta::commit();
         const uint32_t a = lo[l], b = lo[l + 1];
         const uint32_t e0 = le[l], e1 = le[l + 1];
         const bool staged = (b - a + 1 <= RB) && (e1 - e0 <= EB);
-        const uint32_t* R = rb + (l & 1) * RB;
-        const uint2* Ebuf = eb + (l & 1) * EB;
+        const uint32_t* R = rb + (l % cta::kRing) * RB;
+        const uint2* Ebuf = eb + (l % cta::kRing) * EB;
         for (uint32_t it = tid; it < (b - a) * groups; it += T) {
             const uint32_t i = it / groups, q = it - i * groups;
             uint32_t kb, ke;
@@ -389,7 +393,10 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
 #pragma unroll
             for (int v = 0; v < V; ++v) As[(a + i) * C + q * V + v] = sigmoid32(acc[v]);
         }
-        cta::wait_all();
+        __syncthreads();  // layer l done: its buffer may be refilled
+        if (l + cta::kRing - 1 < n.n_layers) prefetch(l + cta::kRing - 1);
+        cta::commit();
+        cta::wait_ring();  // layer l + 1 staged
         __syncthreads();
     }
 

@@ -156,10 +156,11 @@ class Oracle:
 class Ref:
     """The unmodified reference (oracle/_ref/libasnn_ref.so)."""
 
-    def __init__(self):
-        if not REF_SO.exists():
-            raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference at build time)")
-        L = C.CDLL(str(REF_SO))
+    def __init__(self, path=None):
+        so = pathlib.Path(path) if path else REF_SO
+        if not so.exists():
+            raise FileNotFoundError(f"{so} not built (needs /root/reference at build time)")
+        L = C.CDLL(str(so))
         vp = C.c_void_p
         sig = {
             "ref_generate": (vp, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
@@ -196,6 +197,7 @@ class Ref:
             "ref_eval_batch": (C.c_double, [vp, f32p, C.c_uint32, C.c_int, C.c_uint32, u32p,
                                             C.c_uint32, f32p]),
             "ref_max_threads": (C.c_int, []),
+            "ref_layout_ptr": (vp, [vp]),
             "ref_sigmoid32_many": (None, [f32p, f32p, C.c_uint64]),
         }
         for name, (res, args) in sig.items():
@@ -333,3 +335,28 @@ class RefNet:
 
 def available_ref() -> bool:
     return REF_SO.exists()
+
+
+REF_DEV_SO = HERE / "_ref" / "libasnn_ref_dev.so"
+
+
+class RefDev(Ref):
+    """The reference plus the maintainer's DeviceCompute binding
+    (integration/asnn_device_backend.cpp) linked against libasnn_b200.so."""
+
+    def __init__(self):
+        super().__init__(REF_DEV_SO)
+        self.L.ref_dev_eval.restype = C.c_int
+        self.L.ref_dev_eval.argtypes = [C.c_void_p, f32p, C.c_uint32, f32p]
+
+    def eval_device(self, rn: "RefNet", x):
+        """eval_parallel(..., DeviceCompute) on the reference's own LayeredLayout."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        out = np.zeros(self.L.ref_layout_id_bound(rn.h), np.float32)
+        rc = self.L.ref_dev_eval(self.L.ref_layout_ptr(rn.h), _p(x, C.c_float), len(x),
+                                 _p(out, C.c_float))
+        return rc, out
+
+
+def available_ref_dev() -> bool:
+    return REF_DEV_SO.exists()

@@ -352,6 +352,9 @@ double ref_eval_batch(void* hp, const float* X, std::uint32_t n_vec, int mode, s
 
 int ref_max_threads() { return omp_get_max_threads(); }
 
+// The reference LayeredLayout object of a handle (for integration/ tests).
+const void* ref_layout_ptr(void* hp) { return &static_cast<RefHandle*>(hp)->layout; }
+
 // sigmoid32 (network.hpp:54-59) over an array, for exhaustive exp checks.
 void ref_sigmoid32_many(const float* in, float* out, std::uint64_t n) {
 #pragma omp parallel for schedule(static)

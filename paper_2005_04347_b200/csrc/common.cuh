@@ -4,18 +4,25 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "exp_glibc.h"
+
 namespace asnn_b200 {
 
-// sigmoid32 of the reference (network.hpp:44-59), bit-for-bit in its
-// structure: the logistic 1/(1+exp(-4.97 x)) in double, clamped into (0,1),
-// rounded to float, clamped again.  Explicit _rn intrinsics keep every step a
-// single IEEE operation (no contraction), and the build never enables FTZ:
-// sigmoid32 returns the float denormal 0x1p-149 at negative saturation
-// (SURVEY.md 7.2-8).  exp is CUDA's double exp (<= 1 ulp); glibc's may differ
-// in the last double bit, which flips a float rounding for ~2^-29 of inputs
-// (measured in tests/test_gpu_sigmoid.py).
+// The 2^(i/128) table of exp_glibc (tools/gen_exp_table.py).
+static __device__ const uint64_t kExpTab[256] = {
+#include "exp_table.inc"
+};
+
+// sigmoid32 of the reference (network.hpp:44-59), bit for bit: the logistic
+// 1/(1+exp(-4.97 x)) in double, clamped into (0,1), rounded to float, clamped
+// again.  Explicit _rn intrinsics keep every step a single IEEE operation (no
+// contraction), the build never enables FTZ (sigmoid32 returns the float
+// denormal 0x1p-149 at negative saturation), and exp is the
+// restatement of the host glibc exp (exp_glibc.h) -- identical doubles, so
+// identical floats: checked for all 2^32 inputs (oracle/exp_check.c,
+// tests/test_gpu_sigmoid.py).
 __device__ __forceinline__ float sigmoid32(float x) {
-    const double e = exp(__dmul_rn(-4.97, static_cast<double>(x)));
+    const double e = exp_glibc(__dmul_rn(-4.97, static_cast<double>(x)), kExpTab);
     double v = __ddiv_rn(1.0, __dadd_rn(1.0, e));
     if (v <= 0.0) v = 4.9406564584124654e-324;         // DBL_TRUE_MIN
     if (v >= 1.0) v = 1.0 - 1.1102230246251565e-16;     // 1 - DBL_EPSILON/2

@@ -133,7 +133,7 @@ def test_verify_corpus_against_reference_golden(oracle, verify_corpus, sweep_mod
         d = oracle.layout(net)
         st = A.eval_parallel(to_layout(d), case["x"], DEV)
         check_close(st.outputs, case["op"], stats)
-    assert stats["eq"] / stats["n"] >= 0.999, stats
+    assert stats["eq"] == stats["n"], stats          # bitwise
 
 
 def test_adversarial_against_reference_golden(oracle, adversarial_nets, sweep_mode):
@@ -144,7 +144,7 @@ def test_adversarial_against_reference_golden(oracle, adversarial_nets, sweep_mo
         d = oracle.layout(case["net"])
         st = A.eval_parallel(to_layout(d), case["x"], DEV)
         check_close(st.outputs, case["op"], stats)
-    assert stats["eq"] / stats["n"] >= 0.999, stats
+    assert stats["eq"] == stats["n"], stats          # bitwise
 
 
 # --- batches: every padding / lane configuration -------------------------------------
@@ -161,7 +161,7 @@ def test_batch_widths(oracle, B, sweep_mode):
     stats = {}
     check_close(st, ref, stats)
     assert bitwise_equal(out, st[:, net.outputs])
-    assert stats["eq"] / stats["n"] >= 0.999
+    assert stats["eq"] == stats["n"], stats          # bitwise
 
 
 def test_repeat_activation_is_deterministic(oracle, sweep_mode):
@@ -204,9 +204,7 @@ def test_self_consistency(oracle, sweep_mode):
         vals = st.outputs[d["node_ids"]]
         assert np.all(vals > 0) and np.all(vals < 1)
         rec = oracle.recompute(d, x, st.outputs, np.arange(len(d["node_ids"])))
-        # the oracle's sigmoid is glibc's; allow the rare last-bit exp flip
-        assert (rec.view(np.uint32) == vals.view(np.uint32)).mean() >= 0.999
-        assert rel_close(rec, vals).all()
+        assert np.array_equal(rec.view(np.uint32), vals.view(np.uint32))
 
 
 # --- the streamed heavy-row kernel (k_heavy) ------------------------------------------
@@ -232,4 +230,4 @@ def test_heavy_rows_bitwise(oracle, B, thr):
     assert bitwise_equal(st_heavy, st_light)
     stats = {}
     check_close(st_heavy, oracle.eval_batch(d, X), stats)
-    assert stats["eq"] / stats["n"] >= 0.999
+    assert stats["eq"] == stats["n"], stats          # bitwise

@@ -159,69 +159,81 @@ def profiled_traffic(cfg):
     return None
 
 
+class RefCPU:
+    """The reference's own CPU evaluator (oracle/_ref: the unmodified reference
+    compiled from its sources) prepared once on the same networks; each
+    measurement times a bounded sample of input vectors of that workload.
+
+    Modes: "par" = eval_parallel with all host
+    threads, one vector at a time; "omp-seq" = an OpenMP loop of
+    eval_sequential over `threads` vectors at once.  For C5 the sample is the
+    first `max_nets` networks of the population (each with its own vectors)."""
+
+    def __init__(self, nets, X_all, cfg, max_nets=64):
+        from oracle.bind import Oracle, Ref, available_ref
+        self.kind = "reference" if available_ref() else "port"
+        self.ref = Ref() if self.kind == "reference" else None
+        self.oracle = None if self.ref else Oracle()
+        self.threads = self.ref.L.ref_max_threads() if self.ref else 1
+        self.items = []
+        for gi, net in enumerate(nets[:max_nets]):
+            if cfg in ("c2", "c4"):
+                # reference preprocessing of C4 takes ~20 min (SURVEY 7.2-6):
+                # build its LayeredLayout straight from the banded CSR instead
+                lay = host_layout_banded(cfg, net)
+                h = self.ref.layout_from_csr(lay) if self.ref else lay
+            elif self.ref:
+                h = self.ref.network(net)
+                assert h.preprocess() == 0
+            else:
+                h = self.oracle.layout(net)
+            self.items.append((h, len(net.source), X_all[gi]))
+        self.n_nets = len(self.items)
+
+    def run(self, mode, n_vec):
+        """(conn_evals, seconds) of n_vec vectors per sampled network."""
+        ev, dt = 0, 0.0
+        for h, E, X in self.items:
+            Xs = X[:n_vec]
+            if self.ref is None:
+                t0 = time.perf_counter()
+                self.oracle.eval_batch(h, Xs)
+                t = time.perf_counter() - t0
+            else:
+                t, _ = h.eval_batch(Xs, mode={"par": 1, "omp-seq": 2}[mode], workers=self.threads)
+            ev += E * len(Xs)
+            dt += t
+        return ev, dt
+
+    def measure(self, budget_s=20.0):
+        """Best mode within about budget_s seconds of CPU work."""
+        if self.ref is None:
+            ev, dt = self.run("par", 1)
+            return self.describe("port-seq", ev, dt, 1)
+        res = {}
+        # eval_parallel: vectors one by one until half the budget is spent
+        ev = dt = 0.0
+        n = 0
+        while dt < budget_s / 2 and n < self.items[0][2].shape[0]:
+            e, t = self.run("par", 1)
+            ev += e
+            dt += t
+            n += 1
+        res["par"] = (ev, dt, n)
+        e, t = self.run("omp-seq", self.threads)
+        res["omp-seq"] = (e, t, self.threads)
+        mode = max(res, key=lambda k: res[k][0] / res[k][1])
+        return self.describe(mode, *res[mode])
+
+    def describe(self, mode, ev, dt, n_vec):
+        return {"value": ev / dt, "unit": "conn_evals/s", "cores": self.threads, "kind": self.kind,
+                "mode": mode,
+                "sample": f"{n_vec} vector(s) x {self.n_nets} network(s) of this workload in "
+                          f"{dt:.2f}s ({mode})"}
+
+
 def cpu_baseline(nets, X_all, cfg, budget_s=20.0):
-    """The reference's own CPU evaluator (oracle/_ref, the unmodified
-    reference compiled from its sources) on a bounded sample of the same
-    workload: as many input vectors as fit in ~budget_s, best of
-    eval_parallel (all threads) and an OpenMP loop of eval_sequential."""
-    from oracle.bind import Ref, Oracle, available_ref
-    import paper_2005_04347_b200 as A
-    kind = "reference" if available_ref() else "port"
-    if kind == "reference":
-        ref = Ref()
-        threads = ref.L.ref_max_threads()
-    else:
-        ref = None
-        threads = 1
-    results = []
-    total_edges = 0
-    t_used = 0.0
-    evals = 0
-    for gi, net in enumerate(nets):
-        if cfg in ("c2", "c4"):
-            lay = host_layout_banded(cfg, net)
-            rn = ref.layout_from_csr(lay) if ref else None
-        else:
-            rn = ref.network(net) if ref else None
-            if rn is not None:
-                assert rn.preprocess() == 0
-            lay = None
-        E = len(net.source)
-        X = X_all[gi]
-        if rn is None:
-            o = Oracle()
-            lay = lay or o.layout(net)
-            t0 = time.perf_counter()
-            n = 0
-            while n < X.shape[0] and time.perf_counter() - t0 < budget_s / len(nets):
-                o.eval_batch(lay, X[n:n + 1])
-                n += 1
-            dt = time.perf_counter() - t0
-            results.append(("port-seq", E * n, dt))
-            continue
-        # mode 1: eval_parallel over all host threads, vector by vector
-        n1, t1 = 0, 0.0
-        while n1 < X.shape[0] and t1 < budget_s / (2 * len(nets)):
-            t, _ = rn.eval_batch(X[n1:n1 + 1], mode=1, workers=threads)
-            t1 += t
-            n1 += 1
-        # mode 2: OpenMP loop of eval_sequential over vectors
-        n2 = min(X.shape[0], max(threads, 1))
-        t2, _ = rn.eval_batch(X[:n2], mode=2, workers=threads)
-        results.append(("par", E * n1, t1))
-        results.append(("omp-seq", E * n2, t2))
-        total_edges += E
-    best = {}
-    for mode, ev, dt in results:
-        m = best.setdefault(mode, [0, 0.0])
-        m[0] += ev
-        m[1] += dt
-    rates = {k: v[0] / v[1] for k, v in best.items() if v[1] > 0}
-    mode = max(rates, key=rates.get)
-    sample = ", ".join(f"{k}: {best[k][0] / max(1, sum(len(n.source) for n in nets)):.0f} vectors "
-                       f"in {best[k][1]:.1f}s" for k in best)
-    return {"value": rates[mode], "unit": "conn_evals/s", "cores": threads, "kind": kind,
-            "mode": mode, "sample": sample}
+    return RefCPU(nets, X_all, cfg).measure(budget_s)
 
 
 def run_ours(args, cfg):
@@ -384,9 +396,14 @@ def run_reference(args, cfg):
         X = [rng.uniform(-2, 2, (B_total, len(n.inputs))).astype(np.float32) for n in nets]
     else:
         X = [rng.uniform(-2, 2, (B_total, len(nets[0].inputs))).astype(np.float32)]
+    cpu = RefCPU(nets, X, cfg)
+    first = cpu.measure(budget_s=max(2.0, args.cpu_budget / 4))   # picks the faster mode
+    mode = first["mode"]
+    n_vec = 1 if mode in ("par", "port-seq") else cpu.threads
     vals = []
     for _ in range(args.warmup + args.steps):
-        vals.append(cpu_baseline(nets, X, cfg, budget_s=max(2.0, args.cpu_budget / 4)))
+        ev, dt = cpu.run("par" if mode == "port-seq" else mode, n_vec)
+        vals.append(cpu.describe(mode, ev, dt, n_vec))
     cb = vals[-1]
     timed = vals[args.warmup:]
     value = statistics.mean(v["value"] for v in timed)

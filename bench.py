@@ -252,18 +252,19 @@ def run_ours(args, cfg):
     nets = make_network(cfg, args.scale)
     B_total = CONFIGS[cfg][1]
     rng = np.random.default_rng(12345)
+    from paper_2005_04347_b200.shard import batch_slice, gather_rows, population_shard
     if cfg == "c5":
-        # population: networks are sharded, each keeps its 128 vectors
-        shard = nets[rank::world] if world > 1 else nets
-        lo = 0
+        # population sharding: networks dealt round-robin, each keeps its 128 vectors
+        mine = population_shard(len(nets), world, rank)
+        shard = [nets[g] for g in mine]
         X = [rng.uniform(-2, 2, (B_total, len(n.inputs))).astype(np.float32) for n in nets]
-        Xs = [X[i] for i in range(rank, len(nets), world)]
+        Xs = [X[g] for g in mine]
         B = B_total
     else:
+        # batch sharding: a full layout replica, a contiguous slice of the vectors
         shard = nets
         X_full = rng.uniform(-2, 2, (B_total, len(nets[0].inputs))).astype(np.float32)
-        per = (B_total + world - 1) // world
-        lo, hi = rank * per, min(B_total, (rank + 1) * per)
+        lo, hi = batch_slice(B_total, world, rank)
         Xs = [X_full[lo:hi]]
         X = [X_full]
         B = hi - lo
@@ -322,8 +323,7 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         # NCCL gather of every rank's outputs (the only collective)
-        gathered = [torch.empty_like(out_dev) for _ in range(world)]
-        dist.all_gather(gathered, out_dev)
+        gathered = gather_rows(out_dev.view(-1, max(1, info["n_outputs"])), world)
 
     # e2e: host (pinned) buffers through the C-ABI call, copies inside
     x_pin = torch.from_numpy(np.concatenate([x.reshape(-1) for x in Xs])).pin_memory()

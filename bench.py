@@ -367,7 +367,10 @@ def run_ours(args, cfg):
             "config": {"workload": CONFIGS[cfg][0], "config": cfg, "edges": E,
                        "nodes": int(sum(len(n.nodes) for n in nets)),
                        "levels": info["total_layers"], "batch": B_total,
-                       "batch_per_gpu": B, "parallelism": f"batch-sharded dp{world}",
+                       "batch_per_gpu": B,
+                       "parallelism": (f"population-sharded x{world} (networks per GPU: "
+                                       f"{len(shard)})" if cfg == "c5" else
+                                       f"batch-sharded dp{world}"),
                        "l2": "working set > 126 MB L2 (no flush)" if cfg in ("c2", "c4") else
                              "L2-resident working set; per-step state rewritten"},
             "e2e": {"value": conn_evals_total / e2e_s, "unit": "conn_evals/s",

@@ -202,6 +202,30 @@ struct LevelLaunch {
     uint32_t tiles;
 };
 
+// ASNN_LEVEL_VARIANT (tuning experiments; profiles/r1_level_variants.txt):
+// 1 = 8 gathers in flight, 4 blocks/SM (64 registers; the default), 0 = 8 in
+// flight, unconstrained (74 registers, 3 blocks/SM), 2 = 16 in flight and
+// 2 blocks/SM, 3 = 16 in flight and 3 blocks/SM, 4 = 4 in flight, 6 blocks/SM.
+int level_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("ASNN_LEVEL_VARIANT");
+        v = s ? atoi(s) : 1;
+    }
+    return v;
+}
+
+template <int LANES>
+LevelLaunch wide_level(uint32_t tiles) {
+    switch (level_variant()) {
+        case 0: return {k_level<4, LANES, 8, 1>, LANES, tiles};
+        case 2: return {k_level<4, LANES, 16, 2>, LANES, tiles};
+        case 3: return {k_level<4, LANES, 16, 3>, LANES, tiles};
+        case 4: return {k_level<4, LANES, 4, 6>, LANES, tiles};
+        default: return {k_level<4, LANES, 8, 4>, LANES, tiles};
+    }
+}
+
 LevelLaunch level_launch_for(uint32_t ldA) {
     switch (ldA) {
         case 1: return {k_level<1, 1>, 1, 1};
@@ -210,8 +234,8 @@ LevelLaunch level_launch_for(uint32_t ldA) {
         case 8: return {k_level<4, 2>, 2, 1};
         case 16: return {k_level<4, 4>, 4, 1};
         case 32: return {k_level<4, 8>, 8, 1};
-        case 64: return {k_level<4, 16>, 16, 1};
-        default: return {k_level<4, 32>, 32, ldA / 128};
+        case 64: return wide_level<16>(1);
+        default: return wide_level<32>(ldA / 128);
     }
 }
 

@@ -48,19 +48,19 @@ __global__ void k_sense(const uint4* __restrict__ sinfo, uint32_t n_sensors,
 //   stored edge order with fp32 mul then fp32 add (bit-exact).
 // sched lists the level's positions (heaviest first); item -> (sched[item /
 // tiles], item % tiles).
-template <int V, int LANES>
+template <int V, int LANES, int UU>
 struct LevelCfg {
-    static constexpr int CH = LANES < 8 ? 8 : LANES;  // edges per chunk
-    static constexpr int PER = CH / LANES;            // edges held per lane
-    static constexpr int U = 8;                       // gathers in flight
+    static constexpr int U = UU;                          // gathers in flight per thread
+    static constexpr int CH = LANES < U ? U : LANES;      // edges per chunk
+    static constexpr int PER = CH / LANES;                // edges held per lane
 };
 
-template <int V, int LANES>
-__global__ void __launch_bounds__(256)
+template <int V, int LANES, int U = 8, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB)
 k_level(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
         float* __restrict__ A, uint32_t ldA, const uint32_t* __restrict__ sched,
         uint32_t n_items, uint32_t tiles) {
-    using C = LevelCfg<V, LANES>;
+    using C = LevelCfg<V, LANES, U>;
     const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t item = gt / LANES;
     if (item >= n_items) return;  // uniform across the LANES group

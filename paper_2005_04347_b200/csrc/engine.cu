@@ -306,17 +306,20 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     const uint32_t mode = L->dev->sweep_mode;  // 0 auto, 1 layer launches, 2 K-cta when it fits
     if (mode == 1) return p;
     if (L->n_levels < 2 || L->max_pos == 0) return p;
-    p.RB = std::min<uint32_t>(L->max_width + 1, 4096);
-    p.EB = std::min<uint32_t>(std::max<uint32_t>(L->max_level_edges, 1), 4096);
+    // +3 / +1 entries: the bulk copies start at 16-byte aligned indices
+    p.RB = (std::min<uint32_t>(L->max_width + 1, 4096) + 3 + 3) & ~3u;
+    p.EB = (std::min<uint32_t>(std::max<uint32_t>(L->max_level_edges, 1), 4096) + 1 + 1) & ~1u;
     const uint32_t cmax = std::min<uint32_t>(ldA, 128);
     for (uint32_t C = cmax; C >= 1; C >>= 1) {
         if (ldA % C) continue;
         uint32_t eb = p.EB;
-        const uint64_t as_bytes = (static_cast<uint64_t>(L->max_pos) * C + 3) / 4 * 16;
-        uint64_t sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4;
+        // activations (+ the zero row) | 4 edge slots | 4 row-pointer slots | 4 mbarriers | meta
+        const uint64_t as_bytes = (static_cast<uint64_t>(L->max_pos + 1) * C + 3) / 4 * 16;
+        const uint64_t fixed = 4ull * 8 + 4ull * 16;
+        uint64_t sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4 + fixed;
         while (sm > kMaxDynSmem && eb > 64) {  // stage fewer edges; big layers read global
             eb /= 2;
-            sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4;
+            sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4 + fixed;
         }
         if (sm <= kMaxDynSmem) {
             p.C = C;
@@ -401,7 +404,7 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
     if (L->total_pos)
         k_state_map<<<blocks_for(L->total_pos), kThreads, 0, st>>>(m, flat.node_ids.p, L->total_pos,
                                                                    L->state_map.p, bad.p);
-    CKL(L->edges.alloc(E));
+    CKL(L->edges.alloc(E + 2));  // +2: K-cta bulk copies round up to 16 bytes
     if (E)
         k_edges<<<blocks_for(E), kThreads, 0, st>>>(m, flat.in_ids.p, flat.w.p, E, L->state_map.p,
                                                    L->total_pos, L->edges.p, bad.p);
@@ -847,7 +850,7 @@ int asnn_dev_upload_layout(asnn_dev* dev, const asnn_layout_desc* d, asnn_dev_la
     FlatDevice f;
     DevBuf<uint64_t> row64;
     CK(f.node_ids.alloc(d->node_count));
-    CK(f.row_ptr.alloc(d->node_count + 1));
+    CK(f.row_ptr.alloc(d->node_count + 8));  // slack: K-cta bulk copies round up to 16 bytes
     CK(row64.alloc(d->node_count + 1));
     CK(f.in_ids.alloc(E));
     CK(f.w.alloc(E));

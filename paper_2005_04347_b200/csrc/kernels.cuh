@@ -269,153 +269,7 @@ k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, f
     }
 }
 
-// ---------------------------------------------------------------------------
-// K-cta: the whole level sweep of one network for one slice of C batch
-// columns inside ONE CTA -- the paper's Algorithm 3 (one block, a barrier per
-// layer) done right: activations of the slice live in
-// shared memory, the next level's row pointers and {col, w} edges are staged
-// by cp.async while the current level computes, and the per-level barrier is
-// a __syncthreads instead of a kernel boundary.  Batch columns (and networks
-// of a population) are independent, so CTAs never synchronise with each
-// other.  Used for deep/narrow networks, small networks and populations
-// whose per-slice activations fit in shared memory (C1, C3, C5).
-struct CtaNet {
-    uint32_t pos_base, n_pos, n_sensors, sens_prefix;
-    uint32_t in_prefix, n_in, out_prefix, n_out;
-    uint32_t lo_base, n_layers, pad0, pad1;
-};
-
-namespace cta {
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(heavy::smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(heavy::smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-constexpr uint32_t kRing = 4;  // staged layers (3 prefetched ahead of the one computing)
-__device__ __forceinline__ void wait_ring() { asm volatile("cp.async.wait_group 2;" ::: "memory"); }
-}  // namespace cta
-
-// lo_cat/le_cat: per network, layer boundaries as local positions and as
-// global edge offsets ([n_layers + 1] entries from lo_base).  Shared memory:
-// As[max_pos][C] | eb[kRing][EB] uint2 | rb[kRing][RB] u32.
-template <int V>
-__global__ void __launch_bounds__(256)
-k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
-      const uint32_t* __restrict__ le_cat, const uint32_t* __restrict__ row_ptr,
-      const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,
-      const uint4* __restrict__ oinfo, const float* __restrict__ x, uint32_t n_vec,
-      float* __restrict__ A, uint32_t ldA, uint32_t C, uint32_t max_pos, uint32_t EB, uint32_t RB,
-      int write_all) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    float* As = reinterpret_cast<float*>(smem);
-    // activations region rounded up to 16 bytes so the edge buffers stay aligned
-    uint2* eb = reinterpret_cast<uint2*>(As + ((static_cast<size_t>(max_pos) * C + 3) & ~size_t(3)));
-    uint32_t* rb = reinterpret_cast<uint32_t*>(eb + cta::kRing * EB);
-    const CtaNet n = nets[blockIdx.y];
-    const uint32_t c0 = blockIdx.x * C;
-    const uint32_t groups = C / V;  // column groups per row
-    const uint32_t T = blockDim.x, tid = threadIdx.x;
-    const uint32_t* lo = lo_cat + n.lo_base;
-    const uint32_t* le = le_cat + n.lo_base;
-
-    // level l's row pointers and edges -> buffer (l & 1), when they fit
-    auto prefetch = [&](uint32_t l) {
-        const uint32_t a = lo[l], b = lo[l + 1];
-        const uint32_t e0 = le[l], e1 = le[l + 1];
-        if (b - a + 1 > RB || e1 - e0 > EB) return;
-        uint32_t* rdst = rb + (l % cta::kRing) * RB;
-        uint2* edst = eb + (l % cta::kRing) * EB;
-        for (uint32_t i = tid; i <= b - a; i += T) cta::cp_async4(&rdst[i], &row_ptr[n.pos_base + a + i]);
-        for (uint32_t i = tid; i < e1 - e0; i += T) cta::cp_async8(&edst[i], &edges[e0 + i]);
-    };
-
-    // sensors: eval.cpp:17 (sigmoided input values)
-    for (uint32_t i = tid; i < n.n_sensors * groups; i += T) {
-        const uint32_t s = i / groups, q = i - s * groups;
-        const uint32_t k = sinfo[n.sens_prefix + s].w;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const uint32_t col = c0 + q * V + v;
-            float xv = 0.0f;
-            if (col < n_vec && k != kUnassigned)
-                xv = x[static_cast<uint64_t>(n_vec) * n.in_prefix + static_cast<uint64_t>(col) * n.n_in + k];
-            As[s * C + q * V + v] = sigmoid32(xv);
-        }
-    }
-    // layers 1 .. kRing-1 in flight before the first one is needed; one
-    // commit group per layer so wait_group(kRing - 2) retires exactly the next
-    for (uint32_t l = 1; l < cta::kRing; ++l) {
-        if (l < n.n_layers) prefetch(l);
-        cta::commit();
-    }
-    cta::wait_ring();
-    __syncthreads();
-
-    for (uint32_t l = 1; l < n.n_layers; ++l) {
-        const uint32_t a = lo[l], b = lo[l + 1];
-        const uint32_t e0 = le[l], e1 = le[l + 1];
-        const bool staged = (b - a + 1 <= RB) && (e1 - e0 <= EB);
-        const uint32_t* R = rb + (l % cta::kRing) * RB;
-        const uint2* Ebuf = eb + (l % cta::kRing) * EB;
-        for (uint32_t it = tid; it < (b - a) * groups; it += T) {
-            const uint32_t i = it / groups, q = it - i * groups;
-            uint32_t kb, ke;
-            const uint2* Ep;
-            if (staged) {
-                kb = R[i] - e0;
-                ke = R[i + 1] - e0;
-                Ep = Ebuf;
-            } else {
-                kb = row_ptr[n.pos_base + a + i];
-                ke = row_ptr[n.pos_base + a + i + 1];
-                Ep = edges;
-            }
-            float acc[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) acc[v] = 0.0f;
-            for (uint32_t k = kb; k < ke; ++k) {
-                const uint2 ed = Ep[k];
-                const float w = __uint_as_float(ed.y);
-                const float* src = As + (ed.x - n.pos_base) * C + q * V;
-                if constexpr (V == 4) {
-                    const float4 s4 = *reinterpret_cast<const float4*>(src);
-                    acc[0] = mac(acc[0], w, s4.x);
-                    acc[1] = mac(acc[1], w, s4.y);
-                    acc[2] = mac(acc[2], w, s4.z);
-                    acc[3] = mac(acc[3], w, s4.w);
-                } else {
-#pragma unroll
-                    for (int v = 0; v < V; ++v) acc[v] = mac(acc[v], w, src[v]);
-                }
-            }
-#pragma unroll
-            for (int v = 0; v < V; ++v) As[(a + i) * C + q * V + v] = sigmoid32(acc[v]);
-        }
-        __syncthreads();  // layer l done: its buffer may be refilled
-        if (l + cta::kRing - 1 < n.n_layers) prefetch(l + cta::kRing - 1);
-        cta::commit();
-        cta::wait_ring();  // layer l + 1 staged
-        __syncthreads();
-    }
-
-    // write back: every row (state requested) or only the declared outputs
-    const uint32_t ncols = min(C, ldA - c0);
-    if (write_all) {
-        for (uint32_t i = tid; i < n.n_pos * ncols; i += T) {
-            const uint32_t p = i / ncols, c = i - p * ncols;
-            A[static_cast<uint64_t>(n.pos_base + p) * ldA + c0 + c] = As[p * C + c];
-        }
-    } else {
-        for (uint32_t i = tid; i < n.n_out * ncols; i += T) {
-            const uint32_t j = i / ncols, c = i - j * ncols;
-            const uint32_t pos = oinfo[n.out_prefix + j].x;
-            if (pos != kUnassigned)
-                A[static_cast<uint64_t>(pos) * ldA + c0 + c] = As[(pos - n.pos_base) * C + c];
-        }
-    }
-}
+#include "cta.cuh"
 
 __global__ void k_sigmoid_many(const float* __restrict__ x, float* __restrict__ y, uint64_t n) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -628,7 +628,7 @@ int run_flatten(asnn_dev* dev, DevNet& d, std::vector<NetMeta>& metas, FlatDevic
         // sort needs distinct alternates: use a fresh buffer set
         SortBuffers eb2;
         RC(radix_sort_pairs(dev, kbuf, v1, K, std::max(1, bits_for(P)), eb2, &k2, &v2, st));
-        CK(f.row_ptr.alloc(P + 1));
+        CK(f.row_ptr.alloc(P + 8));  // slack: K-cta bulk copies round up to 16 bytes
         RC(exclusive_scan(dev, rowcnt.p, f.row_ptr.p, P + 1, nullptr, st));
         CK(f.in_ids.alloc(K + 1));
         CK(f.w.alloc(K + 1));

@@ -12,9 +12,8 @@
 //    per layer.
 // Used for deep/narrow networks, small networks and populations whose
 // per-slice activations fit in shared memory (C1, C3, C5).
+// Included by kernels.cuh inside namespace asnn_b200 (uses heavy::, sigmoid32, mac).
 #pragma once
-
-namespace asnn_b200 {
 
 struct CtaNet {
     uint32_t pos_base, n_pos, n_sensors, sens_prefix;
@@ -211,5 +210,3 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
         }
     }
 }
-
-}  // namespace asnn_b200

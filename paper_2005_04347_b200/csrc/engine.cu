@@ -318,7 +318,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         const uint64_t fixed = 4ull * 8 + 4ull * 16;
         uint64_t sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4 + fixed;
         while (sm > kMaxDynSmem && eb > 64) {  // stage fewer edges; big layers read global
-            eb /= 2;
+            eb = (eb / 2) & ~1u;                // stays even: 16-byte aligned slots
             sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4 + fixed;
         }
         if (sm <= kMaxDynSmem) {

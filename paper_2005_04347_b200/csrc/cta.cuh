@@ -2,11 +2,12 @@
 // batch columns inside ONE CTA.  The paper's Algorithm 3 (one block, a
 // barrier per layer) done right:
 //  * the slice's activations live in shared memory (gathers are LDS);
-//  * layers are staged ahead: thread 0 copies each layer's row pointers and
-//    {col, w} edges -- contiguous in the level-sorted CSR -- with two TMA bulk
-//    copies into a 4-slot ring (mbarrier complete_tx), three layers ahead of
-//    the one computing, so the per-layer critical path is LDS + the in-order
-//    FADD chain + the sigmoid + one __syncthreads;
+//  * a producer warp stages each layer's row pointers and {col, w} edges --
+//    contiguous in the level-sorted CSR -- with two TMA bulk copies into a
+//    4-slot ring (mbarrier complete_tx), up to three layers ahead; consumer
+//    warps release slots through an "empty" mbarrier;
+//  * the consumer warps' per-layer critical path is LDS + the in-order FADD
+//    chain + the sigmoid + one named barrier among themselves;
 //  * batch columns (and networks of a population) are independent, so CTAs
 //    never synchronise with each other -- no grid barrier, no kernel boundary
 //    per layer.
@@ -22,7 +23,7 @@ struct CtaNet {
 };
 
 namespace cta {
-constexpr uint32_t kRing = 4;  // staged layers (3 ahead of the one computing)
+constexpr uint32_t kRing = 4;  // staged layers
 constexpr uint32_t kNotStaged = 0xFFFFFFFFu;
 
 __device__ __forceinline__ void expect_tx(uint64_t* b, uint32_t bytes) {
@@ -38,16 +39,82 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(heavy::smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void consumer_barrier(uint32_t n_threads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(n_threads) : "memory");
+}
+
+// One layer's items for one thread: item it = (node i, column group q).
+// Rp / Ep point at the staged slot (shared memory) or at the global arrays.
+template <int V>
+__device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const uint2* Ep, uint32_t e0,
+                                            uint32_t a, uint32_t b, uint32_t C, uint32_t gshift,
+                                            uint32_t pos_base, uint32_t n_pos, uint32_t zero_row,
+                                            uint32_t tid, uint32_t T) {
+    const uint32_t groups_mask = (1u << gshift) - 1u;
+    for (uint32_t it = tid; it < ((b - a) << gshift); it += T) {
+        const uint32_t i = it >> gshift, q = it & groups_mask;
+        uint32_t k = Rp[i] - e0;
+        const uint32_t ke = Rp[i + 1] - e0;
+        const float* Aq = As + q * V;
+        auto row = [&](uint32_t pos) {
+            const uint32_t p = pos - pos_base;
+            return (p < n_pos ? p : zero_row) * C;
+        };
+        float acc[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = 0.0f;
+        // four edges' loads in flight, then their adds in stored order
+        for (; k + 4 <= ke; k += 4) {
+            uint2 ed[4];
+            float av[4][V];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ed[j] = Ep[k + j];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float* src = Aq + row(ed[j].x);
+                if constexpr (V == 4) {
+                    const float4 t = *reinterpret_cast<const float4*>(src);
+                    av[j][0] = t.x;
+                    av[j][1] = t.y;
+                    av[j][2] = t.z;
+                    av[j][3] = t.w;
+                } else {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) av[j][v] = src[v];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] = mac(acc[v], __uint_as_float(ed[j].y), av[j][v]);
+        }
+        for (; k < ke; ++k) {
+            const uint2 ed = Ep[k];
+            const float* src = Aq + row(ed.x);
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] = mac(acc[v], __uint_as_float(ed.y), src[v]);
+        }
+        float* dst = As + (a + i) * C + q * V;
+        if constexpr (V == 4) {
+            *reinterpret_cast<float4*>(dst) =
+                make_float4(sigmoid32(acc[0]), sigmoid32(acc[1]), sigmoid32(acc[2]), sigmoid32(acc[3]));
+        } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) dst[v] = sigmoid32(acc[v]);
+        }
+    }
+}
 }  // namespace cta
 
-// Shared memory: As[max_pos*C, 16-B rounded] | eb[kRing][EB] uint2 |
-// rb[kRing][RB] u32 | bar[kRing] u64 | meta[kRing][4] u32.
+// Block = consumer warps + 1 producer warp (the last).  Shared memory:
+// As[(max_pos+1)*C, 16-B rounded; row max_pos is zeros] | eb[kRing][EB] uint2 |
+// rb[kRing][RB] u32 | full[kRing], empty[kRing] u64 | meta[kRing][4] u32.
 // EB is even and RB a multiple of 4 (16-byte aligned slots); row_ptr and
 // edges are allocated with slack so the rounded-up copies stay in bounds.
 // lo_cat / le_cat: per network, layer boundaries as local positions and as
 // global edge indices ([n_layers + 1] entries from lo_base).
 template <int V>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(288)
 k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       const uint32_t* __restrict__ le_cat, const uint32_t* __restrict__ row_ptr,
       const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,
@@ -61,140 +128,91 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     // layout does not hold) read 0.0f like the reference's untouched op slots
     uint2* eb = reinterpret_cast<uint2*>(As + ((static_cast<size_t>(max_pos + 1) * C + 3) & ~size_t(3)));
     uint32_t* rb = reinterpret_cast<uint32_t*>(eb + kRing * EB);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(rb + kRing * RB);
-    uint32_t* meta = reinterpret_cast<uint32_t*>(bar + kRing);
+    uint64_t* full = reinterpret_cast<uint64_t*>(rb + kRing * RB);
+    uint64_t* empty = full + kRing;
+    uint32_t* meta = reinterpret_cast<uint32_t*>(empty + kRing);
 
     const CtaNet n = nets[blockIdx.y];
     const uint32_t c0 = blockIdx.x * C;
     const uint32_t groups = C / V;  // column groups per row (a power of two)
     const uint32_t gshift = __ffs(groups) - 1;
-    const uint32_t T = blockDim.x, tid = threadIdx.x;
-    const uint32_t* lo = lo_cat + n.lo_base;
-    const uint32_t* le = le_cat + n.lo_base;
-
-    // layer l (>= 1) uses ring slot (l - 1) % kRing for the ((l - 1) / kRing)-th time
-    // thread 0: stage layer l into its slot (or mark it unstaged)
-    auto issue = [&](uint32_t l) {
-        const uint32_t s = (l - 1) % kRing;
-        const uint32_t a = lo[l], b = lo[l + 1];
-        const uint32_t e0 = le[l], e1 = le[l + 1];
-        const uint32_t r0 = n.pos_base + a, r0a = r0 & ~3u;
-        const uint32_t rbytes = ((b - a + 1 + (r0 - r0a)) * 4 + 15) & ~15u;
-        const uint32_t e0a = e0 & ~1u;
-        const uint32_t ebytes = ((e1 - e0 + (e0 - e0a)) * 8 + 15) & ~15u;
-        uint32_t* m = meta + 4 * s;
-        m[0] = a;
-        m[1] = b;
-        m[2] = e0;
-        if (rbytes <= RB * 4 && ebytes <= EB * 8) {
-            m[3] = (r0 - r0a) | ((e0 - e0a) << 8);
-            expect_tx(&bar[s], rbytes + (ebytes ? ebytes : 0));
-            bulk_g2s(rb + s * RB, row_ptr + r0a, rbytes, &bar[s]);
-            if (ebytes) bulk_g2s(eb + s * EB, edges + e0a, ebytes, &bar[s]);
-        } else {
-            m[3] = kNotStaged;
-            heavy::mbar_arrive(&bar[s]);
-        }
-    };
+    const uint32_t Tc = blockDim.x - 32;  // consumer threads
+    const uint32_t tid = threadIdx.x;
 
     if (tid == 0) {
-        for (uint32_t s = 0; s < kRing; ++s) heavy::mbar_init(&bar[s], 1);
+        for (uint32_t s = 0; s < kRing; ++s) {
+            heavy::mbar_init(&full[s], 1);
+            heavy::mbar_init(&empty[s], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (uint32_t l = 1; l < kRing && l < n.n_layers; ++l) issue(l);  // layers 1..3
     }
+    __syncthreads();
 
-    for (uint32_t c = tid; c < C; c += T) As[max_pos * C + c] = 0.0f;
-    auto local = [&](uint32_t pos) {
-        const uint32_t p = pos - n.pos_base;
-        return p < n.n_pos ? p : max_pos;
-    };
-
-    // sensors: eval.cpp:17 (sigmoided input values), overlapping the staging
-    for (uint32_t i = tid; i < (n.n_sensors << gshift); i += T) {
-        const uint32_t s = i >> gshift, q = i & (groups - 1);
-        const uint32_t k = sinfo[n.sens_prefix + s].w;
+    if (tid >= Tc) {
+        // producer: layer l (>= 1) lives in slot (l - 1) % kRing for its
+        // ((l - 1) / kRing)-th use
+        if (tid == Tc) {
+            const uint32_t* lo = lo_cat + n.lo_base;
+            const uint32_t* le = le_cat + n.lo_base;
+            for (uint32_t l = 1; l < n.n_layers; ++l) {
+                const uint32_t s = (l - 1) % kRing, u = (l - 1) / kRing;
+                const uint32_t a = lo[l], b = lo[l + 1];
+                const uint32_t e0 = le[l], e1 = le[l + 1];
+                if (u > 0) heavy::mbar_wait(&empty[s], (u - 1) & 1);
+                const uint32_t r0 = n.pos_base + a, r0a = r0 & ~3u;
+                const uint32_t rbytes = ((b - a + 1 + (r0 - r0a)) * 4 + 15) & ~15u;
+                const uint32_t e0a = e0 & ~1u;
+                const uint32_t ebytes = ((e1 - e0 + (e0 - e0a)) * 8 + 15) & ~15u;
+                uint32_t* m = meta + 4 * s;
+                m[0] = a;
+                m[1] = b;
+                m[2] = e0;
+                if (rbytes <= RB * 4 && ebytes <= EB * 8) {
+                    m[3] = (r0 - r0a) | ((e0 - e0a) << 8);
+                    expect_tx(&full[s], rbytes + ebytes);
+                    bulk_g2s(rb + s * RB, row_ptr + r0a, rbytes, &full[s]);
+                    if (ebytes) bulk_g2s(eb + s * EB, edges + e0a, ebytes, &full[s]);
+                } else {
+                    m[3] = kNotStaged;
+                    heavy::mbar_arrive(&full[s]);
+                }
+            }
+        }
+    } else {
+        for (uint32_t c = tid; c < C; c += Tc) As[max_pos * C + c] = 0.0f;
+        // sensors: eval.cpp:17 (sigmoided input values), overlapping the staging
+        for (uint32_t i = tid; i < (n.n_sensors << gshift); i += Tc) {
+            const uint32_t s = i >> gshift, q = i & (groups - 1);
+            const uint32_t k = sinfo[n.sens_prefix + s].w;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const uint32_t col = c0 + q * V + v;
-            float xv = 0.0f;
-            if (col < n_vec && k != kUnassigned)
-                xv = x[static_cast<uint64_t>(n_vec) * n.in_prefix + static_cast<uint64_t>(col) * n.n_in + k];
-            As[s * C + q * V + v] = sigmoid32(xv);
+            for (int v = 0; v < V; ++v) {
+                const uint32_t col = c0 + q * V + v;
+                float xv = 0.0f;
+                if (col < n_vec && k != kUnassigned)
+                    xv = x[static_cast<uint64_t>(n_vec) * n.in_prefix + static_cast<uint64_t>(col) * n.n_in + k];
+                As[s * C + q * V + v] = sigmoid32(xv);
+            }
+        }
+        consumer_barrier(Tc);
+        for (uint32_t l = 1; l < n.n_layers; ++l) {
+            const uint32_t s = (l - 1) % kRing;
+            heavy::mbar_wait(&full[s], ((l - 1) / kRing) & 1);
+            const uint32_t* m = meta + 4 * s;
+            const uint32_t a = m[0], b = m[1], e0 = m[2], off = m[3];
+            if (off != kNotStaged)
+                layer_items<V>(As, rb + s * RB + (off & 0xFF), eb + s * EB + (off >> 8), e0, a, b, C,
+                               gshift, n.pos_base, n.n_pos, max_pos, tid, Tc);
+            else
+                layer_items<V>(As, row_ptr + n.pos_base + a, edges, 0, a, b, C, gshift, n.pos_base,
+                               n.n_pos, max_pos, tid, Tc);
+            consumer_barrier(Tc);  // layer l visible to every consumer
+            if (tid == 0) heavy::mbar_arrive(&empty[s]);
         }
     }
     __syncthreads();
 
-    for (uint32_t l = 1; l < n.n_layers; ++l) {
-        const uint32_t s = (l - 1) % kRing;
-        // layer l + 3 reuses the slot of layer l - 1, finished at the last barrier
-        if (tid == 0 && l + kRing - 1 < n.n_layers) issue(l + kRing - 1);
-        heavy::mbar_wait(&bar[s], ((l - 1) / kRing) & 1);
-        const uint32_t* m = meta + 4 * s;
-        const uint32_t a = m[0], b = m[1], e0 = m[2], off = m[3];
-        const bool staged = off != kNotStaged;
-        const uint32_t* R = rb + s * RB + (off & 0xFF);
-        const uint2* Eb = eb + s * EB + (off >> 8);
-        for (uint32_t it = tid; it < ((b - a) << gshift); it += T) {
-            const uint32_t i = it >> gshift, q = it & (groups - 1);
-            uint32_t k, ke;
-            const uint2* Ep;
-            if (staged) {
-                k = R[i] - e0;
-                ke = R[i + 1] - e0;
-                Ep = Eb;
-            } else {
-                k = row_ptr[n.pos_base + a + i];
-                ke = row_ptr[n.pos_base + a + i + 1];
-                Ep = edges;
-            }
-            const float* Aq = As + q * V;
-            float acc[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) acc[v] = 0.0f;
-            // four edges' loads in flight, then their adds in stored order
-            for (; k + 4 <= ke; k += 4) {
-                uint2 ed[4];
-                float av[4][V];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) ed[j] = Ep[k + j];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float* src = Aq + local(ed[j].x) * C;
-                    if constexpr (V == 4) {
-                        const float4 t = *reinterpret_cast<const float4*>(src);
-                        av[j][0] = t.x;
-                        av[j][1] = t.y;
-                        av[j][2] = t.z;
-                        av[j][3] = t.w;
-                    } else {
-#pragma unroll
-                        for (int v = 0; v < V; ++v) av[j][v] = src[v];
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                    for (int v = 0; v < V; ++v) acc[v] = mac(acc[v], __uint_as_float(ed[j].y), av[j][v]);
-            }
-            for (; k < ke; ++k) {
-                const uint2 ed = Ep[k];
-                const float* src = Aq + local(ed.x) * C;
-#pragma unroll
-                for (int v = 0; v < V; ++v) acc[v] = mac(acc[v], __uint_as_float(ed.y), src[v]);
-            }
-            float* dst = As + (a + i) * C + q * V;
-            if constexpr (V == 4) {
-                *reinterpret_cast<float4*>(dst) =
-                    make_float4(sigmoid32(acc[0]), sigmoid32(acc[1]), sigmoid32(acc[2]), sigmoid32(acc[3]));
-            } else {
-#pragma unroll
-                for (int v = 0; v < V; ++v) dst[v] = sigmoid32(acc[v]);
-            }
-        }
-        __syncthreads();  // layer l visible; its slot may be refilled
-    }
-
     // write back: every row (state requested) or only the declared outputs
+    const uint32_t T = blockDim.x;
     const uint32_t ncols = min(C, ldA - c0);
     if (write_all) {
         for (uint32_t i = tid; i < n.n_pos * ncols; i += T) {

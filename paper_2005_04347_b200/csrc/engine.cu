@@ -315,7 +315,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         uint32_t eb = p.EB;
         // activations (+ the zero row) | 4 edge slots | 4 row-pointer slots | 4 mbarriers | meta
         const uint64_t as_bytes = (static_cast<uint64_t>(L->max_pos + 1) * C + 3) / 4 * 16;
-        const uint64_t fixed = 4ull * 8 + 4ull * 16;
+        const uint64_t fixed = 2ull * 4 * 8 + 4ull * 16;  // full/empty mbarriers + slot meta
         uint64_t sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4 + fixed;
         while (sm > kMaxDynSmem && eb > 64) {  // stage fewer edges; big layers read global
             eb = (eb / 2) & ~1u;                // stays even: 16-byte aligned slots
@@ -574,7 +574,8 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         auto fn = cp.V == 4 ? k_cta<4> : k_cta<1>;
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(cp.smem)));
-        fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T, cp.smem, st>>>(
+        // cp.T consumer threads + one producer warp
+        fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T + 32, cp.smem, st>>>(
             reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->le_cat.p, L->row_ptr.p,
             L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos, cp.EB, cp.RB,
             state ? 1 : 0);

@@ -122,8 +122,8 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       float* __restrict__ A, uint32_t ldA, uint32_t C, uint32_t max_pos, uint32_t EB, uint32_t RB,
       int write_all) {
     using namespace cta;
-    extern __shared__ __align__(16) unsigned char smem[];
-    float* As = reinterpret_cast<float*>(smem);
+    extern __shared__ __align__(128) unsigned char cta_smem[];
+    float* As = reinterpret_cast<float*>(cta_smem);
     // row max_pos of As is all zeros: predecessors without a position (ids the
     // layout does not hold) read 0.0f like the reference's untouched op slots
     uint2* eb = reinterpret_cast<uint2*>(As + ((static_cast<size_t>(max_pos + 1) * C + 3) & ~size_t(3)));

@@ -4,7 +4,8 @@
 //  * the slice's activations live in shared memory (gathers are LDS);
 //  * a producer warp stages each layer's row pointers and {col, w} edges --
 //    contiguous in the level-sorted CSR -- with two TMA bulk copies into a
-//    4-slot ring (mbarrier complete_tx), up to three layers ahead; consumer
+//    ring of R slots (a power of two chosen to fill shared memory; mbarrier
+//    complete_tx), up to R-1 layers ahead of the one computing; consumer
 //    warps release slots through an "empty" mbarrier;
 //  * the consumer warps' per-layer critical path is LDS + the in-order FADD
 //    chain + the sigmoid + one named barrier among themselves;
@@ -23,7 +24,6 @@ struct CtaNet {
 };
 
 namespace cta {
-constexpr uint32_t kRing = 4;  // staged layers
 constexpr uint32_t kNotStaged = 0xFFFFFFFFu;
 
 __device__ __forceinline__ void expect_tx(uint64_t* b, uint32_t bytes) {
@@ -107,8 +107,8 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
 }  // namespace cta
 
 // Block = consumer warps + 1 producer warp (the last).  Shared memory:
-// As[(max_pos+1)*C, 16-B rounded; row max_pos is zeros] | eb[kRing][EB] uint2 |
-// rb[kRing][RB] u32 | full[kRing], empty[kRing] u64 | meta[kRing][4] u32.
+// As[(max_pos+1)*C, 16-B rounded; row max_pos is zeros] | eb[R][EB] uint2 |
+// rb[R][RB] u32 | full[R], empty[R] u64 | meta[R][4] u32.
 // EB is even and RB a multiple of 4 (16-byte aligned slots); row_ptr and
 // edges are allocated with slack so the rounded-up copies stay in bounds.
 // lo_cat / le_cat: per network, layer boundaries as local positions and as
@@ -120,8 +120,9 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,
       const uint4* __restrict__ oinfo, const float* __restrict__ x, uint32_t n_vec,
       float* __restrict__ A, uint32_t ldA, uint32_t C, uint32_t max_pos, uint32_t EB, uint32_t RB,
-      int write_all) {
+      uint32_t ring_shift, int write_all) {
     using namespace cta;
+    const uint32_t kRing = 1u << ring_shift, ring_mask = kRing - 1u;
     extern __shared__ __align__(128) unsigned char cta_smem[];
     float* As = reinterpret_cast<float*>(cta_smem);
     // row max_pos of As is all zeros: predecessors without a position (ids the
@@ -149,13 +150,13 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     __syncthreads();
 
     if (tid >= Tc) {
-        // producer: layer l (>= 1) lives in slot (l - 1) % kRing for its
-        // ((l - 1) / kRing)-th use
+        // producer: layer l (>= 1) lives in slot (l - 1) % R for its
+        // ((l - 1) / R)-th use
         if (tid == Tc) {
             const uint32_t* lo = lo_cat + n.lo_base;
             const uint32_t* le = le_cat + n.lo_base;
             for (uint32_t l = 1; l < n.n_layers; ++l) {
-                const uint32_t s = (l - 1) % kRing, u = (l - 1) / kRing;
+                const uint32_t s = (l - 1) & ring_mask, u = (l - 1) >> ring_shift;
                 const uint32_t a = lo[l], b = lo[l + 1];
                 const uint32_t e0 = le[l], e1 = le[l + 1];
                 if (u > 0) heavy::mbar_wait(&empty[s], (u - 1) & 1);
@@ -195,8 +196,8 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
         }
         consumer_barrier(Tc);
         for (uint32_t l = 1; l < n.n_layers; ++l) {
-            const uint32_t s = (l - 1) % kRing;
-            heavy::mbar_wait(&full[s], ((l - 1) / kRing) & 1);
+            const uint32_t s = (l - 1) & ring_mask;
+            heavy::mbar_wait(&full[s], ((l - 1) >> ring_shift) & 1);
             const uint32_t* m = meta + 4 * s;
             const uint32_t a = m[0], b = m[1], e0 = m[2], off = m[3];
             if (off != kNotStaged)

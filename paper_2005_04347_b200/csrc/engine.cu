@@ -296,7 +296,7 @@ uint32_t default_heavy_threshold() {
 // slice whose activations (plus the staged edge buffers) fit in shared memory.
 struct CtaPlan {
     bool use = false;
-    uint32_t C = 0, V = 1, T = 32, smem = 0, EB = 0, RB = 0;
+    uint32_t C = 0, V = 1, T = 32, smem = 0, EB = 0, RB = 0, ring_shift = 2;
 };
 
 constexpr uint32_t kMaxDynSmem = 227 * 1024;
@@ -313,18 +313,23 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     for (uint32_t C = cmax; C >= 1; C >>= 1) {
         if (ldA % C) continue;
         uint32_t eb = p.EB;
-        // activations (+ the zero row) | 4 edge slots | 4 row-pointer slots | 4 mbarriers | meta
+        // activations (+ the zero row) | R edge slots | R row-pointer slots |
+        // R full + R empty mbarriers | R slot metas; R = 4 .. 16 staged layers
         const uint64_t as_bytes = (static_cast<uint64_t>(L->max_pos + 1) * C + 3) / 4 * 16;
-        const uint64_t fixed = 2ull * 4 * 8 + 4ull * 16;  // full/empty mbarriers + slot meta
-        uint64_t sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4 + fixed;
-        while (sm > kMaxDynSmem && eb > 64) {  // stage fewer edges; big layers read global
-            eb = (eb / 2) & ~1u;                // stays even: 16-byte aligned slots
-            sm = as_bytes + 4ull * eb * 8 + 4ull * p.RB * 4 + fixed;
+        auto smem_for = [&](uint32_t ebs, uint32_t rs) {
+            const uint64_t R = 1ull << rs;
+            return as_bytes + R * (ebs * 8ull + p.RB * 4ull + 2 * 8 + 16);
+        };
+        uint32_t rs = 4;
+        while (rs > 2 && smem_for(eb, rs) > kMaxDynSmem) --rs;
+        while (smem_for(eb, rs) > kMaxDynSmem && eb > 64) {  // stage fewer edges; big layers read global
+            eb = (eb / 2) & ~1u;                              // stays even: 16-byte aligned slots
         }
-        if (sm <= kMaxDynSmem) {
+        if (smem_for(eb, rs) <= kMaxDynSmem) {
             p.C = C;
             p.EB = eb;
-            p.smem = static_cast<uint32_t>(sm);
+            p.ring_shift = rs;
+            p.smem = static_cast<uint32_t>(smem_for(eb, rs));
             break;
         }
         if (C == 1) break;
@@ -578,7 +583,7 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T + 32, cp.smem, st>>>(
             reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->le_cat.p, L->row_ptr.p,
             L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos, cp.EB, cp.RB,
-            state ? 1 : 0);
+            cp.ring_shift, state ? 1 : 0);
     } else {
         if (L->total_sensors)
             k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(

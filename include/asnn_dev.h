@@ -206,6 +206,11 @@ int asnn_dev_activate_plan(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* ke
  * exhaustive parity checks of the epilogue. */
 int asnn_dev_sigmoid32(asnn_dev* dev, const float* x, float* y, uint64_t n);
 
+/* Microarchitecture probe: SM cycles per operation of a dependent chain of n
+ * ops run by one thread (which: 0 sigmoid32, 1 DFMA, 2 FADD, 3 shared-memory
+ * load, 4 double division, 5 exp).  Evidence for DESIGN.md's latency model. */
+int asnn_dev_latency_probe(asnn_dev* dev, int which, int n, double* cycles_per_op);
+
 /* ---- synthetic corpora (host, deterministic) ------------------------------
  * generate(GenSpec) byte-identical to the reference (netgen.cpp:71-157),
  * the MLP-adjacent shape (config 2) and the banded power-law shape

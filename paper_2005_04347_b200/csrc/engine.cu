@@ -711,6 +711,23 @@ extern "C" {
 
 const char* asnn_dev_version(void) { return "asnn-b200 0.1 (sm_100a)"; }
 
+int asnn_dev_latency_probe(asnn_dev* dev, int which, int n, double* cycles_per_op) {
+    if (!dev || !cycles_per_op || n <= 0) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    CK(cudaSetDevice(dev->device));
+    DevBuf<long long> c;
+    DevBuf<float> sink;
+    CK(c.alloc(1));
+    CK(sink.alloc(1));
+    k_latency_probe<<<1, 32, 0, dev->stream>>>(which, n, 0.37f, c.p, sink.p);
+    CK(cudaGetLastError());
+    long long h = 0;
+    CK(cudaMemcpyAsync(&h, c.p, 8, cudaMemcpyDeviceToHost, dev->stream));
+    CK(cudaStreamSynchronize(dev->stream));
+    *cycles_per_op = static_cast<double>(h) / n;
+    return ASNN_OK;
+}
+
 int asnn_dev_sigmoid32(asnn_dev* dev, const float* x, float* y, uint64_t n) {
     if (!dev || (n && (!x || !y))) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);

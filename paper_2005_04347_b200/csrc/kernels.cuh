@@ -271,6 +271,32 @@ k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, f
 
 #include "cta.cuh"
 
+// Latency probes (one thread, dependent chains, clock64): which = 0 sigmoid32,
+// 1 DFMA, 2 FADD, 3 shared-memory load chain, 4 __ddiv_rn, 5 exp_glibc.
+__global__ void k_latency_probe(int which, int n, float seed, long long* cycles, float* sink) {
+    __shared__ uint32_t chain[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) chain[i] = (i * 97 + 13) & 255;
+    __syncthreads();
+    if (threadIdx.x) return;
+    float f = seed;
+    double d = seed;
+    uint32_t p = static_cast<uint32_t>(seed);
+    const long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+        switch (which) {
+            case 0: f = sigmoid32(f); break;
+            case 1: d = __fma_rn(d, 1.0000001, 1e-9); break;
+            case 2: f = __fadd_rn(f, 1e-7f); break;
+            case 3: p = chain[p & 255]; break;
+            case 4: d = __ddiv_rn(1.0, __dadd_rn(1.0, d)); break;
+            default: d = exp_glibc(-d * 1e-3, kExpTab); break;
+        }
+    }
+    const long long t1 = clock64();
+    *cycles = t1 - t0;
+    *sink = f + static_cast<float>(d) + static_cast<float>(p);
+}
+
 __global__ void k_sigmoid_many(const float* __restrict__ x, float* __restrict__ y, uint64_t n) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) y[i] = sigmoid32(x[i]);

@@ -208,7 +208,8 @@ int asnn_dev_sigmoid32(asnn_dev* dev, const float* x, float* y, uint64_t n);
 
 /* Microarchitecture probe: SM cycles per operation of a dependent chain of n
  * ops run by one thread (which: 0 sigmoid32, 1 DFMA, 2 FADD, 3 shared-memory
- * load, 4 double division, 5 exp).  Evidence for DESIGN.md's latency model. */
+ * load, 4 double division, 5 exp, 6 empty loop iteration).  Evidence for
+ * DESIGN.md's latency model. */
 int asnn_dev_latency_probe(asnn_dev* dev, int which, int n, double* cycles_per_op);
 
 /* ---- synthetic corpora (host, deterministic) ------------------------------

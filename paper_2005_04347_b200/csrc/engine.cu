@@ -719,7 +719,12 @@ int asnn_dev_latency_probe(asnn_dev* dev, int which, int n, double* cycles_per_o
     DevBuf<float> sink;
     CK(c.alloc(1));
     CK(sink.alloc(1));
-    k_latency_probe<<<1, 32, 0, dev->stream>>>(which, n, 0.37f, c.p, sink.p);
+    void (*fns[])(int, float, long long*, float*) = {k_latency_probe<0>, k_latency_probe<1>,
+                                                      k_latency_probe<2>, k_latency_probe<3>,
+                                                      k_latency_probe<4>, k_latency_probe<5>,
+                                                      k_latency_probe<6>};
+    if (which < 0 || which > 6) return fail(dev, ASNN_E_INVALID, "probe index");
+    fns[which]<<<1, 32, 0, dev->stream>>>(n, 0.37f, c.p, sink.p);
     CK(cudaGetLastError());
     long long h = 0;
     CK(cudaMemcpyAsync(&h, c.p, 8, cudaMemcpyDeviceToHost, dev->stream));

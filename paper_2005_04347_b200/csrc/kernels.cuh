@@ -271,25 +271,36 @@ k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, f
 
 #include "cta.cuh"
 
-// Latency probes (one thread, dependent chains, clock64): which = 0 sigmoid32,
-// 1 DFMA, 2 FADD, 3 shared-memory load chain, 4 __ddiv_rn, 5 exp_glibc.
-__global__ void k_latency_probe(int which, int n, float seed, long long* cycles, float* sink) {
+// Latency probes (one thread, dependent chains, clock64), op templated and the
+// loop unrolled 8x so the loop branch is amortised:
+//   0 sigmoid32, 1 DFMA, 2 FADD, 3 shared-memory load chain, 4 double
+//   division, 5 exp, 6 an empty loop iteration (branch + counter).
+template <int W>
+__device__ __forceinline__ void probe_op(float& f, double& d, uint32_t& p, const uint32_t* chain) {
+    if constexpr (W == 0) f = sigmoid32(f);
+    else if constexpr (W == 1) d = __fma_rn(d, 1.0000001, 1e-9);
+    else if constexpr (W == 2) f = __fadd_rn(f, 1e-7f);
+    else if constexpr (W == 3) p = chain[p & 255];
+    else if constexpr (W == 4) d = __ddiv_rn(1.0, __dadd_rn(1.0, d));
+    else if constexpr (W == 5) d = exp_glibc(__dmul_rn(-d, 1e-3), kExpTab);
+}
+
+template <int W>
+__global__ void k_latency_probe(int n, float seed, long long* cycles, float* sink) {
     __shared__ uint32_t chain[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) chain[i] = (i * 97 + 13) & 255;
     __syncthreads();
     if (threadIdx.x) return;
     float f = seed;
     double d = seed;
-    uint32_t p = static_cast<uint32_t>(seed);
+    uint32_t p = static_cast<uint32_t>(seed * 100);
     const long long t0 = clock64();
-    for (int i = 0; i < n; ++i) {
-        switch (which) {
-            case 0: f = sigmoid32(f); break;
-            case 1: d = __fma_rn(d, 1.0000001, 1e-9); break;
-            case 2: f = __fadd_rn(f, 1e-7f); break;
-            case 3: p = chain[p & 255]; break;
-            case 4: d = __ddiv_rn(1.0, __dadd_rn(1.0, d)); break;
-            default: d = exp_glibc(-d * 1e-3, kExpTab); break;
+    if constexpr (W == 6) {
+        for (int i = 0; i < n; ++i) asm volatile("" : "+r"(p));
+    } else {
+        for (int i = 0; i < n; i += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) probe_op<W>(f, d, p, chain);
         }
     }
     const long long t1 = clock64();

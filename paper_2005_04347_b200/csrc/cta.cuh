@@ -45,7 +45,7 @@ __device__ __forceinline__ void consumer_barrier(uint32_t n_threads) {
 
 // One layer's items for one thread: item it = (node i, column group q).
 // Rp / Ep point at the staged slot (shared memory) or at the global arrays.
-template <int V>
+template <int V, bool GUARD>
 __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const uint2* Ep, uint32_t e0,
                                             uint32_t a, uint32_t b, uint32_t C, uint32_t gshift,
                                             uint32_t pos_base, uint32_t n_pos, uint32_t zero_row,
@@ -56,9 +56,12 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
         uint32_t k = Rp[i] - e0;
         const uint32_t ke = Rp[i + 1] - e0;
         const float* Aq = As + q * V;
+        // GUARD: some predecessor of this layout has no position (hand-built
+        // layouts only); it reads the zero row
         auto row = [&](uint32_t pos) {
             const uint32_t p = pos - pos_base;
-            return (p < n_pos ? p : zero_row) * C;
+            if constexpr (GUARD) return (p < n_pos ? p : zero_row) * C;
+            else return p * C;
         };
         float acc[V];
 #pragma unroll
@@ -113,7 +116,7 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
 // edges are allocated with slack so the rounded-up copies stay in bounds.
 // lo_cat / le_cat: per network, layer boundaries as local positions and as
 // global edge indices ([n_layers + 1] entries from lo_base).
-template <int V>
+template <int V, bool GUARD>
 __global__ void __launch_bounds__(288)
 k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       const uint32_t* __restrict__ le_cat, const uint32_t* __restrict__ row_ptr,
@@ -201,11 +204,11 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
             const uint32_t* m = meta + 4 * s;
             const uint32_t a = m[0], b = m[1], e0 = m[2], off = m[3];
             if (off != kNotStaged)
-                layer_items<V>(As, rb + s * RB + (off & 0xFF), eb + s * EB + (off >> 8), e0, a, b, C,
-                               gshift, n.pos_base, n.n_pos, max_pos, tid, Tc);
+                layer_items<V, GUARD>(As, rb + s * RB + (off & 0xFF), eb + s * EB + (off >> 8), e0, a,
+                                      b, C, gshift, n.pos_base, n.n_pos, max_pos, tid, Tc);
             else
-                layer_items<V>(As, row_ptr + n.pos_base + a, edges, 0, a, b, C, gshift, n.pos_base,
-                               n.n_pos, max_pos, tid, Tc);
+                layer_items<V, GUARD>(As, row_ptr + n.pos_base + a, edges, 0, a, b, C, gshift,
+                                      n.pos_base, n.n_pos, max_pos, tid, Tc);
             consumer_barrier(Tc);  // layer l visible to every consumer
             if (tid == 0) heavy::mbar_arrive(&empty[s]);
         }

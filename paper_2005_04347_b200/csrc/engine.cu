@@ -95,6 +95,7 @@ __global__ void k_edges(MetaPtrs m, const uint32_t* __restrict__ in_ids, const f
         // A predecessor without a position reads its never-written 0.0f slot,
         // exactly like the reference's zero-initialised op array.
         pos = (q == kUnassigned) ? zero_row : q;
+        if (q == kUnassigned) atomicOr(bad, 8u);  // not an error: K-cta keeps its guard
     }
     edges[k] = make_uint2(pos, __float_as_uint(w[k]));
 }
@@ -320,8 +321,12 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
             const uint64_t R = 1ull << rs;
             return as_bytes + R * (ebs * 8ull + p.RB * 4ull + 2 * 8 + 16);
         };
+        // deepest ring that keeps the CTAs-per-SM the activations alone allow
+        const uint64_t per_sm = 228ull * 1024;
+        const uint64_t fit = std::max<uint64_t>(1, per_sm / (as_bytes + 1024));
+        const uint64_t budget = std::min<uint64_t>(kMaxDynSmem, per_sm / fit - 1024);
         uint32_t rs = 4;
-        while (rs > 2 && smem_for(eb, rs) > kMaxDynSmem) --rs;
+        while (rs > 1 && smem_for(eb, rs) > budget) --rs;
         while (smem_for(eb, rs) > kMaxDynSmem && eb > 64) {  // stage fewer edges; big layers read global
             eb = (eb / 2) & ~1u;                              // stays even: 16-byte aligned slots
         }
@@ -537,11 +542,12 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
     CKL(cudaMemcpyAsync(&L->max_deg, maxdeg.p, 4, cudaMemcpyDeviceToHost, st));
     CKL(cudaStreamSynchronize(st));
 #undef CKL
-    if (h_bad[0]) {
+    if (h_bad[0] & 7u) {
         delete L;
         return fail(dev, ASNN_E_INVALID,
                     "layout references an id >= id_bound (code " + std::to_string(h_bad[0]) + ")");
     }
+    L->zero_refs = (h_bad[0] & 8u) != 0;
     L->row_ptr = std::move(flat.row_ptr);
     L->node_ids = std::move(flat.node_ids);
     L->nets = std::move(nets);
@@ -576,7 +582,8 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
     const CtaPlan cp = cta_plan(L, ldA);
     if (cp.use) {
         // the whole sweep (sensors + every layer) of each (network, slice) in one CTA
-        auto fn = cp.V == 4 ? k_cta<4> : k_cta<1>;
+        auto fn = cp.V == 4 ? (L->zero_refs ? k_cta<4, true> : k_cta<4, false>)
+                            : (L->zero_refs ? k_cta<1, true> : k_cta<1, false>);
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(cp.smem)));
         // cp.T consumer threads + one producer warp

@@ -165,6 +165,7 @@ struct asnn_dev_layout {
     asnn_b200::DevBuf<uint32_t> le_cat;    // per net: layer offsets as global edge indices
     uint32_t max_pos = 0;                  // largest network (positions)
     uint32_t max_level_edges = 0;          // most edges into one layer of one network
+    bool zero_refs = false;                // some predecessor has no position (zero row)
 
     ~asnn_dev_layout() { graph.reset(); }
 };

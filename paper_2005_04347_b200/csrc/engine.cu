@@ -679,6 +679,31 @@ int run_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out, fl
     if (!(g.exec && g.n_vec == n_vec && g.x == x && g.out == out && g.state == state &&
           g.stream == st && g.epoch == dev->option_epoch)) {
         g.reset();
+        // L2 persistence for the front of the activation array: positions are
+        // level-sorted, so the earliest layers -- the sources most later rows
+        // gather from -- sit at the start of A (ASNN_L2_PERSIST_MB, 0 = off).
+        {
+            static const long want_mb = [] {
+                const char* s = getenv("ASNN_L2_PERSIST_MB");
+                return s ? atol(s) : 0L;
+            }();
+            cudaStreamAttrValue av{};
+            if (want_mb > 0) {
+                int max_persist = 0;
+                cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev->device);
+                const size_t bytes = std::min<size_t>(static_cast<size_t>(want_mb) << 20,
+                                                      static_cast<size_t>(max_persist));
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes);
+                av.accessPolicyWindow.base_ptr = L->A.p;
+                av.accessPolicyWindow.num_bytes = std::min(bytes, L->A.n * sizeof(float));
+                av.accessPolicyWindow.hitRatio = 1.0f;
+                av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            }
+            cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av);
+            cudaStreamSetAttribute(dev->aux, cudaStreamAttributeAccessPolicyWindow, &av);
+            cudaGetLastError();
+        }
         cudaGraph_t graph = nullptr;
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         rc = launch_sweep(L, x, n_vec, out, state, st);

@@ -45,11 +45,14 @@ __device__ __forceinline__ void consumer_barrier(uint32_t n_threads) {
 
 // One layer's items for one thread: item it = (node i, column group q).
 // Rp / Ep point at the staged slot (shared memory) or at the global arrays.
+// As holds the slice's activations with row stride ld; position p lives in
+// row p - row_base (shared memory: the network's rows, row_base = pos_base;
+// global/L2 mode: the whole A, row_base = 0, As already offset by c0).
 template <int V, bool GUARD>
 __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const uint2* Ep, uint32_t e0,
-                                            uint32_t a, uint32_t b, uint32_t C, uint32_t gshift,
-                                            uint32_t pos_base, uint32_t n_pos, uint32_t zero_row,
-                                            uint32_t tid, uint32_t T) {
+                                            uint32_t a, uint32_t b, uint32_t ld, uint32_t gshift,
+                                            uint32_t pos_base, uint32_t row_base, uint32_t n_pos,
+                                            uint32_t zero_row, uint32_t tid, uint32_t T) {
     const uint32_t groups_mask = (1u << gshift) - 1u;
     for (uint32_t it = tid; it < ((b - a) << gshift); it += T) {
         const uint32_t i = it >> gshift, q = it & groups_mask;
@@ -58,10 +61,10 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
         const float* Aq = As + q * V;
         // GUARD: some predecessor of this layout has no position (hand-built
         // layouts only); it reads the zero row
-        auto row = [&](uint32_t pos) {
-            const uint32_t p = pos - pos_base;
-            if constexpr (GUARD) return (p < n_pos ? p : zero_row) * C;
-            else return p * C;
+        auto row = [&](uint32_t pos) -> size_t {
+            const uint32_t p = pos - row_base;
+            if constexpr (GUARD) return static_cast<size_t>(p - (pos_base - row_base) < n_pos ? p : zero_row) * ld;
+            else return static_cast<size_t>(p) * ld;
         };
         float acc[V];
 #pragma unroll
@@ -97,7 +100,7 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
 #pragma unroll
             for (int v = 0; v < V; ++v) acc[v] = mac(acc[v], __uint_as_float(ed.y), src[v]);
         }
-        float* dst = As + (a + i) * C + q * V;
+        float* dst = As + static_cast<size_t>(pos_base - row_base + a + i) * ld + q * V;
         if constexpr (V == 4) {
             *reinterpret_cast<float4*>(dst) =
                 make_float4(sigmoid32(acc[0]), sigmoid32(acc[1]), sigmoid32(acc[2]), sigmoid32(acc[3]));
@@ -110,13 +113,16 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
 }  // namespace cta
 
 // Block = consumer warps + 1 producer warp (the last).  Shared memory:
-// As[(max_pos+1)*C, 16-B rounded; row max_pos is zeros] | eb[R][EB] uint2 |
-// rb[R][RB] u32 | full[R], empty[R] u64 | meta[R][4] u32.
+// [As[(max_pos+1)*C, 16-B rounded; row max_pos is zeros] unless GLOBAL] |
+// eb[R][EB] uint2 | rb[R][RB] u32 | full[R], empty[R] u64 | meta[R][4] u32.
 // EB is even and RB a multiple of 4 (16-byte aligned slots); row_ptr and
 // edges are allocated with slack so the rounded-up copies stay in bounds.
 // lo_cat / le_cat: per network, layer boundaries as local positions and as
 // global edge indices ([n_layers + 1] entries from lo_base).
-template <int V, bool GUARD>
+// GLOBAL: the activations stay in A (L2-resident when A fits in L2) so a CTA
+// can own C columns whose rows would not fit in shared memory -- one wave of
+// CTAs instead of several for deep networks with wide batches (config 3).
+template <int V, bool GUARD, bool GLOBAL>
 __global__ void __launch_bounds__(288)
 k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       const uint32_t* __restrict__ le_cat, const uint32_t* __restrict__ row_ptr,
@@ -127,17 +133,20 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     using namespace cta;
     const uint32_t kRing = 1u << ring_shift, ring_mask = kRing - 1u;
     extern __shared__ __align__(128) unsigned char cta_smem[];
-    float* As = reinterpret_cast<float*>(cta_smem);
-    // row max_pos of As is all zeros: predecessors without a position (ids the
-    // layout does not hold) read 0.0f like the reference's untouched op slots
-    uint2* eb = reinterpret_cast<uint2*>(As + ((static_cast<size_t>(max_pos + 1) * C + 3) & ~size_t(3)));
+    const CtaNet n = nets[blockIdx.y];
+    const uint32_t c0 = blockIdx.x * C;
+    // activations: shared-memory rows of this network (row max_pos is the
+    // zero row for predecessors without a position), or A itself
+    float* As = GLOBAL ? A + c0 : reinterpret_cast<float*>(cta_smem);
+    const uint32_t ld = GLOBAL ? ldA : C;
+    const uint32_t row_base = GLOBAL ? 0u : n.pos_base;
+    const size_t as_floats = GLOBAL ? 0 : ((static_cast<size_t>(max_pos + 1) * C + 3) & ~size_t(3));
+    uint2* eb = reinterpret_cast<uint2*>(reinterpret_cast<float*>(cta_smem) + as_floats);
     uint32_t* rb = reinterpret_cast<uint32_t*>(eb + kRing * EB);
     uint64_t* full = reinterpret_cast<uint64_t*>(rb + kRing * RB);
     uint64_t* empty = full + kRing;
     uint32_t* meta = reinterpret_cast<uint32_t*>(empty + kRing);
 
-    const CtaNet n = nets[blockIdx.y];
-    const uint32_t c0 = blockIdx.x * C;
     const uint32_t groups = C / V;  // column groups per row (a power of two)
     const uint32_t gshift = __ffs(groups) - 1;
     const uint32_t Tc = blockDim.x - 32;  // consumer threads
@@ -183,7 +192,8 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
             }
         }
     } else {
-        for (uint32_t c = tid; c < C; c += Tc) As[max_pos * C + c] = 0.0f;
+        if constexpr (!GLOBAL)
+            for (uint32_t c = tid; c < C; c += Tc) As[max_pos * C + c] = 0.0f;
         // sensors: eval.cpp:17 (sigmoided input values), overlapping the staging
         for (uint32_t i = tid; i < (n.n_sensors << gshift); i += Tc) {
             const uint32_t s = i >> gshift, q = i & (groups - 1);
@@ -194,7 +204,7 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                 float xv = 0.0f;
                 if (col < n_vec && k != kUnassigned)
                     xv = x[static_cast<uint64_t>(n_vec) * n.in_prefix + static_cast<uint64_t>(col) * n.n_in + k];
-                As[s * C + q * V + v] = sigmoid32(xv);
+                As[static_cast<size_t>(n.pos_base - row_base + s) * ld + q * V + v] = sigmoid32(xv);
             }
         }
         consumer_barrier(Tc);
@@ -205,14 +215,15 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
             const uint32_t a = m[0], b = m[1], e0 = m[2], off = m[3];
             if (off != kNotStaged)
                 layer_items<V, GUARD>(As, rb + s * RB + (off & 0xFF), eb + s * EB + (off >> 8), e0, a,
-                                      b, C, gshift, n.pos_base, n.n_pos, max_pos, tid, Tc);
+                                      b, ld, gshift, n.pos_base, row_base, n.n_pos, max_pos, tid, Tc);
             else
-                layer_items<V, GUARD>(As, row_ptr + n.pos_base + a, edges, 0, a, b, C, gshift,
-                                      n.pos_base, n.n_pos, max_pos, tid, Tc);
+                layer_items<V, GUARD>(As, row_ptr + n.pos_base + a, edges, 0, a, b, ld, gshift,
+                                      n.pos_base, row_base, n.n_pos, max_pos, tid, Tc);
             consumer_barrier(Tc);  // layer l visible to every consumer
             if (tid == 0) heavy::mbar_arrive(&empty[s]);
         }
     }
+    if constexpr (GLOBAL) return;  // the activations are already in A
     __syncthreads();
 
     // write back: every row (state requested) or only the declared outputs

@@ -298,6 +298,7 @@ uint32_t default_heavy_threshold() {
 struct CtaPlan {
     bool use = false;
     uint32_t C = 0, V = 1, T = 32, smem = 0, EB = 0, RB = 0, ring_shift = 2;
+    bool global = false;  // activations in A (L2) instead of shared memory
 };
 
 constexpr uint32_t kMaxDynSmem = 227 * 1024;
@@ -338,6 +339,29 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
             break;
         }
         if (C == 1) break;
+    }
+    // Global (L2-resident) variant for one network whose shared-memory slices
+    // would need more than one wave of CTAs: C columns per CTA with the
+    // activations in A (which must fit in L2), so ldA / C <= #SMs.
+    const uint64_t a_bytes = (static_cast<uint64_t>(L->total_pos) + 1) * ldA * 4;
+    const uint32_t sms = static_cast<uint32_t>(L->dev->sm_count);
+    const uint64_t smem_waves =
+        p.C ? (static_cast<uint64_t>(ldA / p.C) * L->nets.size() +
+               sms * std::max<uint64_t>(1, (228ull * 1024) / (p.smem + 1024)) - 1) /
+                  (sms * std::max<uint64_t>(1, (228ull * 1024) / (p.smem + 1024)))
+             : ~0ull;
+    if (L->nets.size() == 1 && smem_waves > 1 && a_bytes <= (96ull << 20) && !L->zero_refs) {
+        uint32_t C = 1;
+        while (ldA / C > sms && C < 128) C <<= 1;
+        p.C = C;
+        p.global = true;
+        p.EB = (std::min<uint32_t>(std::max<uint32_t>(L->max_level_edges, 1), 4096) + 1 + 1) & ~1u;
+        p.ring_shift = 4;
+        p.smem = static_cast<uint32_t>((1ull << p.ring_shift) * (p.EB * 8ull + p.RB * 4ull + 2 * 8 + 16));
+        while (p.smem > kMaxDynSmem && p.ring_shift > 1) {
+            --p.ring_shift;
+            p.smem = static_cast<uint32_t>((1ull << p.ring_shift) * (p.EB * 8ull + p.RB * 4ull + 2 * 8 + 16));
+        }
     }
     if (!p.C) return p;
     p.V = p.C >= 4 ? 4 : 1;
@@ -582,8 +606,9 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
     const CtaPlan cp = cta_plan(L, ldA);
     if (cp.use) {
         // the whole sweep (sensors + every layer) of each (network, slice) in one CTA
-        auto fn = cp.V == 4 ? (L->zero_refs ? k_cta<4, true> : k_cta<4, false>)
-                            : (L->zero_refs ? k_cta<1, true> : k_cta<1, false>);
+        auto fn = cp.global ? (cp.V == 4 ? k_cta<4, false, true> : k_cta<1, false, true>)
+                  : cp.V == 4 ? (L->zero_refs ? k_cta<4, true, false> : k_cta<4, false, false>)
+                              : (L->zero_refs ? k_cta<1, true, false> : k_cta<1, false, false>);
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(cp.smem)));
         // cp.T consumer threads + one producer warp

@@ -180,7 +180,7 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                 m[0] = a;
                 m[1] = b;
                 m[2] = e0;
-                if (rbytes <= RB * 4 && ebytes <= EB * 8) {
+                if (rbytes <= RB * 4 && ebytes <= EB * 8 && !(write_all & 2)) {
                     m[3] = (r0 - r0a) | ((e0 - e0a) << 8);
                     expect_tx(&full[s], rbytes + ebytes);
                     bulk_g2s(rb + s * RB, row_ptr + r0a, rbytes, &full[s]);
@@ -229,7 +229,7 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     // write back: every row (state requested) or only the declared outputs
     const uint32_t T = blockDim.x;
     const uint32_t ncols = min(C, ldA - c0);
-    if (write_all) {
+    if (write_all & 1) {
         for (uint32_t i = tid; i < n.n_pos * ncols; i += T) {
             const uint32_t p = i / ncols, c = i - p * ncols;
             A[static_cast<uint64_t>(n.pos_base + p) * ldA + c0 + c] = As[p * C + c];

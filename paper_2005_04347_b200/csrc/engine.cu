@@ -303,6 +303,17 @@ struct CtaPlan {
 
 constexpr uint32_t kMaxDynSmem = 227 * 1024;
 
+// ASNN_CTA_DEBUG (timing experiments only): 2 = no layer staging (read row
+// pointers and edges from global memory).
+int cta_debug_flags() {
+    static int f = -1;
+    if (f < 0) {
+        const char* s = getenv("ASNN_CTA_DEBUG");
+        f = s ? (atoi(s) & 2) : 0;
+    }
+    return f;
+}
+
 CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     CtaPlan p;
     const uint32_t mode = L->dev->sweep_mode;  // 0 auto, 1 layer launches, 2 K-cta when it fits
@@ -350,7 +361,14 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
                sms * std::max<uint64_t>(1, (228ull * 1024) / (p.smem + 1024)) - 1) /
                   (sms * std::max<uint64_t>(1, (228ull * 1024) / (p.smem + 1024)))
              : ~0ull;
-    if (L->nets.size() == 1 && smem_waves > 1 && a_bytes <= (96ull << 20) && !L->zero_refs) {
+    // Off by default: on C3 it measured 5.6 ms against 4.2 ms for the two
+    // shared-memory waves (profiles/r1_cta_modes.txt); ASNN_CTA_GLOBAL=1 enables.
+    static const bool want_global = [] {
+        const char* s = getenv("ASNN_CTA_GLOBAL");
+        return s && s[0] == '1';
+    }();
+    if (want_global && L->nets.size() == 1 && smem_waves > 1 && a_bytes <= (96ull << 20) &&
+        !L->zero_refs) {
         uint32_t C = 1;
         while (ldA / C > sms && C < 128) C <<= 1;
         p.C = C;
@@ -615,7 +633,7 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T + 32, cp.smem, st>>>(
             reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->le_cat.p, L->row_ptr.p,
             L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos, cp.EB, cp.RB,
-            cp.ring_shift, state ? 1 : 0);
+            cp.ring_shift, (state ? 1 : 0) | cta_debug_flags());
     } else {
         if (L->total_sensors)
             k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(

@@ -380,7 +380,10 @@ def run_ours(args, cfg):
                          "frac": achieved / peak, "traffic": profiled_traffic(cfg),
                          "peak_source": peak_src,
                          "alg_bytes_per_step": plan["alg_bytes"],
-                         "kernel": "k_level (one launch per dependency level)",
+                         "kernel": {"rows": "k_rows + k_heavy (one launch each per dependency level)",
+                                    "segments": "k_rows (heavy rows split across levels) per dependency level",
+                                    "k_cta": "k_cta (one CTA per network x batch slice, whole sweep)"}
+                                   [plan["strategy"]],
                          "kernel_ms_per_step": level_ms, "launches_per_step": len(prof),
                          "max_launch_ms": float(prof.max()),
                          "sweep_achieved_gbs": plan["alg_bytes"] / (ms / 1e3) / 1e9},

@@ -127,9 +127,12 @@ int asnn_dev_synchronize(asnn_dev* dev);
  * Numerics are identical either way; this is a scheduling knob. */
 int asnn_dev_set_heavy_threshold(asnn_dev* dev, uint32_t min_in_degree);
 /* Sweep strategy: 0 = automatic (default, $ASNN_SWEEP_MODE), 1 = one launch
- * per dependency level, 2 = one CTA per (network, batch slice) running every
- * level with shared-memory-resident activations whenever they fit.  Also a
- * scheduling knob: results are identical. */
+ * per dependency level (for one network with a batch of 64 or a multiple of
+ * 128, heavy rows are split into segments that run in the levels of their
+ * sources), 2 = one CTA per (network, batch slice) running every level with
+ * shared-memory-resident activations whenever they fit, 3 = one launch per
+ * level with whole rows only.  Also a scheduling knob: results are
+ * identical. */
 int asnn_dev_set_sweep_mode(asnn_dev* dev, uint32_t mode);
 int asnn_dev_last_timings(const asnn_dev* dev, asnn_timings* out);
 
@@ -201,6 +204,13 @@ int asnn_dev_profile_sweep(asnn_dev_layout* layout, const float* x_dev, uint32_t
  * algorithmic bytes it moves. */
 int asnn_dev_activate_plan(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* kernels,
                            uint64_t* alg_bytes, uint64_t* conn_evals);
+
+/* Which sweep strategy an activate of n_vec vectors uses: 0 = per-level
+ * launches of whole rows (k_rows / k_level, heavy rows on k_heavy), 1 =
+ * per-level launches with heavy rows split into segments across the levels of
+ * their sources (k_rows, long segments on k_heavy), 2 = one CTA per (network,
+ * batch slice) for the whole sweep (k_cta). */
+int asnn_dev_sweep_kind(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* kind);
 
 /* The device's sigmoid32 (network.hpp:54-59) over n host floats, for
  * exhaustive parity checks of the epilogue. */

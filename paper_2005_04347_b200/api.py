@@ -299,7 +299,9 @@ class Device:
         self.check(self.lib.asnn_dev_synchronize(self.h))
 
     def set_sweep_mode(self, mode: int):
-        """0 automatic, 1 one launch per level, 2 one CTA per (network, slice)."""
+        """0 automatic, 1 one launch per level (heavy rows split across levels
+        where eligible), 2 one CTA per (network, slice), 3 one launch per level
+        with whole rows only."""
         self.check(self.lib.asnn_dev_set_sweep_mode(self.h, int(mode)))
 
     def set_heavy_threshold(self, min_in_degree: Optional[int]):
@@ -439,11 +441,14 @@ class DeviceLayout:
         k, b, ce = C.c_uint32(), C.c_uint64(), C.c_uint64()
         self.dev.check(self.dev.lib.asnn_dev_activate_plan(self.h, n_vec, C.byref(k), C.byref(b),
                                                            C.byref(ce)))
-        return {"kernels": k.value, "alg_bytes": b.value, "conn_evals": ce.value}
+        kind = C.c_uint32()
+        self.dev.check(self.dev.lib.asnn_dev_sweep_kind(self.h, n_vec, C.byref(kind)))
+        return {"kernels": k.value, "alg_bytes": b.value, "conn_evals": ce.value,
+                "strategy": ("rows", "segments", "k_cta")[kind.value]}
 
     def profile(self, x_ptr: int, n_vec: int, out_ptr: int) -> np.ndarray:
-        """Per-launch device ms of one sweep (sensors, levels, gather)."""
-        k = self.plan(n_vec)["kernels"]
+        """Per-stage device ms of one sweep (sensors, each level, gather)."""
+        k = self.plan(n_vec)["kernels"] + 2 * self.info()["total_layers"] + 2
         ms = np.zeros(k, np.float32)
         n = C.c_uint32()
         self.dev.check(self.dev.lib.asnn_dev_profile_sweep(

@@ -8,6 +8,16 @@
 
 namespace asnn_b200 {
 
+
+// Row segments (uint4 {row, first edge, end edge, aux}): a heavy row's stored
+// edges split across the levels whose sources they need.  aux: kAccLoad =
+// start from the partial sum in accbuf[slot], kAccStore = leave the partial
+// sum there instead of finishing the row; slot = aux & kSlotMask.  The fp32
+// accumulation is the same sequence of roundings as one uninterrupted sum.
+constexpr uint32_t kAccLoad = 0x80000000u;
+constexpr uint32_t kAccStore = 0x40000000u;
+constexpr uint32_t kSlotMask = 0x3FFFFFFFu;
+
 // The 2^(i/128) table of exp_glibc (tools/gen_exp_table.py).
 static __device__ const uint64_t kExpTab[256] = {
 #include "exp_table.inc"

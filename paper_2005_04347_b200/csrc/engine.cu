@@ -197,51 +197,66 @@ uint32_t padded_batch(uint32_t n_vec) {
     return (n_vec + 127) / 128 * 128;
 }
 
+// One launch per level: k_level (row items, any batch width) or k_rows (row
+// segments + row items, 4 columns per lane).
+using LevelFn = void (*)(const uint32_t*, const uint2*, float*, uint32_t, const uint32_t*, uint32_t, uint32_t);
+using RowsFn = void (*)(const uint32_t*, const uint2*, float*, uint32_t, const uint32_t*, uint32_t, uint32_t,
+                        const uint4*, uint32_t, float*);
 struct LevelLaunch {
-    void (*fn)(const uint32_t*, const uint2*, float*, uint32_t, const uint32_t*, uint32_t, uint32_t);
-    uint32_t lanes;
-    uint32_t tiles;
+    LevelFn lvl = nullptr;
+    RowsFn rows = nullptr;
+    uint32_t lanes = 1;
+    uint32_t tiles = 1;
 };
 
-// ASNN_LEVEL_VARIANT (tuning experiments; profiles/r1_level_variants.txt):
-// 1 = 8 gathers in flight, 4 blocks/SM (64 registers; the default), 0 = 8 in
-// flight, unconstrained (74 registers, 3 blocks/SM), 2 = 16 in flight and
-// 2 blocks/SM, 3 = 16 in flight and 3 blocks/SM, 4 = 4 in flight, 6 blocks/SM.
+// ASNN_LEVEL_VARIANT (tuning experiments; profiles/r1_level_variants.txt,
+// profiles/r1_light_variants.txt): 5 = k_rows, 8 gathers in flight, 4
+// blocks/SM (the default); 6/7/8 = k_rows with 8/12/16 in flight at 3/3/2
+// blocks/SM; 0..4 = k_level (8 in flight unconstrained, 8 at 4 blocks/SM,
+// 16 at 2, 16 at 3, 4 at 6).
 int level_variant() {
     static int v = -1;
     if (v < 0) {
         const char* s = getenv("ASNN_LEVEL_VARIANT");
-        v = s ? atoi(s) : 1;
+        v = s ? atoi(s) : 5;
     }
     return v;
 }
 
 template <int LANES>
 LevelLaunch wide_level(uint32_t tiles) {
+    LevelLaunch l;
+    l.lanes = LANES;
+    l.tiles = tiles;
     switch (level_variant()) {
-        case 0: return {k_level<4, LANES, 8, 1>, LANES, tiles};
-        case 2: return {k_level<4, LANES, 16, 2>, LANES, tiles};
-        case 3: return {k_level<4, LANES, 16, 3>, LANES, tiles};
-        case 4: return {k_level<4, LANES, 4, 6>, LANES, tiles};
-        default: return {k_level<4, LANES, 8, 4>, LANES, tiles};
+        case 0: l.lvl = k_level<4, LANES, 8, 1>; break;
+        case 1: l.lvl = k_level<4, LANES, 8, 4>; break;
+        case 2: l.lvl = k_level<4, LANES, 16, 2>; break;
+        case 3: l.lvl = k_level<4, LANES, 16, 3>; break;
+        case 4: l.lvl = k_level<4, LANES, 4, 6>; break;
+        case 6: l.rows = k_rows<LANES, 8, 3>; break;
+        case 7: l.rows = k_rows<LANES, 12, 3>; break;
+        case 8: l.rows = k_rows<LANES, 16, 2>; break;
+        default: l.rows = k_rows<LANES, 8, 4>; break;
     }
+    return l;
 }
 
 LevelLaunch level_launch_for(uint32_t ldA) {
     switch (ldA) {
-        case 1: return {k_level<1, 1>, 1, 1};
-        case 2: return {k_level<2, 1>, 1, 1};
-        case 4: return {k_level<4, 1>, 1, 1};
-        case 8: return {k_level<4, 2>, 2, 1};
-        case 16: return {k_level<4, 4>, 4, 1};
-        case 32: return {k_level<4, 8>, 8, 1};
+        case 1: return {k_level<1, 1>, nullptr, 1, 1};
+        case 2: return {k_level<2, 1>, nullptr, 1, 1};
+        case 4: return {k_level<4, 1>, nullptr, 1, 1};
+        case 8: return {k_level<4, 2>, nullptr, 2, 1};
+        case 16: return {k_level<4, 4>, nullptr, 4, 1};
+        case 32: return {k_level<4, 8>, nullptr, 8, 1};
         case 64: return wide_level<16>(1);
         default: return wide_level<32>(ldA / 128);
     }
 }
 
 struct HeavyLaunch {
-    void (*fn)(const uint32_t*, const uint2*, float*, uint32_t, const uint32_t*, uint32_t);
+    void (*fn)(const uint32_t*, const uint2*, float*, uint32_t, const uint32_t*, uint32_t, const uint4*, float*);
     uint32_t threads;
     uint32_t smem;
     uint32_t tiles;
@@ -316,8 +331,8 @@ int cta_debug_flags() {
 
 CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     CtaPlan p;
-    const uint32_t mode = L->dev->sweep_mode;  // 0 auto, 1 layer launches, 2 K-cta when it fits
-    if (mode == 1) return p;
+    const uint32_t mode = L->dev->sweep_mode;  // 0 auto, 1/3 layer launches, 2 K-cta when it fits
+    if (mode == 1 || mode == 3) return p;
     if (L->n_levels < 2 || L->max_pos == 0) return p;
     // +3 / +1 entries: the bulk copies start at 16-byte aligned indices
     p.RB = (std::min<uint32_t>(L->max_width + 1, 4096) + 3 + 3) & ~3u;
@@ -425,6 +440,7 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
         delete L;
         return fail(dev, ASNN_E_INVALID, "more than 2^32-1 stored edges");
     }
+
     L->total_pos = meta[0 * (G + 1) + G];
     L->total_idb = meta[1 * (G + 1) + G];
     L->total_in = meta[2 * (G + 1) + G];
@@ -605,6 +621,118 @@ namespace {
 template <typename Mark>
 int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark);
 
+// ---- heavy-row segments (segments.cuh) --------------------------------------
+// Shortest interrupted segment and longest segment k_rows takes (longer ones
+// stream through k_heavy): ASNN_SEG_MIN (default 64), ASNN_SEG_LONG (512).
+uint32_t env_u32(const char* name, uint32_t dflt) {
+    const char* s = getenv(name);
+    return s ? static_cast<uint32_t>(strtoul(s, nullptr, 10)) : dflt;
+}
+
+// One network, 4 columns per lane (batch 64 or a multiple of 128), a heavy
+// threshold, per-level launches not restricted to whole rows (sweep mode 3),
+// and not disabled (ASNN_SEGMENTS=0).
+bool seg_eligible(const asnn_dev_layout* L, uint32_t ldA) {
+    static const bool enabled = env_u32("ASNN_SEGMENTS", 1) != 0;
+    return enabled && L->nets.size() == 1 && L->dev->sweep_mode != 3 && level_launch_for(ldA).rows &&
+           heavy_launch_for(ldA).fn && heavy_index_for(L->dev->heavy_threshold) >= 0 &&
+           L->total_pos > L->total_sensors;
+}
+
+uint64_t seg_key_for(const asnn_dev_layout* L) {
+    return (static_cast<uint64_t>(heavy_index_for(L->dev->heavy_threshold)) << 48) ^
+           (static_cast<uint64_t>(env_u32("ASNN_SEG_MIN", 64)) << 24) ^ env_u32("ASNN_SEG_LONG", 512);
+}
+
+// Splits every heavy row of the (single) network into segments by the levels
+// of its sources; groups them by (short/long, step), longest first.
+int ensure_segments(asnn_dev_layout* L) {
+    asnn_dev* dev = L->dev;
+    cudaStream_t st = dev->stream;
+    const NetMeta& n = L->nets[0];
+    const int thr = heavy_index_for(dev->heavy_threshold);
+    const uint32_t NL = L->n_levels;
+    std::vector<uint32_t> hv_prefix(NL + 1, 0);
+    for (uint32_t l = 0; l < NL; ++l)
+        hv_prefix[l + 1] = hv_prefix[l] + (l ? L->heavy_cnt[thr * (NL + 1) + l] : 0u);
+    const uint32_t H = hv_prefix[NL];
+    L->seg_short_off.assign(NL + 1, 0);
+    L->seg_long_off.assign(NL + 1, 0);
+    L->n_slots = H;
+    L->seg_key = seg_key_for(L);
+    L->seg.reset();
+    if (!H) return ASNN_OK;
+    int lb = 0;
+    while ((1u << lb) <= NL) ++lb;
+    DevBuf<uint32_t> d_prefix, d_lvl_off, lo, hv_level, hv_sched, count, base, keys, vals, step_count;
+    DevBuf<uint4> tasks;
+    CK(d_prefix.alloc(NL + 1));
+    CK(d_lvl_off.alloc(NL + 1));
+    CK(lo.alloc(n.layer_offsets.size()));
+    CK(hv_level.alloc(H));
+    CK(hv_sched.alloc(H));
+    CK(count.alloc(H + 1));
+    CK(base.alloc(H + 1));
+    CK(step_count.alloc(2 * (n.n_layers + 1)));
+    CK(cudaMemcpyAsync(d_prefix.p, hv_prefix.data(), (NL + 1) * 4ull, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_lvl_off.p, L->lvl_off.data(), (NL + 1) * 4ull, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(lo.p, n.layer_offsets.data(), n.layer_offsets.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(count.p + H, 0, 4, st));
+    CK(cudaMemsetAsync(step_count.p, 0, 2 * (n.n_layers + 1) * 4ull, st));
+    k_heavy_rows<<<blocks_for(H), kThreads, 0, st>>>(d_prefix.p, d_lvl_off.p, NL, H, hv_level.p, hv_sched.p);
+    SegArgs a{};
+    a.row_ptr = L->row_ptr.p;
+    a.edges = L->edges.p;
+    a.lo = lo.p;
+    a.nl = n.n_layers;
+    a.sched = L->sched.p;
+    a.hv_level = hv_level.p;
+    a.hv_sched = hv_sched.p;
+    a.n_heavy = H;
+    a.min_len = std::max<uint32_t>(1, env_u32("ASNN_SEG_MIN", 64));
+    a.long_len = env_u32("ASNN_SEG_LONG", 512);
+    a.lb = static_cast<uint32_t>(lb);
+    a.count = count.p;
+    k_segments<0><<<blocks_for(static_cast<uint64_t>(H) * 32), kThreads, 0, st>>>(a);
+    CK(cudaGetLastError());
+    int rc = exclusive_scan(dev, count.p, base.p, H + 1, nullptr, st);
+    if (rc) return rc;
+    uint32_t total = 0;
+    CK(cudaMemcpyAsync(&total, base.p + H, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(tasks.alloc(total));
+    CK(keys.alloc(total));
+    CK(vals.alloc(total));
+    a.base = base.p;
+    a.tasks = tasks.p;
+    a.keys = keys.p;
+    a.vals = vals.p;
+    a.step_count = step_count.p;
+    k_segments<1><<<blocks_for(static_cast<uint64_t>(H) * 32), kThreads, 0, st>>>(a);
+    CK(cudaGetLastError());
+    SortBuffers sb;
+    uint32_t *ks = nullptr, *vs = nullptr;
+    rc = radix_sort_pairs(dev, keys.p, vals.p, total, lb + 17, sb, &ks, &vs, st);
+    if (rc) return rc;
+    CK(L->seg.alloc(total));
+    k_gather_tasks<<<blocks_for(total), kThreads, 0, st>>>(tasks.p, vs, total, L->seg.p);
+    CK(cudaGetLastError());
+    std::vector<uint32_t> sc(2 * (n.n_layers + 1));
+    CK(cudaMemcpyAsync(sc.data(), step_count.p, sc.size() * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    // sorted order: all short (step ascending), then all long
+    uint32_t acc = 0;
+    for (uint32_t l = 0; l <= NL; ++l) {
+        L->seg_short_off[l] = acc;
+        if (l < NL && l <= n.n_layers) acc += sc[l];
+    }
+    for (uint32_t l = 0; l <= NL; ++l) {
+        L->seg_long_off[l] = acc;
+        if (l < NL && l <= n.n_layers) acc += sc[(n.n_layers + 1) + l];
+    }
+    return ASNN_OK;
+}
+
 #define RC_(expr)          \
     do {                   \
         int _r = (expr);   \
@@ -661,6 +789,9 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
     const LevelLaunch ll = level_launch_for(ldA);
     const HeavyLaunch hl = heavy_launch_for(ldA);
     const int thr = heavy_index_for(dev->heavy_threshold);
+    const bool segs = seg_eligible(L, ldA);
+    if (segs && L->seg_key != seg_key_for(L))
+        return fail(dev, ASNN_E_INVALID, "internal: row segments not prepared");
     if (dev->fork_ev.size() < L->n_levels) {
         for (size_t i = dev->fork_ev.size(); i < L->n_levels; ++i) {
             cudaEvent_t a, b;
@@ -670,26 +801,54 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
             dev->join_ev.push_back(b);
         }
     }
+    int prio = 0;
+    cudaStreamGetPriority(dev->aux, &prio);
+    auto launch_heavy = [&](uint32_t l, uint32_t count, const uint32_t* sched, const uint4* seg) -> int {
+        CK(cudaEventRecord(dev->fork_ev[l], st));
+        CK(cudaStreamWaitEvent(dev->aux, dev->fork_ev[l], 0));
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributePriority;
+        attr[0].val.priority = prio;
+        cfg.gridDim = dim3(count * hl.tiles);
+        cfg.blockDim = dim3(hl.threads);
+        cfg.dynamicSmemBytes = hl.smem;
+        cfg.stream = dev->aux;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, hl.fn, static_cast<const uint32_t*>(L->row_ptr.p),
+                              static_cast<const uint2*>(L->edges.p), L->A.p, ldA, sched, hl.tiles, seg,
+                              L->accbuf.p));
+        return ASNN_OK;
+    };
     for (uint32_t l = 1; l < L->n_levels; ++l) {
         const uint32_t n = L->lvl_off[l + 1] - L->lvl_off[l];
-        if (!n) continue;
-        // rows above the threshold stream through k_heavy on the aux branch,
-        // concurrently with the light rows on the main stream
+        // heavy rows of this level: whole rows on k_heavy, or (segmented)
+        // segments of heavy rows of this and later levels
         const uint32_t nh = (hl.fn && thr >= 0) ? L->heavy_cnt[thr * (L->n_levels + 1) + l] : 0;
+        const uint32_t ns = segs ? L->seg_short_off[l + 1] - L->seg_short_off[l] : 0;
+        const uint32_t nlong = segs ? L->seg_long_off[l + 1] - L->seg_long_off[l] : 0;
+        if (!n && !ns && !nlong) continue;
         if (L->total_sensors || l > 1) mark();
-        if (nh) {
-            CK(cudaEventRecord(dev->fork_ev[l], st));
-            CK(cudaStreamWaitEvent(dev->aux, dev->fork_ev[l], 0));
-            hl.fn<<<nh * hl.tiles, hl.threads, hl.smem, dev->aux>>>(
-                L->row_ptr.p, L->edges.p, L->A.p, ldA, L->sched.p + L->lvl_off[l], hl.tiles);
+        const bool fork = segs ? nlong > 0 : nh > 0;
+        if (fork) {
+            const int rc = segs ? launch_heavy(l, nlong, nullptr, L->seg.p + L->seg_long_off[l])
+                                : launch_heavy(l, nh, L->sched.p + L->lvl_off[l], nullptr);
+            if (rc) return rc;
         }
-        if (n > nh) {
-            const uint64_t items = static_cast<uint64_t>(n - nh) * ll.tiles;
-            ll.fn<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(
-                L->row_ptr.p, L->edges.p, L->A.p, ldA, L->sched.p + L->lvl_off[l] + nh,
-                static_cast<uint32_t>(items), ll.tiles);
+        const uint32_t nrows = n - nh;
+        if (nrows || ns) {
+            const uint64_t items = static_cast<uint64_t>(nrows + ns) * ll.tiles;
+            if (ll.rows)
+                ll.rows<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(
+                    L->row_ptr.p, L->edges.p, L->A.p, ldA, L->sched.p + L->lvl_off[l] + nh, nrows, ll.tiles,
+                    segs ? L->seg.p + L->seg_short_off[l] : nullptr, ns, L->accbuf.p);
+            else
+                ll.lvl<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(
+                    L->row_ptr.p, L->edges.p, L->A.p, ldA, L->sched.p + L->lvl_off[l] + nh,
+                    static_cast<uint32_t>(items), ll.tiles);
         }
-        if (nh) {
+        if (fork) {
             CK(cudaEventRecord(dev->join_ev[l], dev->aux));
             CK(cudaStreamWaitEvent(st, dev->join_ev[l], 0));
         }
@@ -701,6 +860,17 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
 int ensure_workspace(asnn_dev_layout* L, uint32_t n_vec) {
     asnn_dev* dev = L->dev;
     const uint32_t ldA = padded_batch(n_vec);
+    if (seg_eligible(L, ldA)) {
+        if (L->seg_key != seg_key_for(L)) {
+            L->graph.reset();
+            const int rc = ensure_segments(L);
+            if (rc) return rc;
+        }
+        if (L->accbuf.n < static_cast<size_t>(L->n_slots) * ldA) {
+            L->graph.reset();
+            CK(L->accbuf.alloc(static_cast<size_t>(L->n_slots) * ldA));
+        }
+    }
     // +1 row: the never-written zero row for predecessors without a position.
     const size_t need = (static_cast<size_t>(L->total_pos) + 1) * ldA;
     if (need > L->A.n) {
@@ -860,8 +1030,17 @@ int asnn_dev_open(int device, asnn_dev** out) {
     }
     dev->stream = dev->own_stream;
     dev->heavy_threshold = default_heavy_threshold();
-    if (const char* m = getenv("ASNN_SWEEP_MODE")) dev->sweep_mode = static_cast<uint32_t>(atoi(m)) % 3;
-    if (cudaStreamCreateWithFlags(&dev->aux, cudaStreamNonBlocking) != cudaSuccess) {
+    if (const char* m = getenv("ASNN_SWEEP_MODE")) dev->sweep_mode = static_cast<uint32_t>(atoi(m)) % 4;
+    // The heavy-row branch gets the highest stream priority: its CTAs carry
+    // the longest dependent-add chains of the layer and must become resident
+    // before the light rows fill the machine (ASNN_HEAVY_PRIO=0 disables).
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    {
+        const char* hp = getenv("ASNN_HEAVY_PRIO");
+        if (hp && atoi(hp) == 0) prio_hi = prio_lo;
+    }
+    if (cudaStreamCreateWithPriority(&dev->aux, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
         cudaGetLastError();
         delete dev;
         return ASNN_E_UNAVAILABLE;
@@ -895,7 +1074,7 @@ int asnn_dev_set_stream(asnn_dev* dev, void* s) {
 void* asnn_dev_get_stream(asnn_dev* dev) { return dev ? dev->stream : nullptr; }
 
 int asnn_dev_set_sweep_mode(asnn_dev* dev, uint32_t mode) {
-    if (!dev || mode > 2) return ASNN_E_INVALID;
+    if (!dev || mode > 3) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
     dev->sweep_mode = mode;
     ++dev->option_epoch;
@@ -1081,6 +1260,32 @@ int asnn_dev_layout_download(asnn_dev_layout* L, uint32_t g, uint32_t* layer_off
     return ASNN_OK;
 }
 
+// Kernels one sweep launches (stages = false) or the stages profile_sweep
+// brackets with events (stages = true: sensors, one per level, output gather).
+static uint32_t sweep_launches(asnn_dev_layout* L, uint32_t n_vec, bool stages) {
+    uint32_t k = 0;
+    const uint32_t ldA = padded_batch(n_vec);
+    if (cta_plan(L, ldA).use) {
+        k = 1;  // K-cta runs sensors and every layer
+    } else {
+        const int thr = heavy_index_for(L->dev->heavy_threshold);
+        const bool heavy = heavy_launch_for(ldA).fn && thr >= 0;
+        const bool segs = seg_eligible(L, ldA);
+        if (segs && L->seg_key != seg_key_for(L)) ensure_segments(L);
+        k = L->total_sensors ? 1 : 0;
+        for (uint32_t l = 1; l < L->n_levels; ++l) {
+            const uint32_t n = L->lvl_off[l + 1] - L->lvl_off[l];
+            const uint32_t nh = heavy ? L->heavy_cnt[thr * (L->n_levels + 1) + l] : 0;
+            const uint32_t ns = segs ? L->seg_short_off[l + 1] - L->seg_short_off[l] : 0;
+            const uint32_t nl = segs ? L->seg_long_off[l + 1] - L->seg_long_off[l] : 0;
+            if (stages) k += (n || ns || nl) ? 1 : 0;
+            else if (segs) k += (n - nh + ns > 0) + (nl > 0);
+            else k += (n > nh) + (nh > 0);
+        }
+    }
+    return k + (L->total_out ? 1 : 0);
+}
+
 int asnn_dev_profile_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_vec, float* out_dev,
                            float* ms, uint32_t* n_launches) {
     if (!L || !ms || !n_launches) return ASNN_E_INVALID;
@@ -1089,9 +1294,7 @@ int asnn_dev_profile_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_ve
     CK(cudaSetDevice(dev->device));
     int rc = ensure_workspace(L, n_vec);
     if (rc) return rc;
-    uint32_t k = 0;
-    rc = asnn_dev_activate_plan(L, n_vec, &k, nullptr, nullptr);
-    if (rc) return rc;
+    uint32_t k = sweep_launches(L, n_vec, true);
     if (!out_dev) k -= L->total_out ? 1 : 0;
     std::vector<cudaEvent_t> evs(k + 1);
     for (auto& e : evs) CK(cudaEventCreate(&e));
@@ -1108,19 +1311,19 @@ int asnn_dev_profile_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_ve
 int asnn_dev_activate_plan(asnn_dev_layout* L, uint32_t n_vec, uint32_t* kernels, uint64_t* alg_bytes,
                            uint64_t* conn_evals) {
     if (!L) return ASNN_E_INVALID;
-    uint32_t k = 0;
-    if (cta_plan(L, padded_batch(n_vec)).use) {
-        k = 1;  // K-cta runs sensors and every layer
-    } else {
-        k = L->total_sensors ? 1 : 0;
-        for (uint32_t l = 1; l < L->n_levels; ++l) k += (L->lvl_off[l + 1] > L->lvl_off[l]);
-    }
-    k += L->total_out ? 1 : 0;
+    const uint32_t k = sweep_launches(L, n_vec, false);
     if (kernels) *kernels = k;
     const uint64_t B = n_vec, E = L->total_edges, N = L->total_pos;
     // 8E (col+w) + 4(N+1) row_ptr + 4EB gathers + 4NB writes + 4 n_in B reads
     if (alg_bytes) *alg_bytes = 8 * E + 4 * (N + 1) + 4 * E * B + 4 * N * B + 4ull * L->total_in * B;
     if (conn_evals) *conn_evals = E * B;
+    return ASNN_OK;
+}
+
+int asnn_dev_sweep_kind(asnn_dev_layout* L, uint32_t n_vec, uint32_t* kind) {
+    if (!L || !kind) return ASNN_E_INVALID;
+    const uint32_t ldA = padded_batch(n_vec);
+    *kind = cta_plan(L, ldA).use ? 2u : seg_eligible(L, ldA) ? 1u : 0u;
     return ASNN_OK;
 }
 

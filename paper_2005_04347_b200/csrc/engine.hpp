@@ -167,6 +167,15 @@ struct asnn_dev_layout {
     uint32_t max_level_edges = 0;          // most edges into one layer of one network
     bool zero_refs = false;                // some predecessor has no position (zero row)
 
+    // Heavy-row segments (one network; segments.cuh): short ones run in k_rows
+    // ahead of the level's rows, long ones in k_heavy
+    asnn_b200::DevBuf<uint4> seg;          // {row, first edge, end edge, aux}
+    std::vector<uint32_t> seg_short_off;   // [n_levels + 1] short segments of each step
+    std::vector<uint32_t> seg_long_off;    // [n_levels + 1] long segments of each step
+    uint32_t n_slots = 0;                  // partial-sum slots (heavy rows)
+    uint64_t seg_key = ~0ull;              // options they were cut for
+    asnn_b200::DevBuf<float> accbuf;       // [n_slots][ldA] partial sums
+
     ~asnn_dev_layout() { graph.reset(); }
 };
 

@@ -128,6 +128,96 @@ k_level(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
 }
 
 // ---------------------------------------------------------------------------
+// K-rows: the lean form of K-act-lane for 4 columns per lane (batch >= 64).
+// Same arithmetic as k_level, fewer instructions per gathered row: every
+// lane reads the edge record itself (all lanes of the group hit the same L1
+// line: one broadcast load, no shuffles), the edge line two batches ahead is
+// prefetched into L1, and each of the U source-row gathers is one 128-bit
+// load straight into registers.  Per edge and lane: 1 L1 load, 1 address
+// IMAD, 1 gather, 4 FMUL + 4 FADD.
+//
+// Items: the first n_seg are row segments (uint4 {row, first edge, end edge,
+// aux}, see stream.cuh: a heavy row's edges split across the levels whose
+// sources they need, the partial sum carried in accbuf), then n_rows whole
+// rows sched[0..n_rows); each item runs on `tiles` column tiles.
+template <int LANES, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+k_rows(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
+       float* __restrict__ A, uint32_t ldA, const uint32_t* __restrict__ sched,
+       uint32_t n_rows, uint32_t tiles, const uint4* __restrict__ seg, uint32_t n_seg,
+       float* __restrict__ accbuf) {
+    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t item = gt / LANES;
+    const uint32_t ni = item / tiles;
+    if (ni >= n_seg + n_rows) return;  // uniform across the LANES group
+    const uint32_t lane = threadIdx.x % LANES;
+    const uint32_t tile = item - ni * tiles;
+    uint32_t node, beg, end, aux = 0;
+    if (ni < n_seg) {
+        const uint4 t = __ldg(&seg[ni]);
+        node = t.x, beg = t.y, end = t.z, aux = t.w;
+    } else {
+        node = __ldg(&sched[ni - n_seg]);
+        beg = __ldg(&row_ptr[node]);
+        end = __ldg(&row_ptr[node + 1]);
+    }
+    const uint32_t col = tile * (LANES * 4) + lane * 4;
+    const uint32_t stride = ldA * 4u;
+    const char* __restrict__ Acol = reinterpret_cast<const char*>(A + col);
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    if (aux & kAccLoad) {
+        const float4 p = *reinterpret_cast<const float4*>(accbuf + static_cast<uint64_t>(aux & kSlotMask) * ldA + col);
+        a0 = p.x, a1 = p.y, a2 = p.z, a3 = p.w;
+    }
+    for (uint32_t k = beg; k < end; k += U) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(edges + k + 2 * U));
+        float4 v[U];
+        float w[U];
+        const uint32_t n = min(static_cast<uint32_t>(U), end - k);
+        if (n == U) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint2 e = __ldg(&edges[k + u]);
+                w[u] = __uint_as_float(e.y);
+                v[u] = __ldg(reinterpret_cast<const float4*>(Acol + static_cast<uint64_t>(e.x) * stride));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                a0 = mac(a0, w[u], v[u].x);
+                a1 = mac(a1, w[u], v[u].y);
+                a2 = mac(a2, w[u], v[u].z);
+                a3 = mac(a3, w[u], v[u].w);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (static_cast<uint32_t>(u) < n) {
+                    const uint2 e = __ldg(&edges[k + u]);
+                    w[u] = __uint_as_float(e.y);
+                    v[u] = __ldg(reinterpret_cast<const float4*>(Acol + static_cast<uint64_t>(e.x) * stride));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (static_cast<uint32_t>(u) < n) {
+                    a0 = mac(a0, w[u], v[u].x);
+                    a1 = mac(a1, w[u], v[u].y);
+                    a2 = mac(a2, w[u], v[u].z);
+                    a3 = mac(a3, w[u], v[u].w);
+                }
+            }
+        }
+    }
+    if (aux & kAccStore) {
+        *reinterpret_cast<float4*>(accbuf + static_cast<uint64_t>(aux & kSlotMask) * ldA + col) =
+            make_float4(a0, a1, a2, a3);
+    } else {
+        *reinterpret_cast<float4*>(A + static_cast<uint64_t>(node) * ldA + col) =
+            make_float4(sigmoid32(a0), sigmoid32(a1), sigmoid32(a2), sigmoid32(a3));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K-act-heavy: one CTA per (high in-degree node, column tile).  The serial
 // fp32 sum of a node cannot be split without changing its rounding, so the
 // row is streamed instead: two producer warps copy predecessor rows with
@@ -175,7 +265,8 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
 template <int TC>
 __global__ void __launch_bounds__(32 * heavy::kProducers + (TC < 32 ? 32 : TC))
 k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, float* __restrict__ A,
-        uint32_t ldA, const uint32_t* __restrict__ sched, uint32_t tiles) {
+        uint32_t ldA, const uint32_t* __restrict__ sched, uint32_t tiles, const uint4* __restrict__ seg,
+        float* __restrict__ accbuf) {
     using namespace heavy;
     extern __shared__ __align__(128) unsigned char smem[];
     float* ring = reinterpret_cast<float*>(smem);                         // [S][R][TC]
@@ -186,9 +277,16 @@ k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, f
     constexpr int kPieces = TC / 4;  // 16-byte pieces per row
 
     const uint32_t item = blockIdx.x;
-    const uint32_t node = sched[item / tiles];
     const uint32_t tile = item % tiles;
-    const uint32_t beg = row_ptr[node], end = row_ptr[node + 1];
+    // a whole row sched[i], or a row segment seg[i] (common.cuh)
+    uint32_t node, beg, end, aux = 0;
+    if (seg) {
+        const uint4 t = seg[item / tiles];
+        node = t.x, beg = t.y, end = t.z, aux = t.w;
+    } else {
+        node = sched[item / tiles];
+        beg = row_ptr[node], end = row_ptr[node + 1];
+    }
     const uint32_t n_chunks = (end - beg + kRows - 1) / kRows;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -248,6 +346,8 @@ k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, f
         // ---- consumers: thread = one batch column of the tile ----
         const int col = threadIdx.x;
         float acc = 0.0f;
+        if ((aux & kAccLoad) && col < TC)
+            acc = accbuf[static_cast<uint64_t>(aux & kSlotMask) * ldA + tile * TC + col];
         for (uint32_t c = 0; c < n_chunks; ++c) {
             const int s = c % kStages;
             mbar_wait(&full[s], (c / kStages) & 1);
@@ -265,11 +365,15 @@ k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, f
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }
-        if (col < TC) A[static_cast<uint64_t>(node) * ldA + tile * TC + col] = sigmoid32(acc);
+        if (col < TC) {
+            if (aux & kAccStore) accbuf[static_cast<uint64_t>(aux & kSlotMask) * ldA + tile * TC + col] = acc;
+            else A[static_cast<uint64_t>(node) * ldA + tile * TC + col] = sigmoid32(acc);
+        }
     }
 }
 
 #include "cta.cuh"
+#include "segments.cuh"
 
 // Latency probes (one thread, dependent chains, clock64), op templated and the
 // loop unrolled 8x so the loop branch is amortised:

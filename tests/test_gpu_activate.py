@@ -20,10 +20,12 @@ pytestmark = pytest.mark.gpu
 DEV = A.ParallelConfig(backend=A.Backend.DeviceCompute)
 
 
-@pytest.fixture(params=[1, 2], ids=["layer-launches", "k_cta"])
+@pytest.fixture(params=[1, 2, 3], ids=["layer-launches", "k_cta", "whole-rows"])
 def sweep_mode(request):
-    """Run a test under both sweep strategies: one launch per dependency level
-    (k_level/k_heavy) and the one-CTA-per-slice sweep (k_cta)."""
+    """Run a test under every sweep strategy: one launch per dependency level
+    (heavy rows split into segments where eligible), the one-CTA-per-slice
+    sweep (k_cta), and per-level launches of whole rows (k_rows/k_level +
+    k_heavy)."""
     dev = A.Device.get(0)
     dev.set_sweep_mode(request.param)
     yield request.param

@@ -200,8 +200,8 @@ uint32_t padded_batch(uint32_t n_vec) {
 // One launch per level: k_level (row items, any batch width) or k_rows (row
 // segments + row items, 4 columns per lane).
 using LevelFn = void (*)(const uint32_t*, const uint2*, float*, uint32_t, const uint32_t*, uint32_t, uint32_t);
-using RowsFn = void (*)(const uint32_t*, const uint2*, float*, uint32_t, const uint32_t*, uint32_t, uint32_t,
-                        const uint4*, uint32_t, float*);
+using RowsFn = void (*)(const uint2*, float*, uint32_t, const uint4*, uint32_t, uint32_t, const uint4*, uint32_t,
+                        float*);
 struct LevelLaunch {
     LevelFn lvl = nullptr;
     RowsFn rows = nullptr;
@@ -545,6 +545,9 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
         CKL(L->sched.alloc(P - S + 1));
         if (P > S)
             CKL(cudaMemcpyAsync(L->sched.p, vs + S, (P - S) * 4ull, cudaMemcpyDeviceToDevice, st));
+        CKL(L->rtask.alloc(P - S + 1));
+        if (P > S)
+            k_row_tasks<<<blocks_for(P - S), kThreads, 0, st>>>(L->sched.p, flat.row_ptr.p, P - S, L->rtask.p);
         // heavy-row counts per level for each threshold kHeavyThr[t]
         const size_t nh = static_cast<size_t>(kNumHeavyThr) * (n_levels + 1);
         CKL(hv.alloc(nh));
@@ -841,7 +844,7 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
             const uint64_t items = static_cast<uint64_t>(nrows + ns) * ll.tiles;
             if (ll.rows)
                 ll.rows<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(
-                    L->row_ptr.p, L->edges.p, L->A.p, ldA, L->sched.p + L->lvl_off[l] + nh, nrows, ll.tiles,
+                    L->edges.p, L->A.p, ldA, L->rtask.p + L->lvl_off[l] + nh, nrows, ll.tiles,
                     segs ? L->seg.p + L->seg_short_off[l] : nullptr, ns, L->accbuf.p);
             else
                 ll.lvl<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(

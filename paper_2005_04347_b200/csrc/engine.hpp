@@ -147,6 +147,7 @@ struct asnn_dev_layout {
     asnn_b200::DevBuf<uint32_t> row_ptr;    // [total_pos + 1]
     asnn_b200::DevBuf<uint2> edges;         // [total_edges] {src pos, w bits}
     asnn_b200::DevBuf<uint32_t> sched;      // [total_pos] level-major schedule
+    asnn_b200::DevBuf<uint4> rtask;         // [total_pos - sensors] {row, first edge, end edge, 0} per sched entry
     asnn_b200::DevBuf<uint4> sinfo;         // [total_sensors]
     asnn_b200::DevBuf<uint4> oinfo;         // [total_out]
     asnn_b200::DevBuf<uint32_t> state_map;  // [total_idb] id -> pos

@@ -137,30 +137,24 @@ k_level(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
 // IMAD, 1 gather, 4 FMUL + 4 FADD.
 //
 // Items: the first n_seg are row segments (uint4 {row, first edge, end edge,
-// aux}, see stream.cuh: a heavy row's edges split across the levels whose
-// sources they need, the partial sum carried in accbuf), then n_rows whole
-// rows sched[0..n_rows); each item runs on `tiles` column tiles.
+// aux}, common.cuh / segments.cuh: a heavy row's edges split across the
+// levels whose sources they need, the partial sum carried in accbuf), then
+// n_rows whole rows (the same record with aux = 0, in schedule order); each
+// item runs on `tiles` column tiles.
 template <int LANES, int U, int MINB>
 __global__ void __launch_bounds__(256, MINB)
-k_rows(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
-       float* __restrict__ A, uint32_t ldA, const uint32_t* __restrict__ sched,
-       uint32_t n_rows, uint32_t tiles, const uint4* __restrict__ seg, uint32_t n_seg,
-       float* __restrict__ accbuf) {
+k_rows(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ldA,
+       const uint4* __restrict__ rows, uint32_t n_rows, uint32_t tiles, const uint4* __restrict__ seg,
+       uint32_t n_seg, float* __restrict__ accbuf) {
     const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t item = gt / LANES;
     const uint32_t ni = item / tiles;
     if (ni >= n_seg + n_rows) return;  // uniform across the LANES group
     const uint32_t lane = threadIdx.x % LANES;
     const uint32_t tile = item - ni * tiles;
-    uint32_t node, beg, end, aux = 0;
-    if (ni < n_seg) {
-        const uint4 t = __ldg(&seg[ni]);
-        node = t.x, beg = t.y, end = t.z, aux = t.w;
-    } else {
-        node = __ldg(&sched[ni - n_seg]);
-        beg = __ldg(&row_ptr[node]);
-        end = __ldg(&row_ptr[node + 1]);
-    }
+    // one 16-byte task record per item (no sched -> row_ptr dependent loads)
+    const uint4 t = ni < n_seg ? __ldg(&seg[ni]) : __ldg(&rows[ni - n_seg]);
+    const uint32_t node = t.x, beg = t.y, end = t.z, aux = t.w;
     const uint32_t col = tile * (LANES * 4) + lane * 4;
     const uint32_t stride = ldA * 4u;
     const char* __restrict__ Acol = reinterpret_cast<const char*>(A + col);

@@ -126,3 +126,13 @@ __global__ void k_heavy_rows(const uint32_t* __restrict__ hv_prefix, const uint3
     hv_level[h] = a;
     hv_sched[h] = lvl_off[a] + (h - hv_prefix[a]);
 }
+
+// Whole-row task records in schedule order: rtask[i] = {sched[i], row_ptr of
+// it, row_ptr of the next position, 0}.
+__global__ void k_row_tasks(const uint32_t* __restrict__ sched, const uint32_t* __restrict__ row_ptr, uint32_t n,
+                            uint4* __restrict__ rtask) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t p = sched[i];
+    rtask[i] = make_uint4(p, row_ptr[p], row_ptr[p + 1], 0u);
+}

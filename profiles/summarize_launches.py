@@ -29,7 +29,7 @@ def load(path):
 
 
 def main():
-    keep = ("k_level", "k_heavy", "k_sense", "k_gather_out", "k_state", "k_cta")
+    keep = ("k_level", "k_rows", "k_heavy", "k_sense", "k_gather_out", "k_state", "k_cta")
     launches = [l for l in load(sys.argv[1])
                 if l["name"].replace("void ", "").split("::")[-1].split("<")[0] in keep]
     # the last sweep starts at the last k_sense launch

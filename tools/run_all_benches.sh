@@ -1,6 +1,8 @@
 #!/bin/bash
-# Round-end evidence run (one GPU): GPU tests, every config's bench line with
-# its CPU baseline, the default bench invocation and the reference arm.
+# Evidence run (one GPU): GPU tests, every config's bench line with its CPU
+# baseline, the default bench invocation, the reference arm, the ncu launch
+# lists of C4/C2 (per-kernel shares, DRAM traffic per sweep) and one full ncu
+# capture of the dominant kernel (k_rows on a middle C4 level).
 set -u
 mkdir -p gpurun_out
 python -m pytest tests/ -q -m gpu > gpurun_out/pytest_gpu.txt 2>&1; tail -1 gpurun_out/pytest_gpu.txt
@@ -11,5 +13,10 @@ for C in c1 c2 c3 c5; do
 done
 python bench.py 2>/dev/null | tail -1 > gpurun_out/bench_c4.json          # the driver's default invocation
 python bench.py --impl reference --steps 5 --warmup 3 2>/dev/null | tail -1 > gpurun_out/bench_c4_reference.json
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+for C in c4 c2; do
+  ncu --metrics $M --clock-control none --csv --log-file gpurun_out/${C}_launches.csv python bench.py --config $C --ncu-sweeps 2 > /dev/null 2>&1
+done
+ncu --set full --clock-control none --import-source on -k regex:k_rows -s 120 -c 1 -o gpurun_out/c4_k_rows python bench.py --config c4 --ncu-sweeps 1 > /dev/null 2>&1
 python tools/latency_probe.py > gpurun_out/latency.json 2>&1
 ls -la gpurun_out

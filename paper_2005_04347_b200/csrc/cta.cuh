@@ -129,7 +129,7 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,
       const uint4* __restrict__ oinfo, const float* __restrict__ x, uint32_t n_vec,
       float* __restrict__ A, uint32_t ldA, uint32_t C, uint32_t max_pos, uint32_t EB, uint32_t RB,
-      uint32_t ring_shift, int write_all) {
+      uint32_t ring_shift, int write_all, float* __restrict__ out) {
     using namespace cta;
     const uint32_t kRing = 1u << ring_shift, ring_mask = kRing - 1u;
     extern __shared__ __align__(128) unsigned char cta_smem[];
@@ -194,18 +194,18 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     } else {
         if constexpr (!GLOBAL)
             for (uint32_t c = tid; c < C; c += Tc) As[max_pos * C + c] = 0.0f;
-        // sensors: eval.cpp:17 (sigmoided input values), overlapping the staging
-        for (uint32_t i = tid; i < (n.n_sensors << gshift); i += Tc) {
-            const uint32_t s = i >> gshift, q = i & (groups - 1);
+        // sensors: eval.cpp:17 (sigmoided input values), overlapping the staging.
+        // One (column, sensor) per thread, sensor fastest: a column's inputs
+        // are contiguous in x ([vector][input]), so the reads coalesce (they
+        // may cross the host link when x is mapped host memory).
+        for (uint32_t i = tid; i < n.n_sensors * C; i += Tc) {
+            const uint32_t c = i / n.n_sensors, s = i - c * n.n_sensors;
             const uint32_t k = sinfo[n.sens_prefix + s].w;
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-                const uint32_t col = c0 + q * V + v;
-                float xv = 0.0f;
-                if (col < n_vec && k != kUnassigned)
-                    xv = x[static_cast<uint64_t>(n_vec) * n.in_prefix + static_cast<uint64_t>(col) * n.n_in + k];
-                As[static_cast<size_t>(n.pos_base - row_base + s) * ld + q * V + v] = sigmoid32(xv);
-            }
+            const uint32_t col = c0 + c;
+            float xv = 0.0f;
+            if (col < n_vec && k != kUnassigned)
+                xv = x[static_cast<uint64_t>(n_vec) * n.in_prefix + static_cast<uint64_t>(col) * n.n_in + k];
+            As[static_cast<size_t>(n.pos_base - row_base + s) * ld + c] = sigmoid32(xv);
         }
         consumer_barrier(Tc);
         for (uint32_t l = 1; l < n.n_layers; ++l) {
@@ -233,6 +233,18 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
         for (uint32_t i = tid; i < n.n_pos * ncols; i += T) {
             const uint32_t p = i / ncols, c = i - p * ncols;
             A[static_cast<uint64_t>(n.pos_base + p) * ldA + c0 + c] = As[p * C + c];
+        }
+    } else if (out) {
+        // read_outputs (eval.cpp:82-87) straight from shared memory into the
+        // caller's [net][vector][output] buffer (device or mapped host memory):
+        // no output gather launch, and the writes of finished CTAs overlap the
+        // sweeps of the others
+        const uint32_t vcols = c0 < n_vec ? min(C, n_vec - c0) : 0u;
+        for (uint32_t i = tid; i < n.n_out * vcols; i += T) {
+            const uint32_t c = i / n.n_out, j = i - c * n.n_out;
+            const uint32_t pos = oinfo[n.out_prefix + j].x;
+            out[static_cast<uint64_t>(n_vec) * n.out_prefix + static_cast<uint64_t>(c0 + c) * n.n_out + j] =
+                pos != kUnassigned ? As[(pos - n.pos_base) * C + c] : 0.0f;
         }
     } else {
         for (uint32_t i = tid; i < n.n_out * ncols; i += T) {

@@ -753,6 +753,8 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
     };
     mark();
     const CtaPlan cp = cta_plan(L, ldA);
+    // K-cta writes the declared outputs itself (shared-memory variant, no state)
+    const bool cta_out = cp.use && !cp.global && !state && out && L->total_out;
     if (cp.use) {
         // the whole sweep (sensors + every layer) of each (network, slice) in one CTA
         auto fn = cp.global ? (cp.V == 4 ? k_cta<4, false, true> : k_cta<1, false, true>)
@@ -764,14 +766,14 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T + 32, cp.smem, st>>>(
             reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->le_cat.p, L->row_ptr.p,
             L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos, cp.EB, cp.RB,
-            cp.ring_shift, (state ? 1 : 0) | cta_debug_flags());
+            cp.ring_shift, (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr);
     } else {
         if (L->total_sensors)
             k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(
                 L->sinfo.p, L->total_sensors, x, n_vec, L->A.p, ldA);
         RC_(launch_levels(L, ldA, st, mark));
     }
-    if (out && L->total_out) {
+    if (out && L->total_out && !cta_out) {
         mark();
         k_gather_out<<<blocks_for(static_cast<uint64_t>(L->total_out) * n_vec), kThreads, 0, st>>>(
             L->oinfo.p, L->total_out, L->A.p, ldA, n_vec, out);
@@ -951,6 +953,17 @@ bool is_pinned(const void* p) {
     }
     return a.type == cudaMemoryTypeHost;
 }
+
+// Device-visible address of page-locked, mapped host memory (UVA), or null.
+void* mapped_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 
 }  // namespace
 
@@ -1265,11 +1278,14 @@ int asnn_dev_layout_download(asnn_dev_layout* L, uint32_t g, uint32_t* layer_off
 
 // Kernels one sweep launches (stages = false) or the stages profile_sweep
 // brackets with events (stages = true: sensors, one per level, output gather).
-static uint32_t sweep_launches(asnn_dev_layout* L, uint32_t n_vec, bool stages) {
+static uint32_t sweep_launches(asnn_dev_layout* L, uint32_t n_vec, bool stages, bool with_out = true) {
     uint32_t k = 0;
     const uint32_t ldA = padded_batch(n_vec);
-    if (cta_plan(L, ldA).use) {
-        k = 1;  // K-cta runs sensors and every layer
+    const CtaPlan cp = cta_plan(L, ldA);
+    if (cp.use) {
+        // K-cta runs sensors and every layer, and writes the outputs itself
+        // unless it is the global-memory variant
+        return 1u + (with_out && cp.global && L->total_out ? 1u : 0u);
     } else {
         const int thr = heavy_index_for(L->dev->heavy_threshold);
         const bool heavy = heavy_launch_for(ldA).fn && thr >= 0;
@@ -1286,7 +1302,7 @@ static uint32_t sweep_launches(asnn_dev_layout* L, uint32_t n_vec, bool stages) 
             else k += (n > nh) + (nh > 0);
         }
     }
-    return k + (L->total_out ? 1 : 0);
+    return k + (with_out && L->total_out ? 1 : 0);
 }
 
 int asnn_dev_profile_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_vec, float* out_dev,
@@ -1297,8 +1313,7 @@ int asnn_dev_profile_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_ve
     CK(cudaSetDevice(dev->device));
     int rc = ensure_workspace(L, n_vec);
     if (rc) return rc;
-    uint32_t k = sweep_launches(L, n_vec, true);
-    if (!out_dev) k -= L->total_out ? 1 : 0;
+    const uint32_t k = sweep_launches(L, n_vec, true, out_dev != nullptr);
     std::vector<cudaEvent_t> evs(k + 1);
     for (auto& e : evs) CK(cudaEventCreate(&e));
     rc = launch_sweep(L, x_dev, n_vec, out_dev, nullptr, dev->stream, &evs);
@@ -1360,6 +1375,22 @@ int asnn_dev_activate(asnn_dev_layout* L, const float* x, uint32_t n_vec, uint64
     CK(L->out_stage.ensure(static_cast<size_t>(L->total_out) * n_vec + 1));
     DevBuf<float> state_dev;
     if (state) CK(state_dev.alloc(static_cast<size_t>(L->total_idb) * n_vec));
+    // zero-copy: page-locked, mapped inputs / outputs used in place by the
+    // sweep's kernels (one graph launch, no copy operations; K-cta's reads and
+    // writes overlap the other CTAs' sweeps)
+    if (!state) {
+        void* xd = xb ? mapped_device_ptr(x) : nullptr;
+        void* od = (out && ob) ? mapped_device_ptr(out) : nullptr;
+        if ((xd || !xb) && (od || !(out && ob))) {
+            CK(cudaEventRecord(dev->ev0, st));
+            int rc = run_sweep(L, static_cast<const float*>(xd), n_vec, static_cast<float*>(od), nullptr);
+            if (rc) return rc;
+            CK(cudaEventRecord(dev->ev1, st));
+            CK(cudaEventSynchronize(dev->ev1));
+            cudaEventElapsedTime(&dev->timings.activate_ms, dev->ev0, dev->ev1);
+            return ASNN_OK;
+        }
+    }
     CK(cudaEventRecord(dev->ev0, st));
     if (xb) {
         const float* src = x;

@@ -27,10 +27,12 @@ constexpr uint32_t kUnassigned = 0xFFFFFFFFu;
 __global__ void k_sense(const uint4* __restrict__ sinfo, uint32_t n_sensors,
                         const float* __restrict__ x, uint32_t n_vec, float* __restrict__ A,
                         uint32_t ldA) {
+    // vector-major (sensor fastest): a vector's inputs are contiguous in x
     const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t s = idx / ldA;
-    const uint32_t b = static_cast<uint32_t>(idx - s * ldA);
-    if (s >= n_sensors) return;
+    const uint64_t b64 = idx / n_sensors;
+    const uint32_t s = static_cast<uint32_t>(idx - b64 * n_sensors);
+    const uint32_t b = static_cast<uint32_t>(b64);
+    if (b64 >= ldA) return;
     const uint4 si = sinfo[s];
     float xv = 0.0f;
     if (b < n_vec && si.w != kUnassigned)
@@ -417,10 +419,12 @@ __global__ void k_sigmoid_many(const float* __restrict__ x, float* __restrict__ 
 __global__ void k_gather_out(const uint4* __restrict__ oinfo, uint32_t n_total,
                              const float* __restrict__ A, uint32_t ldA, uint32_t n_vec,
                              float* __restrict__ out) {
+    // vector-major (output fastest): a vector's outputs are contiguous in out
     const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t o = idx / n_vec;
-    const uint32_t b = static_cast<uint32_t>(idx - o * n_vec);
-    if (o >= n_total) return;
+    const uint64_t b64 = idx / n_total;
+    const uint32_t o = static_cast<uint32_t>(idx - b64 * n_total);
+    const uint32_t b = static_cast<uint32_t>(b64);
+    if (b64 >= n_vec) return;
     const uint4 oi = oinfo[o];
     const float v = oi.x == kUnassigned ? 0.0f : A[static_cast<uint64_t>(oi.x) * ldA + b];
     out[static_cast<uint64_t>(n_vec) * oi.y + static_cast<uint64_t>(b) * oi.z + oi.w] = v;

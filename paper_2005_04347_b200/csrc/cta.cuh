@@ -24,7 +24,6 @@ struct CtaNet {
 };
 
 namespace cta {
-constexpr uint32_t kNotStaged = 0xFFFFFFFFu;
 
 __device__ __forceinline__ void expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
@@ -114,24 +113,28 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
 
 // Block = consumer warps + 1 producer warp (the last).  Shared memory:
 // [As[(max_pos+1)*C, 16-B rounded; row max_pos is zeros] unless GLOBAL] |
-// eb[R][EB] uint2 | rb[R][RB] u32 | full[R], empty[R] u64 | meta[R][4] u32.
-// EB is even and RB a multiple of 4 (16-byte aligned slots); row_ptr and
-// edges are allocated with slack so the rounded-up copies stay in bounds.
-// lo_cat / le_cat: per network, layer boundaries as local positions and as
-// global edge indices ([n_layers + 1] entries from lo_base).
-// GLOBAL: the activations stay in A (L2-resident when A fits in L2) so a CTA
-// can own C columns whose rows would not fit in shared memory -- one wave of
-// CTAs instead of several for deep networks with wide batches (config 3).
+// ring[ring_bytes] | full[kSlots], empty[kSlots] u64 | meta[kSlots][8] u32.
+// The ring is byte-granular: layer l's row pointers and edges (16-byte
+// aligned bulk copies) are packed at the producer's write offset, wrapping to
+// 0 when they do not fit before the end, so as many layers are in flight as
+// their sizes allow (up to kSlots) -- small layers no longer pay for a slot
+// sized by the largest one.  Layers larger than the ring (or every layer in
+// debug mode 2) are read from global memory.  Layer l uses mbarrier pair
+// (l-1) % kSlots for its ((l-1) / kSlots)-th time.
+namespace cta {
+constexpr uint32_t kSlots = 32;
+constexpr uint32_t kMetaBytes = kSlots * (8 + 8 + 32);
+}  // namespace cta
+
 template <int V, bool GUARD, bool GLOBAL>
 __global__ void __launch_bounds__(288)
 k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       const uint32_t* __restrict__ le_cat, const uint32_t* __restrict__ row_ptr,
       const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,
       const uint4* __restrict__ oinfo, const float* __restrict__ x, uint32_t n_vec,
-      float* __restrict__ A, uint32_t ldA, uint32_t C, uint32_t max_pos, uint32_t EB, uint32_t RB,
-      uint32_t ring_shift, int write_all, float* __restrict__ out) {
+      float* __restrict__ A, uint32_t ldA, uint32_t C, uint32_t max_pos, uint32_t ring_bytes,
+      int write_all, float* __restrict__ out) {
     using namespace cta;
-    const uint32_t kRing = 1u << ring_shift, ring_mask = kRing - 1u;
     extern __shared__ __align__(128) unsigned char cta_smem[];
     const CtaNet n = nets[blockIdx.y];
     const uint32_t c0 = blockIdx.x * C;
@@ -141,11 +144,10 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     const uint32_t ld = GLOBAL ? ldA : C;
     const uint32_t row_base = GLOBAL ? 0u : n.pos_base;
     const size_t as_floats = GLOBAL ? 0 : ((static_cast<size_t>(max_pos + 1) * C + 3) & ~size_t(3));
-    uint2* eb = reinterpret_cast<uint2*>(reinterpret_cast<float*>(cta_smem) + as_floats);
-    uint32_t* rb = reinterpret_cast<uint32_t*>(eb + kRing * EB);
-    uint64_t* full = reinterpret_cast<uint64_t*>(rb + kRing * RB);
-    uint64_t* empty = full + kRing;
-    uint32_t* meta = reinterpret_cast<uint32_t*>(empty + kRing);
+    unsigned char* ring = reinterpret_cast<unsigned char*>(reinterpret_cast<float*>(cta_smem) + as_floats);
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + ring_bytes);
+    uint64_t* empty = full + kSlots;
+    uint32_t* meta = reinterpret_cast<uint32_t*>(empty + kSlots);
 
     const uint32_t groups = C / V;  // column groups per row (a power of two)
     const uint32_t gshift = __ffs(groups) - 1;
@@ -153,7 +155,7 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     const uint32_t tid = threadIdx.x;
 
     if (tid == 0) {
-        for (uint32_t s = 0; s < kRing; ++s) {
+        for (uint32_t s = 0; s < kSlots; ++s) {
             heavy::mbar_init(&full[s], 1);
             heavy::mbar_init(&empty[s], 1);
         }
@@ -162,32 +164,64 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     __syncthreads();
 
     if (tid >= Tc) {
-        // producer: layer l (>= 1) lives in slot (l - 1) % R for its
-        // ((l - 1) / R)-th use
         if (tid == Tc) {
+            // producer.  meta[m] = {a, b, e0, staged, row index, edge index,
+            // extent} of the layer using slot m; the extent (its bytes plus
+            // the wasted tail when it wrapped) is what its release frees, so
+            // the live bytes are always [w - used, w) modulo the ring.
             const uint32_t* lo = lo_cat + n.lo_base;
             const uint32_t* le = le_cat + n.lo_base;
+            uint32_t w = 0;       // next write offset in the ring
+            uint32_t used = 0;    // bytes of layers in flight (incl. wrap gaps)
+            uint32_t oldest = 1;  // oldest layer whose release the producer has not seen
+            auto release_to = [&](uint32_t upto) {  // layers < upto are released
+                for (; oldest < upto; ++oldest) used -= meta[8 * ((oldest - 1) % kSlots) + 6];
+            };
             for (uint32_t l = 1; l < n.n_layers; ++l) {
-                const uint32_t s = (l - 1) & ring_mask, u = (l - 1) >> ring_shift;
+                const uint32_t m = (l - 1) % kSlots, u = (l - 1) / kSlots;
                 const uint32_t a = lo[l], b = lo[l + 1];
                 const uint32_t e0 = le[l], e1 = le[l + 1];
-                if (u > 0) heavy::mbar_wait(&empty[s], (u - 1) & 1);
                 const uint32_t r0 = n.pos_base + a, r0a = r0 & ~3u;
                 const uint32_t rbytes = ((b - a + 1 + (r0 - r0a)) * 4 + 15) & ~15u;
                 const uint32_t e0a = e0 & ~1u;
                 const uint32_t ebytes = ((e1 - e0 + (e0 - e0a)) * 8 + 15) & ~15u;
-                uint32_t* m = meta + 4 * s;
-                m[0] = a;
-                m[1] = b;
-                m[2] = e0;
-                if (rbytes <= RB * 4 && ebytes <= EB * 8 && !(write_all & 2)) {
-                    m[3] = (r0 - r0a) | ((e0 - e0a) << 8);
-                    expect_tx(&full[s], rbytes + ebytes);
-                    bulk_g2s(rb + s * RB, row_ptr + r0a, rbytes, &full[s]);
-                    if (ebytes) bulk_g2s(eb + s * EB, edges + e0a, ebytes, &full[s]);
+                const uint32_t size = rbytes + ebytes;
+                if (u > 0) {  // slot m's previous layer (l - kSlots) and all before it are released
+                    heavy::mbar_wait(&empty[m], (u - 1) & 1);
+                    release_to(l - kSlots + 1);
+                }
+                const bool staged = size <= ring_bytes && !(write_all & 2);
+                uint32_t at = 0, extent = 0;
+                if (staged) {
+                    for (;;) {
+                        if (used == 0) w = 0;
+                        const bool wrap = w + size > ring_bytes;
+                        const uint32_t need = wrap ? ring_bytes - w + size : size;
+                        if (need <= ring_bytes - used) {
+                            at = wrap ? 0u : w;
+                            extent = need;
+                            w = at + size;
+                            used += need;
+                            break;
+                        }
+                        heavy::mbar_wait(&empty[(oldest - 1) % kSlots], ((oldest - 1) / kSlots) & 1);
+                        release_to(oldest + 1);
+                    }
+                }
+                uint32_t* mm = meta + 8 * m;
+                mm[0] = a;
+                mm[1] = b;
+                mm[2] = e0;
+                mm[3] = staged ? 1u : 0u;
+                mm[4] = at / 4 + (r0 - r0a);
+                mm[5] = (at + rbytes) / 8 + (e0 - e0a);
+                mm[6] = extent;
+                if (staged) {
+                    expect_tx(&full[m], size);
+                    bulk_g2s(ring + at, row_ptr + r0a, rbytes, &full[m]);
+                    if (ebytes) bulk_g2s(ring + at + rbytes, edges + e0a, ebytes, &full[m]);
                 } else {
-                    m[3] = kNotStaged;
-                    heavy::mbar_arrive(&full[s]);
+                    heavy::mbar_arrive(&full[m]);
                 }
             }
         }
@@ -208,19 +242,21 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
             As[static_cast<size_t>(n.pos_base - row_base + s) * ld + c] = sigmoid32(xv);
         }
         consumer_barrier(Tc);
+        const uint32_t* ring_u32 = reinterpret_cast<const uint32_t*>(ring);
+        const uint2* ring_u2 = reinterpret_cast<const uint2*>(ring);
         for (uint32_t l = 1; l < n.n_layers; ++l) {
-            const uint32_t s = (l - 1) & ring_mask;
-            heavy::mbar_wait(&full[s], ((l - 1) >> ring_shift) & 1);
-            const uint32_t* m = meta + 4 * s;
-            const uint32_t a = m[0], b = m[1], e0 = m[2], off = m[3];
-            if (off != kNotStaged)
-                layer_items<V, GUARD>(As, rb + s * RB + (off & 0xFF), eb + s * EB + (off >> 8), e0, a,
-                                      b, ld, gshift, n.pos_base, row_base, n.n_pos, max_pos, tid, Tc);
+            const uint32_t m = (l - 1) % kSlots;
+            heavy::mbar_wait(&full[m], ((l - 1) / kSlots) & 1);
+            const uint32_t* mm = meta + 8 * m;
+            const uint32_t a = mm[0], b = mm[1], e0 = mm[2];
+            if (mm[3])
+                layer_items<V, GUARD>(As, ring_u32 + mm[4], ring_u2 + mm[5], e0, a, b, ld, gshift,
+                                      n.pos_base, row_base, n.n_pos, max_pos, tid, Tc);
             else
                 layer_items<V, GUARD>(As, row_ptr + n.pos_base + a, edges, 0, a, b, ld, gshift,
                                       n.pos_base, row_base, n.n_pos, max_pos, tid, Tc);
             consumer_barrier(Tc);  // layer l visible to every consumer
-            if (tid == 0) heavy::mbar_arrive(&empty[s]);
+            if (tid == 0) heavy::mbar_arrive(&empty[m]);
         }
     }
     if constexpr (GLOBAL) return;  // the activations are already in A

@@ -312,7 +312,7 @@ uint32_t default_heavy_threshold() {
 // slice whose activations (plus the staged edge buffers) fit in shared memory.
 struct CtaPlan {
     bool use = false;
-    uint32_t C = 0, V = 1, T = 32, smem = 0, EB = 0, RB = 0, ring_shift = 2;
+    uint32_t C = 0, V = 1, T = 32, smem = 0, ring_bytes = 0;
     bool global = false;  // activations in A (L2) instead of shared memory
 };
 
@@ -334,37 +334,35 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     const uint32_t mode = L->dev->sweep_mode;  // 0 auto, 1/3 layer launches, 2 K-cta when it fits
     if (mode == 1 || mode == 3) return p;
     if (L->n_levels < 2 || L->max_pos == 0) return p;
-    // +3 / +1 entries: the bulk copies start at 16-byte aligned indices
-    p.RB = (std::min<uint32_t>(L->max_width + 1, 4096) + 3 + 3) & ~3u;
-    p.EB = (std::min<uint32_t>(std::max<uint32_t>(L->max_level_edges, 1), 4096) + 1 + 1) & ~1u;
+    // bytes of the largest layer's staged row pointers + edges (16-byte
+    // aligned bulk copies: up to 3 / 1 extra leading entries)
+    const uint64_t max_layer =
+        ((std::min<uint64_t>(L->max_width, 1u << 20) + 1 + 3) * 4 + 15) / 16 * 16 +
+        ((std::min<uint64_t>(L->max_level_edges, 1u << 20) + 1) * 8 + 15) / 16 * 16;
+    const uint64_t per_sm = 228ull * 1024;
     const uint32_t cmax = std::min<uint32_t>(ldA, 128);
     for (uint32_t C = cmax; C >= 1; C >>= 1) {
         if (ldA % C) continue;
-        uint32_t eb = p.EB;
-        // activations (+ the zero row) | R edge slots | R row-pointer slots |
-        // R full + R empty mbarriers | R slot metas; R = 4 .. 16 staged layers
+        // activations (+ the zero row) | ring | mbarriers + metas
         const uint64_t as_bytes = (static_cast<uint64_t>(L->max_pos + 1) * C + 3) / 4 * 16;
-        auto smem_for = [&](uint32_t ebs, uint32_t rs) {
-            const uint64_t R = 1ull << rs;
-            return as_bytes + R * (ebs * 8ull + p.RB * 4ull + 2 * 8 + 16);
-        };
-        // deepest ring that keeps the CTAs-per-SM the activations alone allow
-        const uint64_t per_sm = 228ull * 1024;
-        const uint64_t fit = std::max<uint64_t>(1, per_sm / (as_bytes + 1024));
+        const uint64_t fixed = as_bytes + cta::kMetaBytes;
+        if (fixed + 1024 > kMaxDynSmem) {
+            if (C == 1) break;
+            continue;
+        }
+        // the ring: up to 32 of the largest layers, within what keeps the
+        // CTAs-per-SM the activations alone allow; at least 2 layers when that
+        // leaves too little, else whatever remains (big layers read global)
+        const uint64_t want = 32 * max_layer;
+        const uint64_t fit = std::max<uint64_t>(1, per_sm / (fixed + 1024 + std::min<uint64_t>(want, 4096)));
         const uint64_t budget = std::min<uint64_t>(kMaxDynSmem, per_sm / fit - 1024);
-        uint32_t rs = 4;
-        while (rs > 1 && smem_for(eb, rs) > budget) --rs;
-        while (smem_for(eb, rs) > kMaxDynSmem && eb > 64) {  // stage fewer edges; big layers read global
-            eb = (eb / 2) & ~1u;                              // stays even: 16-byte aligned slots
-        }
-        if (smem_for(eb, rs) <= kMaxDynSmem) {
-            p.C = C;
-            p.EB = eb;
-            p.ring_shift = rs;
-            p.smem = static_cast<uint32_t>(smem_for(eb, rs));
-            break;
-        }
-        if (C == 1) break;
+        uint64_t ring = budget > fixed ? budget - fixed : 0;
+        if (ring < 2 * max_layer) ring = std::min<uint64_t>(2 * max_layer, kMaxDynSmem - fixed);
+        ring = std::min(ring, want) / 16 * 16;
+        p.C = C;
+        p.ring_bytes = static_cast<uint32_t>(std::max<uint64_t>(ring, 16));
+        p.smem = static_cast<uint32_t>(fixed + p.ring_bytes);
+        break;
     }
     // Global (L2-resident) variant for one network whose shared-memory slices
     // would need more than one wave of CTAs: C columns per CTA with the
@@ -388,13 +386,9 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         while (ldA / C > sms && C < 128) C <<= 1;
         p.C = C;
         p.global = true;
-        p.EB = (std::min<uint32_t>(std::max<uint32_t>(L->max_level_edges, 1), 4096) + 1 + 1) & ~1u;
-        p.ring_shift = 4;
-        p.smem = static_cast<uint32_t>((1ull << p.ring_shift) * (p.EB * 8ull + p.RB * 4ull + 2 * 8 + 16));
-        while (p.smem > kMaxDynSmem && p.ring_shift > 1) {
-            --p.ring_shift;
-            p.smem = static_cast<uint32_t>((1ull << p.ring_shift) * (p.EB * 8ull + p.RB * 4ull + 2 * 8 + 16));
-        }
+        p.ring_bytes = static_cast<uint32_t>(
+            std::min<uint64_t>(32 * max_layer, kMaxDynSmem - cta::kMetaBytes) / 16 * 16);
+        p.smem = p.ring_bytes + cta::kMetaBytes;
     }
     if (!p.C) return p;
     p.V = p.C >= 4 ? 4 : 1;
@@ -765,8 +759,8 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         // cp.T consumer threads + one producer warp
         fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T + 32, cp.smem, st>>>(
             reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->le_cat.p, L->row_ptr.p,
-            L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos, cp.EB, cp.RB,
-            cp.ring_shift, (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr);
+            L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos, cp.ring_bytes,
+            (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr);
     } else {
         if (L->total_sensors)
             k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(

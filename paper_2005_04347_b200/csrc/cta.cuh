@@ -47,16 +47,35 @@ __device__ __forceinline__ void consumer_barrier(uint32_t n_threads) {
 // As holds the slice's activations with row stride ld; position p lives in
 // row p - row_base (shared memory: the network's rows, row_base = pos_base;
 // global/L2 mode: the whole A, row_base = 0, As already offset by c0).
-template <int V, bool GUARD>
+//
+// MODE 0: whole rows, sigmoid into As.  MODE 1 (pipelined finish): start at
+// the row's split edge with the partial sum left in pre[] by MODE 2 one step
+// earlier.  MODE 2 (pipelined prefix): sum the edges before the row's split
+// (global split[] array, absolute edge indices) and park the partial sum and
+// the split in pre[] / pre_k[] for MODE 1.
+template <int V, bool GUARD, int MODE = 0>
 __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const uint2* Ep, uint32_t e0,
                                             uint32_t a, uint32_t b, uint32_t ld, uint32_t gshift,
                                             uint32_t pos_base, uint32_t row_base, uint32_t n_pos,
-                                            uint32_t zero_row, uint32_t tid, uint32_t T) {
+                                            uint32_t zero_row, uint32_t tid, uint32_t T,
+                                            float* pre = nullptr, uint32_t* pre_k = nullptr,
+                                            const uint32_t* split = nullptr) {
     const uint32_t groups_mask = (1u << gshift) - 1u;
     for (uint32_t it = tid; it < ((b - a) << gshift); it += T) {
         const uint32_t i = it >> gshift, q = it & groups_mask;
-        uint32_t k = Rp[i] - e0;
-        const uint32_t ke = Rp[i + 1] - e0;
+        uint32_t k, ke;
+        if constexpr (MODE == 0) {
+            k = Rp[i] - e0;
+            ke = Rp[i + 1] - e0;
+        } else if constexpr (MODE == 1) {
+            k = pre_k[i] - e0;
+            ke = Rp[i + 1] - e0;
+        } else {
+            k = Rp[i] - e0;
+            const uint32_t sp = __ldg(&split[pos_base + a + i]);
+            ke = sp - e0;
+            if (q == 0) pre_k[i] = sp;
+        }
         const float* Aq = As + q * V;
         // GUARD: some predecessor of this layout has no position (hand-built
         // layouts only); it reads the zero row
@@ -67,7 +86,7 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
         };
         float acc[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) acc[v] = 0.0f;
+        for (int v = 0; v < V; ++v) acc[v] = MODE == 1 ? pre[it * V + v] : 0.0f;
         // four edges' loads in flight, then their adds in stored order
         for (; k + 4 <= ke; k += 4) {
             uint2 ed[4];
@@ -99,6 +118,11 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
 #pragma unroll
             for (int v = 0; v < V; ++v) acc[v] = mac(acc[v], __uint_as_float(ed.y), src[v]);
         }
+        if constexpr (MODE == 2) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) pre[it * V + v] = acc[v];
+            continue;
+        }
         float* dst = As + static_cast<size_t>(pos_base - row_base + a + i) * ld + q * V;
         if constexpr (V == 4) {
             *reinterpret_cast<float4*>(dst) =
@@ -126,14 +150,22 @@ constexpr uint32_t kSlots = 32;
 constexpr uint32_t kMetaBytes = kSlots * (8 + 8 + 32);
 }  // namespace cta
 
-template <int V, bool GUARD, bool GLOBAL>
+//
+// PIPE (latency-bound layers: at most two warps of items): the consumers form
+// two groups.  At step l the finish group completes layer l (the edges from
+// each row's split on, whose sources include level l-1, then sigmoid32) while
+// the prefix group sums layer l+1's rows up to their split (sources at levels
+// <= l-1, final since step l-1) -- half of each layer's dependent work moves
+// off the critical path.  The fp32 sum of a row is the same sequence of
+// roundings (segments.cuh); split[] comes from k_splits.
+template <int V, bool GUARD, bool GLOBAL, bool PIPE = false>
 __global__ void __launch_bounds__(288)
 k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       const uint32_t* __restrict__ le_cat, const uint32_t* __restrict__ row_ptr,
       const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,
       const uint4* __restrict__ oinfo, const float* __restrict__ x, uint32_t n_vec,
       float* __restrict__ A, uint32_t ldA, uint32_t C, uint32_t max_pos, uint32_t ring_bytes,
-      int write_all, float* __restrict__ out) {
+      int write_all, float* __restrict__ out, const uint32_t* __restrict__ split, uint32_t max_items) {
     using namespace cta;
     extern __shared__ __align__(128) unsigned char cta_smem[];
     const CtaNet n = nets[blockIdx.y];
@@ -148,6 +180,9 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + ring_bytes);
     uint64_t* empty = full + kSlots;
     uint32_t* meta = reinterpret_cast<uint32_t*>(empty + kSlots);
+    // PIPE: two parity buffers of partial sums [max_items * V] and splits [max_items]
+    float* pre = reinterpret_cast<float*>(meta + 8 * kSlots);
+    uint32_t* pre_k = reinterpret_cast<uint32_t*>(pre + 2 * max_items * V);
 
     const uint32_t groups = C / V;  // column groups per row (a power of two)
     const uint32_t gshift = __ffs(groups) - 1;
@@ -190,7 +225,7 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                     heavy::mbar_wait(&empty[m], (u - 1) & 1);
                     release_to(l - kSlots + 1);
                 }
-                const bool staged = size <= ring_bytes && !(write_all & 2);
+                bool staged = size <= ring_bytes && !(write_all & 2);
                 uint32_t at = 0, extent = 0;
                 if (staged) {
                     for (;;) {
@@ -202,6 +237,13 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                             extent = need;
                             w = at + size;
                             used += need;
+                            break;
+                        }
+                        // PIPE: layer l-1 is released only after the step that
+                        // also needs layer l (its prefix): never wait for it --
+                        // layer l is then read from global memory instead
+                        if (PIPE && oldest + 1 >= l) {
+                            staged = false;
                             break;
                         }
                         heavy::mbar_wait(&empty[(oldest - 1) % kSlots], ((oldest - 1) / kSlots) & 1);
@@ -244,6 +286,34 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
         consumer_barrier(Tc);
         const uint32_t* ring_u32 = reinterpret_cast<const uint32_t*>(ring);
         const uint2* ring_u2 = reinterpret_cast<const uint2*>(ring);
+        if constexpr (PIPE) {
+            const uint32_t Th = Tc / 2;
+            const bool fin = tid < Th;
+            const uint32_t gtid = fin ? tid : tid - Th;
+            for (uint32_t l = 0; l < n.n_layers; ++l) {
+                // finish layer l (l >= 1) | prefix of layer l+1
+                const uint32_t ll = fin ? l : l + 1;
+                if ((fin && l >= 1) || (!fin && ll < n.n_layers)) {
+                    const uint32_t m = (ll - 1) % kSlots;
+                    heavy::mbar_wait(&full[m], ((ll - 1) / kSlots) & 1);
+                    const uint32_t* mm = meta + 8 * m;
+                    const uint32_t a = mm[0], b = mm[1], e0 = mm[2];
+                    const uint32_t* Rp = mm[3] ? ring_u32 + mm[4] : row_ptr + n.pos_base + a;
+                    const uint2* Ep = mm[3] ? ring_u2 + mm[5] : edges;
+                    const uint32_t eb = mm[3] ? e0 : 0u;
+                    float* pb = pre + (ll & 1) * max_items * V;
+                    uint32_t* pk = pre_k + (ll & 1) * max_items;
+                    if (fin)
+                        layer_items<V, GUARD, 1>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base, n.n_pos,
+                                                 max_pos, gtid, Th, pb, pk, split);
+                    else
+                        layer_items<V, GUARD, 2>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base, n.n_pos,
+                                                 max_pos, gtid, Th, pb, pk, split);
+                }
+                consumer_barrier(Tc);  // layer l final, prefix of l+1 parked
+                if (tid == 0 && l >= 1) heavy::mbar_arrive(&empty[(l - 1) % kSlots]);
+            }
+        } else
         for (uint32_t l = 1; l < n.n_layers; ++l) {
             const uint32_t m = (l - 1) % kSlots;
             heavy::mbar_wait(&full[m], ((l - 1) / kSlots) & 1);
@@ -290,4 +360,37 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                 A[static_cast<uint64_t>(pos) * ldA + c0 + c] = As[(pos - n.pos_base) * C + c];
         }
     }
+}
+
+// split[p] for every non-sensor position p of network blockIdx.y: the first
+// stored edge (ascending source id) whose source is on layer level(p) - 1,
+// as an absolute edge index; the edges before it have all their sources on
+// layers <= level(p) - 2.  Sources outside the network (the zero row) count
+// as layer 0.
+__global__ void k_splits(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
+                         const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
+                         uint32_t* __restrict__ split) {
+    const CtaNet n = nets[blockIdx.y];
+    const uint32_t lp = blockIdx.x * blockDim.x + threadIdx.x;
+    if (lp >= n.n_pos || lp < n.n_sensors) return;
+    const uint32_t* lo = lo_cat + n.lo_base;
+    auto layer_of = [&](uint32_t q) {  // lo[a] <= q < lo[a + 1]
+        uint32_t a = 0, b = n.n_layers;
+        while (b - a > 1) {
+            const uint32_t m = (a + b) / 2;
+            if (lo[m] <= q) a = m;
+            else b = m;
+        }
+        return a;
+    };
+    const uint32_t p = n.pos_base + lp;
+    const uint32_t lv = layer_of(lp);
+    const uint32_t e1 = row_ptr[p + 1];
+    uint32_t k = row_ptr[p];
+    for (; k < e1; ++k) {
+        const uint32_t src = edges[k].x;
+        const uint32_t ls = src - n.pos_base < n.n_pos ? layer_of(src - n.pos_base) : 0u;
+        if (ls + 1 >= lv) break;
+    }
+    split[p] = k;
 }

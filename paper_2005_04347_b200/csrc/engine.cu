@@ -313,6 +313,8 @@ uint32_t default_heavy_threshold() {
 struct CtaPlan {
     bool use = false;
     uint32_t C = 0, V = 1, T = 32, smem = 0, ring_bytes = 0;
+    bool pipe = false;        // two consumer groups: finish layer l | prefix of layer l+1
+    uint32_t max_items = 0;   // items (node x column group) of the widest layer
     bool global = false;  // activations in A (L2) instead of shared memory
 };
 
@@ -341,11 +343,19 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         ((std::min<uint64_t>(L->max_level_edges, 1u << 20) + 1) * 8 + 15) / 16 * 16;
     const uint64_t per_sm = 228ull * 1024;
     const uint32_t cmax = std::min<uint32_t>(ldA, 128);
+    // Pipelined consumers (finish group + prefix group) for latency-bound
+    // layers of <= 512 items; off with ASNN_CTA_PIPE=0.
+    const char* pe = getenv("ASNN_CTA_PIPE");
+    const bool want_pipe = !(pe && pe[0] == '0');
     for (uint32_t C = cmax; C >= 1; C >>= 1) {
         if (ldA % C) continue;
-        // activations (+ the zero row) | ring | mbarriers + metas
+        // activations (+ the zero row) | ring | mbarriers + metas | pipelined
+        // consumers' partial sums (2 x items x (V + 1) words)
         const uint64_t as_bytes = (static_cast<uint64_t>(L->max_pos + 1) * C + 3) / 4 * 16;
-        const uint64_t fixed = as_bytes + cta::kMetaBytes;
+        const uint64_t vq = C >= 4 ? 4 : 1;
+        const uint64_t items_c = static_cast<uint64_t>(L->max_width) * (C / vq);
+        const uint64_t pipe_c = want_pipe && items_c <= 512 ? 2 * items_c * (vq + 1) * 4 : 0;
+        const uint64_t fixed = as_bytes + cta::kMetaBytes + pipe_c;
         if (fixed + 1024 > kMaxDynSmem) {
             if (C == 1) break;
             continue;
@@ -362,6 +372,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         p.C = C;
         p.ring_bytes = static_cast<uint32_t>(std::max<uint64_t>(ring, 16));
         p.smem = static_cast<uint32_t>(fixed + p.ring_bytes);
+        p.pipe = pipe_c > 0;
         break;
     }
     // Global (L2-resident) variant for one network whose shared-memory slices
@@ -394,6 +405,11 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     p.V = p.C >= 4 ? 4 : 1;
     const uint64_t items = static_cast<uint64_t>(L->max_width) * (p.C / p.V);
     p.T = static_cast<uint32_t>(std::min<uint64_t>(256, std::max<uint64_t>(32, (items + 31) / 32 * 32)));
+    if (p.global) p.pipe = false;
+    if (p.pipe) {  // finish group + prefix group of up to 4 warps each
+        p.max_items = static_cast<uint32_t>(items);
+        p.T = 2 * static_cast<uint32_t>(std::min<uint64_t>(128, (items + 31) / 32 * 32));
+    }
     const bool latency_bound = L->nets.size() > 1 || L->n_levels >= 24 ||
                                L->total_edges * static_cast<uint64_t>(ldA) <= (1ull << 22);
     p.use = mode == 2 || latency_bound;
@@ -752,6 +768,9 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
     if (cp.use) {
         // the whole sweep (sensors + every layer) of each (network, slice) in one CTA
         auto fn = cp.global ? (cp.V == 4 ? k_cta<4, false, true> : k_cta<1, false, true>)
+                  : cp.pipe
+                      ? (cp.V == 4 ? (L->zero_refs ? k_cta<4, true, false, true> : k_cta<4, false, false, true>)
+                                   : (L->zero_refs ? k_cta<1, true, false, true> : k_cta<1, false, false, true>))
                   : cp.V == 4 ? (L->zero_refs ? k_cta<4, true, false> : k_cta<4, false, false>)
                               : (L->zero_refs ? k_cta<1, true, false> : k_cta<1, false, false>);
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -760,7 +779,7 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T + 32, cp.smem, st>>>(
             reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->le_cat.p, L->row_ptr.p,
             L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos, cp.ring_bytes,
-            (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr);
+            (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr, L->split.p, cp.max_items);
     } else {
         if (L->total_sensors)
             k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(
@@ -859,6 +878,14 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
 int ensure_workspace(asnn_dev_layout* L, uint32_t n_vec) {
     asnn_dev* dev = L->dev;
     const uint32_t ldA = padded_batch(n_vec);
+    if (cta_plan(L, ldA).pipe && !L->split.p) {
+        L->graph.reset();
+        CK(L->split.alloc(L->total_pos));
+        const uint32_t G = static_cast<uint32_t>(L->nets.size());
+        k_splits<<<dim3((L->max_pos + 255) / 256, G), 256, 0, dev->stream>>>(
+            reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->row_ptr.p, L->edges.p, L->split.p);
+        CK(cudaGetLastError());
+    }
     if (seg_eligible(L, ldA)) {
         if (L->seg_key != seg_key_for(L)) {
             L->graph.reset();

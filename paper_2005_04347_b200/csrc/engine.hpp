@@ -176,6 +176,9 @@ struct asnn_dev_layout {
     uint32_t n_slots = 0;                  // partial-sum slots (heavy rows)
     uint64_t seg_key = ~0ull;              // options they were cut for
     asnn_b200::DevBuf<float> accbuf;       // [n_slots][ldA] partial sums
+    // K-cta pipelined consumers: per position, the first stored edge whose
+    // source is on the layer just below (k_splits)
+    asnn_b200::DevBuf<uint32_t> split;     // [total_pos] absolute edge index
 
     ~asnn_dev_layout() { graph.reset(); }
 };

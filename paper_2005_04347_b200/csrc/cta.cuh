@@ -51,8 +51,9 @@ __device__ __forceinline__ void consumer_barrier(uint32_t n_threads) {
 // MODE 0: whole rows, sigmoid into As.  MODE 1 (pipelined finish): start at
 // the row's split edge with the partial sum left in pre[] by MODE 2 one step
 // earlier.  MODE 2 (pipelined prefix): sum the edges before the row's split
-// (global split[] array, absolute edge indices) and park the partial sum and
-// the split in pre[] / pre_k[] for MODE 1.
+// (split[i] for the layer's row i: staged slice or global, absolute edge
+// indices) and park the partial sum and the split in pre[] / pre_k[] for
+// MODE 1.
 template <int V, bool GUARD, int MODE = 0>
 __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const uint2* Ep, uint32_t e0,
                                             uint32_t a, uint32_t b, uint32_t ld, uint32_t gshift,
@@ -72,7 +73,7 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
             ke = Rp[i + 1] - e0;
         } else {
             k = Rp[i] - e0;
-            const uint32_t sp = __ldg(&split[pos_base + a + i]);
+            const uint32_t sp = split[i];
             ke = sp - e0;
             if (q == 0) pre_k[i] = sp;
         }
@@ -218,9 +219,11 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                 const uint32_t e0 = le[l], e1 = le[l + 1];
                 const uint32_t r0 = n.pos_base + a, r0a = r0 & ~3u;
                 const uint32_t rbytes = ((b - a + 1 + (r0 - r0a)) * 4 + 15) & ~15u;
+                // PIPE: the layer's split[] slice too (same alignment as row_ptr)
+                const uint32_t sbytes = PIPE ? ((b - a + (r0 - r0a)) * 4 + 15) & ~15u : 0u;
                 const uint32_t e0a = e0 & ~1u;
                 const uint32_t ebytes = ((e1 - e0 + (e0 - e0a)) * 8 + 15) & ~15u;
-                const uint32_t size = rbytes + ebytes;
+                const uint32_t size = rbytes + sbytes + ebytes;
                 if (u > 0) {  // slot m's previous layer (l - kSlots) and all before it are released
                     heavy::mbar_wait(&empty[m], (u - 1) & 1);
                     release_to(l - kSlots + 1);
@@ -256,12 +259,14 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                 mm[2] = e0;
                 mm[3] = staged ? 1u : 0u;
                 mm[4] = at / 4 + (r0 - r0a);
-                mm[5] = (at + rbytes) / 8 + (e0 - e0a);
+                mm[5] = (at + rbytes + sbytes) / 8 + (e0 - e0a);
                 mm[6] = extent;
+                mm[7] = (at + rbytes) / 4 + (r0 - r0a);
                 if (staged) {
                     expect_tx(&full[m], size);
                     bulk_g2s(ring + at, row_ptr + r0a, rbytes, &full[m]);
-                    if (ebytes) bulk_g2s(ring + at + rbytes, edges + e0a, ebytes, &full[m]);
+                    if (sbytes) bulk_g2s(ring + at + rbytes, split + r0a, sbytes, &full[m]);
+                    if (ebytes) bulk_g2s(ring + at + rbytes + sbytes, edges + e0a, ebytes, &full[m]);
                 } else {
                     heavy::mbar_arrive(&full[m]);
                 }
@@ -299,16 +304,17 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                     const uint32_t* mm = meta + 8 * m;
                     const uint32_t a = mm[0], b = mm[1], e0 = mm[2];
                     const uint32_t* Rp = mm[3] ? ring_u32 + mm[4] : row_ptr + n.pos_base + a;
+                    const uint32_t* Sp = mm[3] ? ring_u32 + mm[7] : split + n.pos_base + a;
                     const uint2* Ep = mm[3] ? ring_u2 + mm[5] : edges;
                     const uint32_t eb = mm[3] ? e0 : 0u;
                     float* pb = pre + (ll & 1) * max_items * V;
                     uint32_t* pk = pre_k + (ll & 1) * max_items;
                     if (fin)
                         layer_items<V, GUARD, 1>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base, n.n_pos,
-                                                 max_pos, gtid, Th, pb, pk, split);
+                                                 max_pos, gtid, Th, pb, pk, Sp);
                     else
                         layer_items<V, GUARD, 2>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base, n.n_pos,
-                                                 max_pos, gtid, Th, pb, pk, split);
+                                                 max_pos, gtid, Th, pb, pk, Sp);
                 }
                 consumer_barrier(Tc);  // layer l final, prefix of l+1 parked
                 if (tid == 0 && l >= 1) heavy::mbar_arrive(&empty[(l - 1) % kSlots]);

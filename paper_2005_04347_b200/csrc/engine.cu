@@ -339,7 +339,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     // bytes of the largest layer's staged row pointers + edges (16-byte
     // aligned bulk copies: up to 3 / 1 extra leading entries)
     const uint64_t max_layer =
-        ((std::min<uint64_t>(L->max_width, 1u << 20) + 1 + 3) * 4 + 15) / 16 * 16 +
+        2 * (((std::min<uint64_t>(L->max_width, 1u << 20) + 1 + 3) * 4 + 15) / 16 * 16) +
         ((std::min<uint64_t>(L->max_level_edges, 1u << 20) + 1) * 8 + 15) / 16 * 16;
     const uint64_t per_sm = 228ull * 1024;
     const uint32_t cmax = std::min<uint32_t>(ldA, 128);

@@ -216,6 +216,11 @@ int asnn_dev_sweep_kind(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* kind)
  * exhaustive parity checks of the epilogue. */
 int asnn_dev_sigmoid32(asnn_dev* dev, const float* x, float* y, uint64_t n);
 
+/* The epilogue's fast path against its exact restatement for all 2^32 float
+ * inputs, on the device: *mismatches must be 0; *exact_path counts the inputs
+ * the rounding test handed to the exact path. */
+int asnn_dev_sigmoid_selfcheck(asnn_dev* dev, uint64_t* mismatches, uint64_t* exact_path);
+
 /* Microarchitecture probe: SM cycles per operation of a dependent chain of n
  * ops run by one thread (which: 0 sigmoid32, 1 DFMA, 2 FADD, 3 shared-memory
  * load, 4 double division, 5 exp, 6 empty loop iteration).  Evidence for

@@ -31,7 +31,7 @@ static __device__ const uint64_t kExpTab[256] = {
 // restatement of the host glibc exp (exp_glibc.h) -- identical doubles, so
 // identical floats: checked for all 2^32 inputs (oracle/exp_check.c,
 // tests/test_gpu_sigmoid.py).
-__device__ __forceinline__ float sigmoid32(float x) {
+__device__ __forceinline__ float sigmoid32_exact(float x) {
     const double e = exp_glibc(__dmul_rn(-4.97, static_cast<double>(x)), kExpTab);
     double v = __ddiv_rn(1.0, __dadd_rn(1.0, e));
     if (v <= 0.0) v = 4.9406564584124654e-324;         // DBL_TRUE_MIN
@@ -40,6 +40,63 @@ __device__ __forceinline__ float sigmoid32(float x) {
     if (f <= 0.0f) f = 1.40129846e-45f;                  // FLT_TRUE_MIN
     if (f >= 1.0f) f = 1.0f - 5.96046448e-08f;           // 1 - FLT_EPSILON/2
     return f;
+}
+
+// sigmoid32 with a short double-precision fast path and an exact rounding
+// test (Ziv): the fast path evaluates 1/(1+exp(-4.97 x)) to a relative error
+// below 2^-48 (degree-4 polynomial on the same 2^(i/128) table, reciprocal by
+// MUFU.RCP64H + two Newton steps) -- about half the FP64 operations of the
+// correctly rounded exp + division.  Whenever that value lies within 2^12
+// double ulps (2^-40 relative) of a float rounding boundary, or the result
+// leaves the normal float range, the exact restatement above decides.  Both
+// results then round to the same float: the reference's double is within
+// ~1 ulp of the true value too.  Checked for all 2^32 inputs against
+// sigmoid32_exact on the device (asnn_dev_sigmoid_selfcheck) and against the
+// reference's host sigmoid32 (tests/test_gpu_sigmoid.py).
+__device__ __forceinline__ float sigmoid32_path(float x, bool& exact) {
+    exact = false;
+    const double t = __dmul_rn(-4.97, static_cast<double>(x));
+    // exp(t) <= 2^-54: 1 + exp(t) == 1 in both, v clamps below 1 and the
+    // float rounds to 1 and clamps to 1 - FLT_EPSILON/2
+    if (t < -40.0) return 1.0f - 5.96046448e-08f;
+    if (!(t < 86.0)) {  // float subnormal / clamped results, NaN
+        exact = true;
+        return sigmoid32_exact(x);
+    }
+    const double zs = __fma_rn(t, XG_INVLN2N, XG_SHIFT);
+    const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(zs));
+    const double kd = __dsub_rn(zs, XG_SHIFT);
+    double r = __fma_rn(kd, XG_NEGLN2HIN, t);
+    r = __fma_rn(kd, XG_NEGLN2LON, r);
+    const uint32_t idx = 2u * static_cast<uint32_t>(ki & 127u);
+    const double tail = __longlong_as_double(static_cast<long long>(__ldg(&kExpTab[idx])));
+    const uint64_t sbits = __ldg(&kExpTab[idx + 1]) + (ki << 45);
+    const double r2 = __dmul_rn(r, r);
+    double p = __fma_rn(r, XG_C3, XG_C2);
+    p = __fma_rn(r2, XG_C4, p);
+    const double tmp = __fma_rn(r2, p, __dadd_rn(r, tail));
+    const double scale = __longlong_as_double(static_cast<long long>(sbits));
+    const double d = __dadd_rn(1.0, __fma_rn(scale, tmp, scale));
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    y = __fma_rn(y, __fma_rn(-d, y, 1.0), y);
+    y = __fma_rn(y, __fma_rn(-d, y, 1.0), y);
+    // y in (2^-125, 1]: distance of its low 29 mantissa bits from the float
+    // rounding midpoint 2^28 (in double ulps of y)
+    const uint64_t yb = static_cast<uint64_t>(__double_as_longlong(y));
+    const int64_t low = static_cast<int64_t>(yb & ((1ull << 29) - 1)) - (1ll << 28);
+    if (low < (1ll << 12) && low > -(1ll << 12)) {
+        exact = true;
+        return sigmoid32_exact(x);
+    }
+    float f = __double2float_rn(y);
+    if (f >= 1.0f) f = 1.0f - 5.96046448e-08f;
+    return f;
+}
+
+__device__ __forceinline__ float sigmoid32(float x) {
+    bool exact;
+    return sigmoid32_path(x, exact);
 }
 
 // One multiply-add of the reference accumulation (eval.cpp:20-21):

@@ -1015,6 +1015,23 @@ int asnn_dev_latency_probe(asnn_dev* dev, int which, int n, double* cycles_per_o
     return ASNN_OK;
 }
 
+int asnn_dev_sigmoid_selfcheck(asnn_dev* dev, uint64_t* mismatches, uint64_t* exact_path) {
+    if (!dev || !mismatches || !exact_path) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    CK(cudaSetDevice(dev->device));
+    DevBuf<unsigned long long> c;
+    CK(c.alloc(2));
+    CK(cudaMemsetAsync(c.p, 0, 16, dev->stream));
+    k_sigmoid_selfcheck<<<dev->sm_count * 8, 256, 0, dev->stream>>>(c.p);
+    CK(cudaGetLastError());
+    unsigned long long h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, c.p, 16, cudaMemcpyDeviceToHost, dev->stream));
+    CK(cudaStreamSynchronize(dev->stream));
+    *mismatches = h[0];
+    *exact_path = h[1];
+    return ASNN_OK;
+}
+
 int asnn_dev_sigmoid32(asnn_dev* dev, const float* x, float* y, uint64_t n) {
     if (!dev || (n && (!x || !y))) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);

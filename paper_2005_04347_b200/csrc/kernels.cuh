@@ -408,6 +408,31 @@ __global__ void k_latency_probe(int n, float seed, long long* cycles, float* sin
     *sink = f + static_cast<float>(d) + static_cast<float>(p);
 }
 
+// Every float bit pattern through sigmoid32 (fast path + rounding test) and
+// sigmoid32_exact: counts[0] = bitwise mismatches (a NaN matches any NaN),
+// counts[1] = inputs the rounding test sent to the exact path.
+__global__ void k_sigmoid_selfcheck(unsigned long long* counts) {
+    unsigned long long bad = 0, slow = 0;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (1ull << 32);
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const float x = __uint_as_float(static_cast<uint32_t>(i));
+        bool exact;
+        const float f = sigmoid32_path(x, exact);
+        const float g = sigmoid32_exact(x);
+        const bool same = __float_as_uint(f) == __float_as_uint(g) || (f != f && g != g);
+        bad += same ? 0 : 1;
+        slow += exact ? 1 : 0;
+    }
+    for (int o = 16; o; o >>= 1) {
+        bad += __shfl_xor_sync(0xFFFFFFFFu, bad, o);
+        slow += __shfl_xor_sync(0xFFFFFFFFu, slow, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&counts[0], bad);
+        atomicAdd(&counts[1], slow);
+    }
+}
+
 __global__ void k_sigmoid_many(const float* __restrict__ x, float* __restrict__ y, uint64_t n) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) y[i] = sigmoid32(x[i]);

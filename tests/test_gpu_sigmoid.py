@@ -64,3 +64,14 @@ def test_all_2pow32_inputs_bitwise(ref):
         mism += int(np.count_nonzero((d != r) & ~nan))
         assert np.all(np.isnan(d.view(np.float32)[nan]) == np.isnan(r.view(np.float32)[nan]))
     assert mism == 0
+
+
+def test_fast_path_against_exact_all_inputs():
+    """sigmoid32's fast path + rounding test (common.cuh) against the exact
+    restatement for every float bit pattern, on the device."""
+    dev = A.Device.get(0)
+    bad, slow = C.c_uint64(), C.c_uint64()
+    dev.check(dev.lib.asnn_dev_sigmoid_selfcheck(dev.h, C.byref(bad), C.byref(slow)))
+    assert bad.value == 0
+    # NaNs, the saturated tails and the rare near-midpoint values take the exact path
+    assert slow.value < (1 << 32) // 4

@@ -46,7 +46,10 @@ typedef enum asnn_status {
     ASNN_E_INVALID = 5,           /* invalid argument (null pointer, size overflow) */
     ASNN_E_CUDA = 6,              /* CUDA runtime / launch failure */
     ASNN_E_OOM = 7,               /* device or pinned allocation failed */
-    ASNN_E_INFEASIBLE = 8         /* InfeasibleSpec (errors.hpp:23-25; netgen.cpp:29-53) */
+    ASNN_E_INFEASIBLE = 8,        /* InfeasibleSpec (errors.hpp:23-25; netgen.cpp:29-53) */
+    ASNN_E_PARSE = 9,             /* ParseError (errors.hpp:31-35): "line N: ..." */
+    ASNN_E_VALIDATION = 10,       /* ValidationError (errors.hpp:37-53): "invalid network\n  ..." */
+    ASNN_E_IO = 11                /* IoError (errors.hpp:27-29) */
 } asnn_status;
 
 #define ASNN_UNASSIGNED 0xFFFFFFFFu
@@ -227,12 +230,32 @@ int asnn_dev_sigmoid_selfcheck(asnn_dev* dev, uint64_t* mismatches, uint64_t* ex
  * DESIGN.md's latency model. */
 int asnn_dev_latency_probe(asnn_dev* dev, int which, int n, double* cycles_per_op);
 
+typedef struct asnn_corpus asnn_corpus;
+
+/* ---- loading (io.hpp:23-31) on the device ---------------------------------
+ * parse_network (io.cpp:83-156) followed by validate (network.cpp:151-216):
+ * text = the bytes of an `asnn 1` file.  On success *out owns the network
+ * (read it with asnn_corpus_desc): nodes sorted unique, inputs / outputs in
+ * declared order, connections in file order.  ASNN_E_PARSE: the first
+ * failing line (*err_line) and the reference's ParseError message
+ * ("line N: ...") in asnn_dev_last_error; ASNN_E_VALIDATION: the
+ * ValidationError message ("invalid network\n  ..."). */
+int asnn_dev_parse_network(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** out,
+                           uint32_t* err_line);
+/* read_network (io.cpp:167-173): ASNN_E_IO when the file cannot be read. */
+int asnn_dev_read_network(asnn_dev* dev, const char* path, asnn_corpus** out, uint32_t* err_line);
+/* parse_weight's from_chars<float> on n tokens buf[off[i], off[i+1]) on the
+ * device: status 0 = parsed, 1 = rejected, 2 / 3 = decided by the host's
+ * from_chars (parsed / rejected) because the device flagged the token; the
+ * parser's number kernel, exposed for parity tests. */
+int asnn_dev_parse_weights(asnn_dev* dev, const char* buf, const uint64_t* off, uint64_t n, float* out,
+                           uint8_t* status);
+
 /* ---- synthetic corpora (host, deterministic) ------------------------------
  * generate(GenSpec) byte-identical to the reference (netgen.cpp:71-157),
  * the MLP-adjacent shape (config 2) and the banded power-law shape
  * (config 4).  A corpus handle owns its arrays; read them with
  * asnn_corpus_desc (pointers valid until asnn_corpus_free). */
-typedef struct asnn_corpus asnn_corpus;
 int asnn_gen_reference(uint32_t input_count, uint32_t output_count, uint32_t hidden_count,
                        uint64_t connection_count, uint32_t target_depth, float weight_min,
                        float weight_max, uint64_t seed, asnn_corpus** out);

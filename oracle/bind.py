@@ -199,12 +199,47 @@ class Ref:
             "ref_max_threads": (C.c_int, []),
             "ref_layout_ptr": (vp, [vp]),
             "ref_sigmoid32_many": (None, [f32p, f32p, C.c_uint64]),
+            "ref_parse": (vp, [C.c_char_p, C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                               C.c_char_p, C.c_uint64]),
+            "ref_serialize": (C.c_uint64, [vp, C.c_char_p, C.c_uint64]),
+            "ref_from_chars_f32": (None, [C.c_char_p, u64p, C.c_uint64, f32p, u8p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
         self.L = L
+
+    # text format (io.cpp) ------------------------------------------------------
+    def parse(self, text: bytes):
+        """parse_network: (RefNet, None) or (None, (kind, line, message)),
+        kind 1 = ParseError, 2 = ValidationError, 3 = other."""
+        kind, line = C.c_int(0), C.c_int(0)
+        err = C.create_string_buffer(1 << 16)
+        h = self.L.ref_parse(text, len(text), C.byref(kind), C.byref(line), err, len(err))
+        if h:
+            return RefNet(self, h), None
+        return None, (kind.value, line.value, err.value.decode())
+
+    def serialize(self, rn: "RefNet") -> bytes:
+        n = self.L.ref_serialize(rn.h, None, 0)
+        if n == 0xFFFFFFFFFFFFFFFF:
+            raise ValueError("serialize_network threw (invalid network)")
+        buf = C.create_string_buffer(n)
+        self.L.ref_serialize(rn.h, buf, n)
+        return buf.raw[:n]
+
+    def from_chars_f32(self, tokens):
+        """std::from_chars<float> on each token: (values, status 0 ok / 1 error)."""
+        enc = [t.encode() if isinstance(t, str) else t for t in tokens]
+        off = np.zeros(len(enc) + 1, np.uint64)
+        off[1:] = np.cumsum([len(t) for t in enc])
+        buf = b"".join(enc)
+        out = np.zeros(len(enc), np.float32)
+        st = np.zeros(len(enc), np.uint8)
+        self.L.ref_from_chars_f32(buf, _p(off, C.c_uint64), len(enc), _p(out, C.c_float),
+                                  _p(st, C.c_uint8))
+        return out, st
 
     # networks ---------------------------------------------------------------
     def generate(self, spec):

@@ -18,8 +18,13 @@
 #include <span>
 #include <vector>
 
+#include <charconv>
+#include <string>
+#include <string_view>
+
 #include "asnn/errors.hpp"
 #include "asnn/eval.hpp"
+#include "asnn/io.hpp"
 #include "asnn/layout.hpp"
 #include "asnn/netgen.hpp"
 #include "asnn/network.hpp"
@@ -356,6 +361,63 @@ int ref_max_threads() { return omp_get_max_threads(); }
 const void* ref_layout_ptr(void* hp) { return &static_cast<RefHandle*>(hp)->layout; }
 
 // sigmoid32 (network.hpp:54-59) over an array, for exhaustive exp checks.
+// asnn::parse_network (io.cpp:83-156).  Returns a handle on success; on
+// failure nullptr with *kind = 1 (ParseError, *line = its line) or 2
+// (ValidationError) or 3 (other) and the exception's what() in err.
+void* ref_parse(const char* text, std::uint64_t len, int* kind, int* line, char* err, std::uint64_t cap) {
+    *kind = 0;
+    *line = 0;
+    if (cap) err[0] = 0;
+    auto put = [&](const char* w) {
+        if (!cap) return;
+        std::strncpy(err, w, cap - 1);
+        err[cap - 1] = 0;
+    };
+    try {
+        auto h = std::make_unique<RefHandle>();
+        h->net = asnn::parse_network(std::string_view(text, len));
+        return h.release();
+    } catch (const asnn::ParseError& e) {
+        *kind = 1;
+        *line = e.line;
+        put(e.what());
+    } catch (const asnn::ValidationError& e) {
+        *kind = 2;
+        put(e.what());
+    } catch (const std::exception& e) {
+        *kind = 3;
+        put(e.what());
+    }
+    return nullptr;
+}
+
+// asnn::serialize_network (io.cpp:25-45) into out (cap bytes); returns the
+// text size (call with cap = 0 for the size), or UINT64_MAX if it throws.
+std::uint64_t ref_serialize(void* hp, char* out, std::uint64_t cap) {
+    try {
+        const std::string t = asnn::serialize_network(static_cast<RefHandle*>(hp)->net);
+        if (cap >= t.size()) std::memcpy(out, t.data(), t.size());
+        return t.size();
+    } catch (...) {
+        return ~0ull;
+    }
+}
+
+// std::from_chars as parse_weight / parse_id use it (io.cpp:66-80): status 0
+// = parsed the whole token, else 1 (error or partial consumption).
+void ref_from_chars_f32(const char* buf, const std::uint64_t* off, std::uint64_t n, float* out,
+                        std::uint8_t* status) {
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < static_cast<std::int64_t>(n); ++i) {
+        const char* b = buf + off[i];
+        const char* e = buf + off[i + 1];
+        float v = 0.0f;
+        const auto r = std::from_chars(b, e, v);
+        status[i] = (r.ec != std::errc{} || r.ptr != e) ? 1 : 0;
+        out[i] = status[i] ? 0.0f : v;
+    }
+}
+
 void ref_sigmoid32_many(const float* in, float* out, std::uint64_t n) {
 #pragma omp parallel for schedule(static)
     for (std::int64_t i = 0; i < static_cast<std::int64_t>(n); ++i) out[i] = asnn::sigmoid32(in[i]);

@@ -7,8 +7,9 @@ API (see api.py) plus ctypes plumbing.
 """
 from .api import (  # noqa: F401
     ActivationState, Backend, BackendUnavailable, Device, DeviceError, DeviceLayout, GenSpec,
-    InfeasibleSpec, InputArityMismatch, LayerAssignment, LayeredLayout, LayerOutOfRange, Network,
-    OutputUnreachable, ParallelConfig, RequiredSet, SplitMix64, UnassignedOutput, compute_required,
+    InfeasibleSpec, InputArityMismatch, IoError, LayerAssignment, LayeredLayout, LayerOutOfRange,
+    Network, OutputUnreachable, ParallelConfig, ParseError, RequiredSet, SplitMix64, UnassignedOutput,
+    ValidationError, compute_required, parse_network, read_network,
     corpus_spec, depth, device_count, eval_parallel, eval_parallel_batch, flatten, generate,
     generate_mlp, generate_powerlaw, layer_slice_bounds, make_network, max_connections,
     max_layer_width, random_spec, read_outputs, segment, unassigned_outputs,

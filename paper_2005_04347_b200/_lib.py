@@ -27,6 +27,9 @@ ASNN_E_INVALID = 5
 ASNN_E_CUDA = 6
 ASNN_E_OOM = 7
 ASNN_E_INFEASIBLE = 8
+ASNN_E_PARSE = 9
+ASNN_E_VALIDATION = 10
+ASNN_E_IO = 11
 UNASSIGNED = 0xFFFFFFFF
 
 
@@ -104,6 +107,9 @@ PROTOTYPES = {
     "asnn_gen_mlp": (C.c_int, [C.c_uint32, C.c_uint32, C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]),
     "asnn_gen_powerlaw": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                     C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "asnn_dev_parse_network": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p), u32p]),
+    "asnn_dev_read_network": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p), u32p]),
+    "asnn_dev_parse_weights": (C.c_int, [C.c_void_p, C.c_char_p, u64p, C.c_uint64, f32p, u8p]),
     "asnn_corpus_desc": (C.c_int, [C.c_void_p, C.POINTER(NetworkDesc)]),
     "asnn_corpus_free": (None, [C.c_void_p]),
 }

@@ -65,6 +65,26 @@ class DeviceError(AsnnError):
     pass
 
 
+class IoError(AsnnError):
+    pass
+
+
+class ParseError(AsnnError):
+    """errors.hpp:31-35: what() = "line N: ...", .line = N."""
+
+    def __init__(self, msg: str, line: int = 0):
+        super().__init__(msg)
+        self.line = line
+
+
+class ValidationError(AsnnError):
+    """errors.hpp:37-53: what() = "invalid network\n  v1\n  v2 ...", .violations."""
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        self.violations = msg.split("\n  ")[1:]
+
+
 def _raise(rc: int, msg: str):
     cls = {
         _lib.ASNN_E_UNAVAILABLE: BackendUnavailable,
@@ -73,6 +93,8 @@ def _raise(rc: int, msg: str):
         _lib.ASNN_E_LAYER_RANGE: LayerOutOfRange,
         _lib.ASNN_E_INFEASIBLE: InfeasibleSpec,
         _lib.ASNN_E_INVALID: ValueError,
+        _lib.ASNN_E_VALIDATION: ValidationError,
+        _lib.ASNN_E_IO: IoError,
     }.get(rc, DeviceError)
     raise cls(msg or f"asnn status {rc}")
 
@@ -590,6 +612,37 @@ def generate(spec: GenSpec) -> Network:
     if rc:
         _raise(rc, "infeasible GenSpec")
     return _corpus_to_network(lib, h)
+
+
+# --- io.hpp:23-31: loading on the device (csrc/parse.cu) ------------------------
+def parse_network(text, device: int = 0) -> Network:
+    """parse_network (io.cpp:83-156) + validate (network.cpp:151-216) on the
+    device: raises ParseError (with .line) or ValidationError with the
+    reference's messages."""
+    if isinstance(text, str):
+        text = text.encode()
+    dev = Device.get(device)
+    h = C.c_void_p()
+    line = C.c_uint32(0)
+    rc = dev.lib.asnn_dev_parse_network(dev.h, text, len(text), C.byref(h), C.byref(line))
+    if rc == _lib.ASNN_E_PARSE:
+        raise ParseError(dev.lib.asnn_dev_last_error(dev.h).decode(), line.value)
+    if rc:
+        _raise(rc, dev.lib.asnn_dev_last_error(dev.h).decode())
+    return _corpus_to_network(dev.lib, h)
+
+
+def read_network(path, device: int = 0) -> Network:
+    """read_network (io.cpp:167-173): the file's bytes through parse_network."""
+    dev = Device.get(device)
+    h = C.c_void_p()
+    line = C.c_uint32(0)
+    rc = dev.lib.asnn_dev_read_network(dev.h, str(path).encode(), C.byref(h), C.byref(line))
+    if rc == _lib.ASNN_E_PARSE:
+        raise ParseError(dev.lib.asnn_dev_last_error(dev.h).decode(), line.value)
+    if rc:
+        _raise(rc, dev.lib.asnn_dev_last_error(dev.h).decode())
+    return _corpus_to_network(dev.lib, h)
 
 
 def max_connections(spec: GenSpec) -> int:

@@ -205,4 +205,9 @@ struct FlatDevice {
 int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& flat,
                     asnn_dev_layout** out);
 
+// validate's cycle test on device arrays (preprocess.cu): nodes sorted unique,
+// connections as (src, dst) ids.
+int device_cycle_check(asnn_dev* dev, const uint32_t* nodes, uint32_t N, const uint32_t* src, const uint32_t* dst,
+                       uint64_t E, bool* cyclic);
+
 }  // namespace asnn_b200

@@ -50,10 +50,7 @@ struct SplitMix64 {
 
 }  // namespace
 
-struct asnn_corpus {
-    std::vector<std::uint32_t> nodes, inputs, outputs, src, dst;
-    std::vector<float> w;
-};
+#include "corpus.hpp"
 
 namespace {
 

@@ -1,0 +1,829 @@
+// parse.cu -- loading a network on the device: parse_network / read_network
+// (io.cpp:83-175) and validate (network.cpp:151-216), SURVEY.md 8f ranks 1-2.
+//
+// The text is copied to HBM once and every step is data-parallel:
+//   1. line starts: newline counts per 256-byte chunk, exclusive scan,
+//      scatter (u64 positions, so files beyond 4 GB work);
+//   2. one thread per line: strip '\r', split on ' '/'\t', classify the first
+//      token (comment, "asnn", "inputs", "outputs", "edge", other) and, for
+//      edge lines, parse "<source> <target> <weight>" with the from_chars
+//      contract of parse_id / parse_weight (parse_tok.cuh);
+//   3. significant lines (not blank / comment) are numbered by a scan: the
+//      first three must be the header, inputs and outputs lines, every later
+//      one an edge line -- the reference's section state machine;
+//   4. errors: each line reports its own code and the first failing line wins
+//      (64-bit atomicMin of line << 8 | code) -- exactly the line at which
+//      the sequential parser would have thrown; duplicate edges come from a
+//      stable radix sort by (source, target): the later line of an equal pair;
+//   5. the ids of the inputs / outputs lines are tokenised in parallel;
+//   6. make_network (sorted unique ids) and validate on the device: duplicate
+//      declarations, input/output overlap, inputs with incoming connections,
+//      and a Kahn pass for cycles (the cycle's text, only needed for the error
+//      message, is recovered by the reference's DFS order on the host).
+// The host formats messages from the failing line's own text, and resolves
+// the rare weight tokens parse_tok.cuh marks kTokHost with std::from_chars.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <charconv>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "corpus.hpp"
+#include "engine.hpp"
+#include "parse_tok.cuh"
+#include "sort.cuh"
+
+namespace asnn_b200 {
+namespace {
+
+using namespace parse;
+
+constexpr uint32_t kT = 256;
+inline uint32_t nb(uint64_t n) { return static_cast<uint32_t>((n + kT - 1) / kT); }
+
+#define CKP(expr)                                                      \
+    do {                                                               \
+        cudaError_t e_ = (expr);                                       \
+        if (e_ != cudaSuccess) return cuda_fail(dev, e_, #expr);       \
+    } while (0)
+#define RCP(expr)          \
+    do {                   \
+        int r_ = (expr);   \
+        if (r_) return r_; \
+    } while (0)
+
+// line kinds
+enum : uint8_t { K_SKIP = 0, K_ASNN = 1, K_INPUTS = 2, K_OUTPUTS = 3, K_EDGE = 4, K_OTHER = 5 };
+// error codes, in the reference's wording (formatted on the host)
+enum : uint8_t {
+    ERR_NONE = 0,
+    ERR_HEADER,        // expected header 'asnn 1'
+    ERR_VERSION,       // unsupported version '<v>'
+    ERR_INPUTS_KW,     // expected 'inputs' line
+    ERR_OUTPUTS_KW,    // expected 'outputs' line
+    ERR_UNKNOWN,       // unknown line '<kw>'
+    ERR_EDGE_NTOK,     // edge needs '<source> <target> <weight>'
+    ERR_BAD_SRC,       // bad node id '<tok 1>'
+    ERR_BAD_TGT,       // bad node id '<tok 2>'
+    ERR_BAD_W,         // bad weight '<tok 3>'
+    ERR_SELF,          // self-loop at node <id>
+    ERR_DUP,           // duplicate edge a->b
+    ERR_BAD_ID,        // bad node id '<tok>' on the inputs / outputs line (token index in aux)
+};
+enum : uint8_t { ES_OK = 0, ES_NTOK, ES_SRC, ES_TGT, ES_W, ES_SELF, ES_HOST };
+
+__device__ __forceinline__ bool tok_eq(const char* p, uint32_t n, const char* lit, uint32_t ln) {
+    if (n != ln) return false;
+    for (uint32_t i = 0; i < n; ++i)
+        if (p[i] != lit[i]) return false;
+    return true;
+}
+
+__global__ void k_nl_count(const char* __restrict__ t, uint64_t len, uint32_t* __restrict__ cnt) {
+    const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t b = c * 256, e = min(b + 256, len);
+    if (b >= len) return;
+    uint32_t n = 0;
+    for (uint64_t i = b; i < e; ++i) n += t[i] == '\n';
+    cnt[c] = n;
+}
+
+// starts[j + 1] = position after the j-th newline; starts[0] = 0 and
+// starts[n_lines] = len + 1 are written by the host.
+__global__ void k_nl_write(const char* __restrict__ t, uint64_t len, const uint32_t* __restrict__ off,
+                           uint64_t* __restrict__ starts) {
+    const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t b = c * 256, e = min(b + 256, len);
+    if (b >= len) return;
+    uint32_t j = off[c];
+    for (uint64_t i = b; i < e; ++i)
+        if (t[i] == '\n') starts[++j] = i + 1;
+}
+
+struct LineOut {
+    uint8_t* kind;
+    uint8_t* estat;
+    uint8_t* hdr;  // bit0: exactly 2 tokens, bit1: version token == "1"
+    uint32_t* src;
+    uint32_t* tgt;
+    float* w;
+};
+
+// One line per thread (io.cpp:92-146 for one line).
+__global__ void k_parse_lines(const char* __restrict__ t, const uint64_t* __restrict__ starts, uint32_t n_lines,
+                              LineOut o) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_lines) return;
+    const uint64_t s = starts[i];
+    uint64_t e = starts[i + 1] - 1;  // excludes the '\n' (or is len for the last line)
+    if (e > s && t[e - 1] == '\r') --e;
+    uint32_t ts[4], tl[4], nt = 0;
+    uint64_t p = s;
+    while (p < e) {
+        while (p < e && is_ws(t[p])) ++p;
+        const uint64_t b = p;
+        while (p < e && !is_ws(t[p])) ++p;
+        if (p > b) {
+            if (nt < 4) {
+                ts[nt] = static_cast<uint32_t>(b - s);
+                tl[nt] = static_cast<uint32_t>(p - b);
+            }
+            ++nt;
+        }
+    }
+    uint8_t kind = K_SKIP, es = ES_OK, hdr = 0;
+    uint32_t a = 0, b = 0;
+    float w = 0.0f;
+    if (nt > 0 && t[s + ts[0]] != '#') {
+        const char* k0 = t + s + ts[0];
+        if (tok_eq(k0, tl[0], "asnn", 4)) {
+            kind = K_ASNN;
+            hdr = (nt == 2 ? 1 : 0) | (nt >= 2 && tok_eq(t + s + ts[1], tl[1], "1", 1) ? 2 : 0);
+        } else if (tok_eq(k0, tl[0], "inputs", 6)) {
+            kind = K_INPUTS;
+        } else if (tok_eq(k0, tl[0], "outputs", 7)) {
+            kind = K_OUTPUTS;
+        } else if (tok_eq(k0, tl[0], "edge", 4)) {
+            kind = K_EDGE;
+            if (nt != 4) {
+                es = ES_NTOK;
+            } else if (parse_u32(t + s + ts[1], t + s + ts[1] + tl[1], a) != kTokOk) {
+                es = ES_SRC;
+            } else if (parse_u32(t + s + ts[2], t + s + ts[2] + tl[2], b) != kTokOk) {
+                es = ES_TGT;
+            } else {
+                const uint8_t r = parse_f32(t + s + ts[3], t + s + ts[3] + tl[3], w);
+                if (r == kTokErr) es = ES_W;
+                else if (r == kTokHost) es = ES_HOST;  // the host decides weight, then self-loop
+                else if (a == b) es = ES_SELF;         // checked after the weight, as the reference does
+            }
+        } else {
+            kind = K_OTHER;
+        }
+    }
+    o.kind[i] = kind;
+    o.estat[i] = es;
+    o.hdr[i] = hdr;
+    o.src[i] = a;
+    o.tgt[i] = b;
+    o.w[i] = w;
+}
+
+__global__ void k_sig_flags(const uint8_t* __restrict__ kind, uint32_t n, uint32_t* __restrict__ f) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) f[i] = kind[i] != K_SKIP;
+}
+
+// Per-line errors of the section state machine (io.cpp:104-145); also flags
+// the edge lines to keep and the weights the host must resolve.
+__global__ void k_line_errors(const uint8_t* __restrict__ kind, const uint8_t* __restrict__ estat,
+                              const uint8_t* __restrict__ hdr, const uint32_t* __restrict__ sig, uint32_t n,
+                              unsigned long long* __restrict__ first_err, uint32_t* __restrict__ special,
+                              uint32_t* __restrict__ keep) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keep[i] = 0;
+    const uint8_t k = kind[i];
+    if (k == K_SKIP) return;
+    const uint32_t si = sig[i];
+    uint8_t err = ERR_NONE;
+    if (si < 3) special[si] = i;
+    if (si == 0) {
+        if (k != K_ASNN || !(hdr[i] & 1)) err = ERR_HEADER;
+        else if (!(hdr[i] & 2)) err = ERR_VERSION;
+    } else if (si == 1) {
+        if (k != K_INPUTS) err = ERR_INPUTS_KW;
+    } else if (si == 2) {
+        if (k != K_OUTPUTS) err = ERR_OUTPUTS_KW;
+    } else if (k != K_EDGE) {
+        err = ERR_UNKNOWN;
+    } else {
+        switch (estat[i]) {
+            case ES_NTOK: err = ERR_EDGE_NTOK; break;
+            case ES_SRC: err = ERR_BAD_SRC; break;
+            case ES_TGT: err = ERR_BAD_TGT; break;
+            case ES_W: err = ERR_BAD_W; break;
+            case ES_SELF: err = ERR_SELF; break;
+            default: keep[i] = 1; break;  // ES_OK, ES_HOST
+        }
+    }
+    if (err != ERR_NONE) atomicMin(first_err, (static_cast<unsigned long long>(i) << 8) | err);
+}
+
+__global__ void k_compact_edges(const uint32_t* __restrict__ keep, const uint32_t* __restrict__ idx, uint32_t n,
+                                const uint32_t* __restrict__ src, const uint32_t* __restrict__ tgt,
+                                const float* __restrict__ w, const uint8_t* __restrict__ estat,
+                                uint32_t* __restrict__ es, uint32_t* __restrict__ et, float* __restrict__ ew,
+                                uint32_t* __restrict__ eline, uint32_t* __restrict__ host_flag) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !keep[i]) return;
+    const uint32_t j = idx[i];
+    es[j] = src[i];
+    et[j] = tgt[i];
+    ew[j] = w[i];
+    eline[j] = i;
+    host_flag[j] = estat[i] == ES_HOST;
+}
+
+// Sorted by (source, target) with stable order: the later of two equal
+// neighbours is a duplicate at its line (io.cpp:137-140).
+__global__ void k_dup_edges(const uint32_t* __restrict__ order, uint64_t E, const uint32_t* __restrict__ es,
+                            const uint32_t* __restrict__ et, const uint32_t* __restrict__ eline,
+                            unsigned long long* __restrict__ first_err) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k == 0 || k >= E) return;
+    const uint32_t a = order[k - 1], b = order[k];
+    if (es[a] == es[b] && et[a] == et[b])
+        atomicMin(first_err, (static_cast<unsigned long long>(eline[b]) << 8) | ERR_DUP);
+}
+
+// Token starts of one line [s, e) (the keyword is token 0).
+__global__ void k_tok_flags(const char* __restrict__ t, uint64_t s, uint64_t e, uint32_t* __restrict__ f) {
+    const uint64_t p = s + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= e) return;
+    f[p - s] = !is_ws(t[p]) && (p == s || is_ws(t[p - 1]));
+}
+
+// ids[k - 1] for every token k >= 1; bad tokens report their index.
+__global__ void k_tok_ids(const char* __restrict__ t, uint64_t s, uint64_t e, const uint32_t* __restrict__ f,
+                          const uint32_t* __restrict__ idx, uint32_t* __restrict__ ids,
+                          unsigned int* __restrict__ first_bad) {
+    const uint64_t p = s + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= e || !f[p - s]) return;
+    const uint32_t k = idx[p - s];
+    if (k == 0) return;
+    uint64_t q = p;
+    while (q < e && !is_ws(t[q])) ++q;
+    uint32_t v = 0;
+    if (parse_u32(t + p, t + q, v) != kTokOk) atomicMin(first_bad, k);
+    ids[k - 1] = v;
+}
+
+// validate: flags[i] = 1 when x[i] occurs earlier in x (sorted copy + stable
+// order: order[] sorts x by value, ties by position).
+__global__ void k_dup_decl(const uint32_t* __restrict__ sorted_vals, const uint32_t* __restrict__ order, uint32_t n,
+                           uint32_t* __restrict__ flag) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    flag[order[k]] = k > 0 && sorted_vals[k] == sorted_vals[k - 1];
+}
+
+__device__ __forceinline__ bool in_sorted(const uint32_t* __restrict__ a, uint32_t n, uint32_t v) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t m = (lo + hi) / 2;
+        if (a[m] < v) lo = m + 1;
+        else hi = m;
+    }
+    return lo < n && a[lo] == v;
+}
+
+__global__ void k_member_flags(const uint32_t* __restrict__ x, uint64_t n, const uint32_t* __restrict__ set,
+                               uint32_t n_set, uint32_t* __restrict__ flag) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = in_sorted(set, n_set, x[i]);
+}
+
+__global__ void k_unique_flags(const uint32_t* __restrict__ s, uint64_t n, uint32_t* __restrict__ f) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) f[i] = i == 0 || s[i] != s[i - 1];
+}
+
+__global__ void k_scatter_flagged(const uint32_t* __restrict__ v, const uint32_t* __restrict__ f,
+                                  const uint32_t* __restrict__ idx, uint64_t n, uint32_t* __restrict__ out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && f[i]) out[idx[i]] = v ? v[i] : static_cast<uint32_t>(i);
+}
+
+__global__ void k_iota(uint32_t* __restrict__ v, uint64_t n) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, uint64_t n,
+                             uint32_t* __restrict__ out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = src[idx[i]];
+}
+
+__global__ void k_parse_weights(const char* __restrict__ buf, const uint64_t* __restrict__ off, uint64_t n,
+                                float* __restrict__ out, uint8_t* __restrict__ status) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float v = 0.0f;
+    const uint8_t r = parse_f32(buf + off[i], buf + off[i + 1], v);
+    out[i] = r == kTokOk ? v : 0.0f;
+    status[i] = r;
+}
+
+// ---- host helpers ---------------------------------------------------------------
+std::vector<std::string_view> split_ws(std::string_view line) {
+    std::vector<std::string_view> out;
+    size_t i = 0;
+    while (i < line.size()) {
+        while (i < line.size() && (line[i] == ' ' || line[i] == '\t')) ++i;
+        const size_t b = i;
+        while (i < line.size() && line[i] != ' ' && line[i] != '\t') ++i;
+        if (i > b) out.push_back(line.substr(b, i - b));
+    }
+    return out;
+}
+
+std::string_view line_text(const char* text, uint64_t len, uint64_t s, uint64_t e_plus1) {
+    uint64_t e = std::min<uint64_t>(e_plus1 - 1, len);
+    std::string_view v(text + s, e - s);
+    if (!v.empty() && v.back() == '\r') v.remove_suffix(1);
+    return v;
+}
+
+// The reference's ParseError message for `code` on this line (io.cpp).
+std::string parse_message(uint8_t code, std::string_view line, uint32_t aux) {
+    const auto tok = split_ws(line);
+    auto t = [&](size_t k) { return k < tok.size() ? std::string(tok[k]) : std::string(); };
+    switch (code) {
+        case ERR_HEADER: return "expected header 'asnn 1'";
+        case ERR_VERSION: return "unsupported version '" + t(1) + "'";
+        case ERR_INPUTS_KW: return "expected 'inputs' line";
+        case ERR_OUTPUTS_KW: return "expected 'outputs' line";
+        case ERR_UNKNOWN: return "unknown line '" + t(0) + "'";
+        case ERR_EDGE_NTOK: return "edge needs '<source> <target> <weight>'";
+        case ERR_BAD_SRC: return "bad node id '" + t(1) + "'";
+        case ERR_BAD_TGT: return "bad node id '" + t(2) + "'";
+        case ERR_BAD_W: return "bad weight '" + t(3) + "'";
+        case ERR_SELF: {
+            uint32_t a = 0;
+            std::from_chars(tok[1].data(), tok[1].data() + tok[1].size(), a);
+            return "self-loop at node " + std::to_string(a);
+        }
+        case ERR_DUP: {
+            uint32_t a = 0, b = 0;
+            std::from_chars(tok[1].data(), tok[1].data() + tok[1].size(), a);
+            std::from_chars(tok[2].data(), tok[2].data() + tok[2].size(), b);
+            return "duplicate edge " + std::to_string(a) + "->" + std::to_string(b);
+        }
+        case ERR_BAD_ID: return "bad node id '" + t(aux) + "'";
+        default: return "parse error";
+    }
+}
+
+// find_cycle (network.cpp:107-149) on host copies -- only for the message of a
+// network the device already found cyclic.
+std::string cycle_message(const std::vector<uint32_t>& nodes, const std::vector<uint32_t>& src,
+                          const std::vector<uint32_t>& dst) {
+    const size_t n = nodes.size();
+    auto index = [&](uint32_t id) {
+        return static_cast<uint32_t>(std::lower_bound(nodes.begin(), nodes.end(), id) - nodes.begin());
+    };
+    std::vector<std::vector<uint32_t>> succ(n);
+    for (size_t k = 0; k < src.size(); ++k) succ[index(src[k])].push_back(index(dst[k]));
+    std::vector<uint8_t> color(n, 0);
+    for (size_t root = 0; root < n; ++root) {
+        if (color[root]) continue;
+        std::vector<std::pair<uint32_t, size_t>> stack;
+        stack.emplace_back(static_cast<uint32_t>(root), 0);
+        color[root] = 1;
+        while (!stack.empty()) {
+            auto& [node, pos] = stack.back();
+            if (pos < succ[node].size()) {
+                const uint32_t next = succ[node][pos++];
+                if (color[next] == 1) {
+                    std::vector<uint32_t> path{nodes[next]};
+                    for (auto it = stack.rbegin(); it != stack.rend(); ++it) {
+                        path.push_back(nodes[it->first]);
+                        if (it->first == next) break;
+                    }
+                    std::reverse(path.begin(), path.end());
+                    path.push_back(nodes[next]);
+                    std::string msg = "cycle:";
+                    for (size_t i = 0; i < path.size(); ++i) msg += (i ? "->" : " ") + std::to_string(path[i]);
+                    return msg;
+                }
+                if (color[next] == 0) {
+                    color[next] = 1;
+                    stack.emplace_back(next, 0);
+                }
+            } else {
+                color[node] = 2;
+                stack.pop_back();
+            }
+        }
+    }
+    return "cycle";
+}
+
+template <typename T>
+int d2h(asnn_dev* dev, std::vector<T>& h, const T* d, uint64_t n) {
+    h.resize(n);
+    if (n) CKP(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, dev->stream));
+    return ASNN_OK;
+}
+
+// compaction of flagged positions: out = indices i with f[i] (in order)
+int flagged_indices(asnn_dev* dev, const uint32_t* f, uint64_t n, std::vector<uint32_t>& out) {
+    cudaStream_t st = dev->stream;
+    out.clear();
+    if (!n) return ASNN_OK;
+    DevBuf<uint32_t> idx, tot, res;
+    CKP(idx.alloc(n));
+    CKP(tot.alloc(1));
+    RCP(exclusive_scan(dev, f, idx.p, n, tot.p, st));
+    uint32_t m = 0;
+    CKP(cudaMemcpyAsync(&m, tot.p, 4, cudaMemcpyDeviceToHost, st));
+    CKP(cudaStreamSynchronize(st));
+    if (!m) return ASNN_OK;
+    CKP(res.alloc(m));
+    k_scatter_flagged<<<nb(n), kT, 0, st>>>(nullptr, f, idx.p, n, res.p);
+    RCP(d2h(dev, out, res.p, m));
+    CKP(cudaStreamSynchronize(st));
+    return ASNN_OK;
+}
+
+int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result, uint32_t* err_line) {
+    cudaStream_t st = dev->stream;
+    *result = nullptr;
+    if (err_line) *err_line = 0;
+    asnn_timings& tm = dev->timings;
+    cudaEventRecord(dev->ev0, st);
+    // ---- 1. text and line starts
+    DevBuf<char> d_text;
+    CKP(d_text.alloc(len + 1));
+    if (len) CKP(cudaMemcpyAsync(d_text.p, text, len, cudaMemcpyHostToDevice, st));
+    const uint64_t n_chunks = (len + 255) / 256;
+    DevBuf<uint32_t> cnt, coff, tot;
+    CKP(cnt.alloc(n_chunks + 1));
+    CKP(coff.alloc(n_chunks + 1));
+    CKP(tot.alloc(1));
+    if (n_chunks) k_nl_count<<<nb(n_chunks), kT, 0, st>>>(d_text.p, len, cnt.p);
+    RCP(exclusive_scan(dev, cnt.p, coff.p, n_chunks, tot.p, st));
+    uint32_t n_nl = 0;
+    CKP(cudaMemcpyAsync(&n_nl, tot.p, 4, cudaMemcpyDeviceToHost, st));
+    CKP(cudaStreamSynchronize(st));
+    const uint32_t n_lines = n_nl + 1;  // the segment after the last '\n' is a line too
+    DevBuf<uint64_t> starts;
+    CKP(starts.alloc(static_cast<uint64_t>(n_lines) + 1));
+    const uint64_t h_first = 0, h_last = len + 1;
+    CKP(cudaMemcpyAsync(starts.p, &h_first, 8, cudaMemcpyHostToDevice, st));
+    CKP(cudaMemcpyAsync(starts.p + n_lines, &h_last, 8, cudaMemcpyHostToDevice, st));
+    if (n_chunks) k_nl_write<<<nb(n_chunks), kT, 0, st>>>(d_text.p, len, coff.p, starts.p);
+    // ---- 2. lines
+    DevBuf<uint8_t> kind, estat, hdr;
+    DevBuf<uint32_t> lsrc, ltgt, sigf, sig, keep, kidx;
+    DevBuf<float> lw;
+    CKP(kind.alloc(n_lines));
+    CKP(estat.alloc(n_lines));
+    CKP(hdr.alloc(n_lines));
+    CKP(lsrc.alloc(n_lines));
+    CKP(ltgt.alloc(n_lines));
+    CKP(lw.alloc(n_lines));
+    k_parse_lines<<<nb(n_lines), kT, 0, st>>>(d_text.p, starts.p, n_lines,
+                                               LineOut{kind.p, estat.p, hdr.p, lsrc.p, ltgt.p, lw.p});
+    CKP(cudaGetLastError());
+    // ---- 3-4. sections and per-line errors
+    CKP(sigf.alloc(n_lines));
+    CKP(sig.alloc(n_lines));
+    CKP(keep.alloc(n_lines));
+    CKP(kidx.alloc(n_lines));
+    k_sig_flags<<<nb(n_lines), kT, 0, st>>>(kind.p, n_lines, sigf.p);
+    DevBuf<uint32_t> tot2;
+    CKP(tot2.alloc(2));
+    RCP(exclusive_scan(dev, sigf.p, sig.p, n_lines, tot2.p, st));
+    DevBuf<unsigned long long> ferr;
+    DevBuf<uint32_t> special;
+    CKP(ferr.alloc(1));
+    CKP(special.alloc(3));
+    CKP(cudaMemsetAsync(ferr.p, 0xFF, 8, st));
+    CKP(cudaMemsetAsync(special.p, 0xFF, 12, st));
+    k_line_errors<<<nb(n_lines), kT, 0, st>>>(kind.p, estat.p, hdr.p, sig.p, n_lines, ferr.p, special.p, keep.p);
+    RCP(exclusive_scan(dev, keep.p, kidx.p, n_lines, tot2.p + 1, st));
+    uint32_t h_tot2[2], h_special[3];
+    CKP(cudaMemcpyAsync(h_tot2, tot2.p, 8, cudaMemcpyDeviceToHost, st));
+    CKP(cudaMemcpyAsync(h_special, special.p, 12, cudaMemcpyDeviceToHost, st));
+    CKP(cudaStreamSynchronize(st));
+    const uint32_t n_sig = h_tot2[0];
+    const uint64_t E = h_tot2[1];
+    DevBuf<uint32_t> es, et, eline, hflag;
+    DevBuf<float> ew;
+    CKP(es.alloc(E));
+    CKP(et.alloc(E));
+    CKP(ew.alloc(E));
+    CKP(eline.alloc(E));
+    CKP(hflag.alloc(E));
+    k_compact_edges<<<nb(n_lines), kT, 0, st>>>(keep.p, kidx.p, n_lines, lsrc.p, ltgt.p, lw.p, estat.p, es.p,
+                                                 et.p, ew.p, eline.p, hflag.p);
+    CKP(cudaGetLastError());
+    // duplicates: stable sort of edge indices by target, then by source
+    if (E > 1) {
+        DevBuf<uint32_t> keys, vals;
+        CKP(keys.alloc(E));
+        CKP(vals.alloc(E));
+        CKP(cudaMemcpyAsync(keys.p, et.p, E * 4, cudaMemcpyDeviceToDevice, st));
+        k_iota<<<nb(E), kT, 0, st>>>(vals.p, E);
+        SortBuffers sb;
+        uint32_t *ks = nullptr, *vs = nullptr;
+        RCP(radix_sort_pairs(dev, keys.p, vals.p, E, 32, sb, &ks, &vs, st));
+        DevBuf<uint32_t> k2;
+        CKP(k2.alloc(E));
+        k_gather_u32<<<nb(E), kT, 0, st>>>(es.p, vs, E, k2.p);
+        DevBuf<uint32_t> v2;
+        CKP(v2.alloc(E));
+        CKP(cudaMemcpyAsync(v2.p, vs, E * 4, cudaMemcpyDeviceToDevice, st));
+        SortBuffers sb2;
+        uint32_t *ks2 = nullptr, *vs2 = nullptr;
+        RCP(radix_sort_pairs(dev, k2.p, v2.p, E, 32, sb2, &ks2, &vs2, st));
+        k_dup_edges<<<nb(E), kT, 0, st>>>(vs2, E, es.p, et.p, eline.p, ferr.p);
+        CKP(cudaGetLastError());
+    }
+    // ---- 5. inputs / outputs ids
+    std::vector<uint64_t> h_starts_sp(6, 0);
+    DevBuf<uint32_t> ids[2];
+    uint32_t n_ids[2] = {0, 0};
+    unsigned long long h_bad_tok[2] = {~0ull, ~0ull};
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t line = h_special[1 + k];
+        if (line == 0xFFFFFFFFu) continue;
+        uint64_t se[2];
+        CKP(cudaMemcpyAsync(se, starts.p + line, 16, cudaMemcpyDeviceToHost, st));
+        CKP(cudaStreamSynchronize(st));
+        uint64_t s = se[0], e = std::min<uint64_t>(se[1] - 1, len);
+        if (e > s && text[e - 1] == '\r') --e;
+        const uint64_t L = e - s;
+        if (!L) continue;
+        DevBuf<uint32_t> f, idx, t1;
+        DevBuf<unsigned int> bad;
+        CKP(f.alloc(L));
+        CKP(idx.alloc(L));
+        CKP(t1.alloc(1));
+        CKP(bad.alloc(1));
+        CKP(cudaMemsetAsync(bad.p, 0xFF, 4, st));
+        k_tok_flags<<<nb(L), kT, 0, st>>>(d_text.p, s, e, f.p);
+        RCP(exclusive_scan(dev, f.p, idx.p, L, t1.p, st));
+        uint32_t ntok = 0;
+        CKP(cudaMemcpyAsync(&ntok, t1.p, 4, cudaMemcpyDeviceToHost, st));
+        CKP(cudaStreamSynchronize(st));
+        n_ids[k] = ntok ? ntok - 1 : 0;
+        CKP(ids[k].alloc(n_ids[k] + 1));
+        k_tok_ids<<<nb(L), kT, 0, st>>>(d_text.p, s, e, f.p, idx.p, ids[k].p, bad.p);
+        unsigned int hb = 0;
+        CKP(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, st));
+        CKP(cudaStreamSynchronize(st));
+        if (hb != 0xFFFFFFFFu) h_bad_tok[k] = hb;
+    }
+    // ---- host side of the error decision
+    unsigned long long h_ferr = 0;
+    CKP(cudaMemcpyAsync(&h_ferr, ferr.p, 8, cudaMemcpyDeviceToHost, st));
+    std::vector<uint32_t> host_edges;
+    RCP(flagged_indices(dev, hflag.p, E, host_edges));
+    uint64_t best = h_ferr;  // (line << 8 | code), UINT64_MAX = none
+    uint32_t best_aux = 0;
+    for (int k = 0; k < 2; ++k)
+        if (h_bad_tok[k] != ~0ull) {
+            const uint64_t v = (static_cast<uint64_t>(h_special[1 + k]) << 8) | ERR_BAD_ID;
+            if (v < best) {
+                best = v;
+                best_aux = static_cast<uint32_t>(h_bad_tok[k]);
+            }
+        }
+    std::vector<uint32_t> h_elines;
+    std::vector<std::pair<uint32_t, float>> patches;
+    if (!host_edges.empty()) {  // weights std::from_chars must decide
+        std::vector<uint32_t> all_lines;
+        RCP(d2h(dev, all_lines, eline.p, E));
+        std::vector<uint64_t> h_st(n_lines + 1);
+        CKP(cudaMemcpyAsync(h_st.data(), starts.p, (n_lines + 1) * 8ull, cudaMemcpyDeviceToHost, st));
+        CKP(cudaStreamSynchronize(st));
+        for (uint32_t j : host_edges) {
+            const uint32_t line = all_lines[j];
+            const auto tok = split_ws(line_text(text, len, h_st[line], h_st[line + 1]));
+            float v = 0.0f;
+            const auto r = std::from_chars(tok[3].data(), tok[3].data() + tok[3].size(), v);
+            uint32_t a = 0, b = 1;
+            std::from_chars(tok[1].data(), tok[1].data() + tok[1].size(), a);
+            std::from_chars(tok[2].data(), tok[2].data() + tok[2].size(), b);
+            uint8_t code = ERR_NONE;
+            if (r.ec != std::errc{} || r.ptr != tok[3].data() + tok[3].size()) code = ERR_BAD_W;
+            else if (a == b) code = ERR_SELF;
+            if (code != ERR_NONE) {
+                const uint64_t cand = (static_cast<uint64_t>(line) << 8) | code;
+                if (cand < best) best = cand;
+            } else {
+                patches.emplace_back(j, v);
+            }
+        }
+    }
+    if (best == ~0ull && n_sig < 3) {  // io.cpp:149: no edges section reached
+        std::string msg = "line " + std::to_string(n_lines) + ": truncated file";
+        dev->err = msg;
+        if (err_line) *err_line = n_lines;
+        return ASNN_E_PARSE;
+    }
+    if (best != ~0ull) {
+        const uint32_t line = static_cast<uint32_t>(best >> 8);
+        uint64_t se[2];
+        CKP(cudaMemcpyAsync(se, starts.p + line, 16, cudaMemcpyDeviceToHost, st));
+        CKP(cudaStreamSynchronize(st));
+        const std::string msg = parse_message(static_cast<uint8_t>(best & 0xFF),
+                                              line_text(text, len, se[0], se[1]), best_aux);
+        dev->err = "line " + std::to_string(line + 1) + ": " + msg;
+        if (err_line) *err_line = line + 1;
+        return ASNN_E_PARSE;
+    }
+    for (const auto& pv : patches) CKP(cudaMemcpyAsync(ew.p + pv.first, &pv.second, 4, cudaMemcpyHostToDevice, st));
+    // ---- 6. make_network (network.cpp:39-55): nodes = sorted unique ids
+    const uint64_t n_all = n_ids[0] + n_ids[1] + 2 * E;
+    DevBuf<uint32_t> all, nodes;
+    CKP(all.alloc(n_all + 1));
+    uint64_t o = 0;
+    for (int k = 0; k < 2; ++k) {
+        if (n_ids[k]) CKP(cudaMemcpyAsync(all.p + o, ids[k].p, n_ids[k] * 4ull, cudaMemcpyDeviceToDevice, st));
+        o += n_ids[k];
+    }
+    if (E) {
+        CKP(cudaMemcpyAsync(all.p + o, es.p, E * 4, cudaMemcpyDeviceToDevice, st));
+        CKP(cudaMemcpyAsync(all.p + o + E, et.p, E * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    uint32_t N = 0;
+    if (n_all) {
+        SortBuffers sb;
+        uint32_t *ks = nullptr, *vs = nullptr;
+        RCP(radix_sort_pairs(dev, all.p, nullptr, n_all, 32, sb, &ks, &vs, st));
+        DevBuf<uint32_t> f, idx, t1;
+        CKP(f.alloc(n_all));
+        CKP(idx.alloc(n_all));
+        CKP(t1.alloc(1));
+        k_unique_flags<<<nb(n_all), kT, 0, st>>>(ks, n_all, f.p);
+        RCP(exclusive_scan(dev, f.p, idx.p, n_all, t1.p, st));
+        CKP(cudaMemcpyAsync(&N, t1.p, 4, cudaMemcpyDeviceToHost, st));
+        CKP(cudaStreamSynchronize(st));
+        CKP(nodes.alloc(N));
+        k_scatter_flagged<<<nb(n_all), kT, 0, st>>>(ks, f.p, idx.p, n_all, nodes.p);
+        CKP(cudaGetLastError());
+    }
+    // ---- validate (network.cpp:151-216)
+    std::vector<std::string> viol;
+    if (!n_ids[0]) viol.push_back("inputs list is empty");
+    if (!n_ids[1]) viol.push_back("outputs list is empty");
+    DevBuf<uint32_t> sorted_in;  // sorted inputs (with repeats) for membership
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t n = n_ids[k];
+        if (!n) continue;
+        DevBuf<uint32_t> keys, vals, flag;
+        CKP(keys.alloc(n));
+        CKP(vals.alloc(n));
+        CKP(flag.alloc(n));
+        CKP(cudaMemcpyAsync(keys.p, ids[k].p, n * 4ull, cudaMemcpyDeviceToDevice, st));
+        k_iota<<<nb(n), kT, 0, st>>>(vals.p, n);
+        SortBuffers sb;
+        uint32_t *ks = nullptr, *vs = nullptr;
+        RCP(radix_sort_pairs(dev, keys.p, vals.p, n, 32, sb, &ks, &vs, st));
+        k_dup_decl<<<nb(n), kT, 0, st>>>(ks, vs, n, flag.p);
+        std::vector<uint32_t> dups, h_ids;
+        RCP(flagged_indices(dev, flag.p, n, dups));
+        if (!dups.empty()) {
+            RCP(d2h(dev, h_ids, ids[k].p, n));
+            CKP(cudaStreamSynchronize(st));
+            for (uint32_t i : dups)
+                viol.push_back("duplicate node " + std::to_string(h_ids[i]) + " in " + (k ? "outputs" : "inputs"));
+        }
+        if (k == 0) {
+            CKP(sorted_in.alloc(n));
+            CKP(cudaMemcpyAsync(sorted_in.p, ks, n * 4ull, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    if (n_ids[0] && n_ids[1]) {  // input/output overlap, in outputs order
+        DevBuf<uint32_t> flag;
+        CKP(flag.alloc(n_ids[1]));
+        k_member_flags<<<nb(n_ids[1]), kT, 0, st>>>(ids[1].p, n_ids[1], sorted_in.p, n_ids[0], flag.p);
+        std::vector<uint32_t> ov, h_out;
+        RCP(flagged_indices(dev, flag.p, n_ids[1], ov));
+        if (!ov.empty()) {
+            RCP(d2h(dev, h_out, ids[1].p, n_ids[1]));
+            CKP(cudaStreamSynchronize(st));
+            std::string m = "input/output overlap:";
+            for (size_t i = 0; i < ov.size(); ++i) m += (i ? " " : " ") + std::to_string(h_out[ov[i]]);
+            viol.push_back(m);
+        }
+    }
+    if (n_ids[0] && E) {  // inputs with incoming connections, in connection order
+        DevBuf<uint32_t> flag;
+        CKP(flag.alloc(E));
+        k_member_flags<<<nb(E), kT, 0, st>>>(et.p, E, sorted_in.p, n_ids[0], flag.p);
+        std::vector<uint32_t> inc;
+        RCP(flagged_indices(dev, flag.p, E, inc));
+        if (!inc.empty()) {
+            std::vector<uint32_t> hs, ht;
+            RCP(d2h(dev, hs, es.p, E));
+            RCP(d2h(dev, ht, et.p, E));
+            CKP(cudaStreamSynchronize(st));
+            for (uint32_t j : inc)
+                viol.push_back("input " + std::to_string(ht[j]) + " has incoming connection from " +
+                               std::to_string(hs[j]));
+        }
+    }
+    bool cyclic = false;
+    if (E) RCP(device_cycle_check(dev, nodes.p, N, es.p, et.p, E, &cyclic));
+    auto* c = new asnn_corpus;
+    int rc = d2h(dev, c->nodes, nodes.p, N);
+    if (!rc) rc = d2h(dev, c->inputs, ids[0].p, n_ids[0]);
+    if (!rc) rc = d2h(dev, c->outputs, ids[1].p, n_ids[1]);
+    if (!rc) rc = d2h(dev, c->src, es.p, E);
+    if (!rc) rc = d2h(dev, c->dst, et.p, E);
+    if (!rc) rc = d2h(dev, c->w, ew.p, E);
+    if (rc) {
+        delete c;
+        return rc;
+    }
+    cudaEventRecord(dev->ev1, st);
+    const cudaError_t ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) {
+        delete c;
+        return cuda_fail(dev, ce, "parse");
+    }
+    cudaEventElapsedTime(&tm.upload_ms, dev->ev0, dev->ev1);
+    if (cyclic) viol.push_back(cycle_message(c->nodes, c->src, c->dst));
+    if (!viol.empty()) {
+        delete c;
+        std::string m = "invalid network";
+        for (const auto& v : viol) m += "\n  " + v;
+        dev->err = m;
+        return ASNN_E_VALIDATION;
+    }
+    *result = c;
+    return ASNN_OK;
+}
+
+}  // namespace
+}  // namespace asnn_b200
+
+extern "C" {
+
+int asnn_dev_parse_network(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** out, uint32_t* err_line) {
+    if (!dev || !out || (!text && len)) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    const cudaError_t e = cudaSetDevice(dev->device);
+    if (e != cudaSuccess) return asnn_b200::cuda_fail(dev, e, "cudaSetDevice");
+    return asnn_b200::do_parse(dev, text, len, out, err_line);
+}
+
+int asnn_dev_parse_weights(asnn_dev* dev, const char* buf, const uint64_t* off, uint64_t n, float* out,
+                           uint8_t* status) {
+    using namespace asnn_b200;
+    if (!dev || (n && (!buf || !off || !out || !status))) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    if (!n) return ASNN_OK;
+    CKP(cudaSetDevice(dev->device));
+    cudaStream_t st = dev->stream;
+    const uint64_t bytes = off[n];
+    DevBuf<char> d_buf;
+    DevBuf<uint64_t> d_off;
+    DevBuf<float> d_out;
+    DevBuf<uint8_t> d_st;
+    CKP(d_buf.alloc(bytes + 1));
+    CKP(d_off.alloc(n + 1));
+    CKP(d_out.alloc(n));
+    CKP(d_st.alloc(n));
+    if (bytes) CKP(cudaMemcpyAsync(d_buf.p, buf, bytes, cudaMemcpyHostToDevice, st));
+    CKP(cudaMemcpyAsync(d_off.p, off, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+    k_parse_weights<<<nb(n), kT, 0, st>>>(d_buf.p, d_off.p, n, d_out.p, d_st.p);
+    CKP(cudaGetLastError());
+    CKP(cudaMemcpyAsync(out, d_out.p, n * 4, cudaMemcpyDeviceToHost, st));
+    CKP(cudaMemcpyAsync(status, d_st.p, n, cudaMemcpyDeviceToHost, st));
+    CKP(cudaStreamSynchronize(st));
+    for (uint64_t i = 0; i < n; ++i) {
+        if (status[i] != kTokHost) continue;
+        float v = 0.0f;
+        const auto r = std::from_chars(buf + off[i], buf + off[i + 1], v);
+        const bool ok = r.ec == std::errc{} && r.ptr == buf + off[i + 1];
+        out[i] = ok ? v : 0.0f;
+        status[i] = ok ? 2 : 3;
+    }
+    return ASNN_OK;
+}
+
+int asnn_dev_read_network(asnn_dev* dev, const char* path, asnn_corpus** out, uint32_t* err_line) {
+    if (!dev || !path || !out) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    FILE* f = std::fopen(path, "rb");
+    if (!f) {
+        dev->err = std::string("cannot open ") + path;
+        return ASNN_E_IO;
+    }
+    std::vector<char> buf;
+    char tmp[1 << 16];
+    size_t n;
+    while ((n = std::fread(tmp, 1, sizeof(tmp), f)) > 0) buf.insert(buf.end(), tmp, tmp + n);
+    const bool bad = std::ferror(f) != 0;
+    std::fclose(f);
+    if (bad) {
+        dev->err = std::string("failed reading ") + path;
+        return ASNN_E_IO;
+    }
+    const cudaError_t e = cudaSetDevice(dev->device);
+    if (e != cudaSuccess) return asnn_b200::cuda_fail(dev, e, "cudaSetDevice");
+    return asnn_b200::do_parse(dev, buf.data(), buf.size(), out, err_line);
+}
+
+}  // extern "C"

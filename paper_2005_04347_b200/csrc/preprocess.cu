@@ -760,6 +760,20 @@ int preprocess(asnn_dev* dev, uint32_t G, const asnn_network_desc* nets, const u
     return ASNN_OK;
 }
 
+__global__ void k_seed_sources(const uint32_t* __restrict__ pred_off, uint32_t N, uint32_t* __restrict__ level,
+                               uint32_t* __restrict__ q, uint32_t* __restrict__ cnt) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < N && pred_off[i + 1] == pred_off[i]) {
+        level[i] = 0u;
+        q[atomicAdd(cnt, 1u)] = i;
+    }
+}
+
+__global__ void k_count_unplaced(const uint32_t* __restrict__ level, uint32_t N, uint32_t* __restrict__ cnt) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < N && level[i] == kUn) atomicAdd(cnt, 1u);
+}
+
 int build(asnn_dev* dev, uint32_t G, const asnn_network_desc* nets, asnn_dev_layout** out) {
     if (!dev || !nets || !out) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
@@ -785,6 +799,51 @@ int build(asnn_dev* dev, uint32_t G, const asnn_network_desc* nets, asnn_dev_lay
 }
 
 }  // namespace
+
+// Cycle test of validate (network.cpp:204): Kahn from every node without
+// predecessors over all connections; a node left without a level lies on, or
+// downstream of, a cycle.  nodes sorted unique; src / dst ids (device).
+int asnn_b200::device_cycle_check(asnn_dev* dev, const uint32_t* nodes, uint32_t N, const uint32_t* src,
+                                  const uint32_t* dst, uint64_t E, bool* cyclic) {
+    cudaStream_t st = dev->stream;
+    *cyclic = false;
+    if (!N || !E) return ASNN_OK;
+    DevNet d;
+    d.N = N;
+    d.E = E;
+    d.dense = false;
+    CK(d.nodes.alloc(N));
+    CK(d.src.alloc(E));
+    CK(d.dst.alloc(E));
+    CK(cudaMemcpyAsync(d.nodes.p, nodes, N * 4ull, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(d.src.p, src, E * 4ull, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(d.dst.p, dst, E * 4ull, cudaMemcpyDeviceToDevice, st));
+    RC(build_adjacency(dev, d));
+    DevBuf<uint32_t> rem, q0, q1, cnt, req, level;
+    CK(level.alloc(N + 1));
+    CK(cudaMemsetAsync(level.p, 0xFF, (N + 1) * 4ull, st));
+    CK(req.alloc(N + 1));
+    CK(cudaMemsetAsync(req.p, 0x01, (N + 1) * 4ull, st));  // nonzero: every node may be placed
+    CK(rem.alloc(N + 1));
+    k_degree<<<nblk(N), kT, 0, st>>>(d.pred_off.p, N, rem.p);
+    CK(q0.alloc(N + 1));
+    CK(q1.alloc(N + 1));
+    CK(cnt.alloc(4));
+    CK(cudaMemsetAsync(cnt.p, 0, 16, st));
+    k_seed_sources<<<nblk(N), kT, 0, st>>>(d.pred_off.p, N, level.p, q0.p, cnt.p);
+    CK(cudaGetLastError());
+    uint32_t blocks = 0;
+    RC(coop_grid(dev, reinterpret_cast<const void*>(k_kahn), &blocks));
+    void* args[] = {&d.succ_off.p, &d.succ_adj.p, &rem.p, &req.p, &level.p, &q0.p, &q1.p, &cnt.p};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_kahn), blocks, kT, args, 0, st));
+    CK(cudaMemsetAsync(cnt.p + 3, 0, 4, st));
+    k_count_unplaced<<<nblk(N), kT, 0, st>>>(level.p, N, cnt.p + 3);
+    uint32_t h = 0;
+    CK(cudaMemcpyAsync(&h, cnt.p + 3, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *cyclic = h != 0;
+    return ASNN_OK;
+}
 
 extern "C" {
 

@@ -8,6 +8,8 @@
 //   flatten             layout.cpp:12-83         -> asnn_dev_build_layout + download
 //   eval_parallel       eval.cpp:49-80           -> asnn_dev_upload_layout + asnn_dev_activate
 //   read_outputs, layer_slice_bounds, max_layer_width, depth, unassigned_outputs
+//   parse_network       io.cpp:83-156 + validate -> asnn_dev_parse_network
+//   read_network        io.cpp:167-173           -> asnn_dev_read_network
 //
 // Types keep the reference's field names and meanings; exceptions mirror
 // errors.hpp:9-55.  There is no host evaluator: ParallelConfig defaults to
@@ -23,6 +25,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <utility>
 #include <vector>
 
@@ -40,6 +43,24 @@ struct LayerOutOfRange : std::out_of_range { using std::out_of_range::out_of_ran
 struct BackendUnavailable : std::runtime_error { using std::runtime_error::runtime_error; };
 struct InfeasibleSpec : std::runtime_error { using std::runtime_error::runtime_error; };
 struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct IoError : std::runtime_error { using std::runtime_error::runtime_error; };
+// ParseError: what() = "line N: ...", line = N (errors.hpp:31-35).
+struct ParseError : std::runtime_error {
+    ParseError(int line_no, const std::string& what) : std::runtime_error(what), line(line_no) {}
+    int line;
+};
+// ValidationError: what() = "invalid network\n  ..." (errors.hpp:37-53).
+struct ValidationError : std::runtime_error {
+    explicit ValidationError(const std::string& what) : std::runtime_error(what) {
+        std::size_t p = what.find("\n  ");
+        while (p != std::string::npos) {
+            const std::size_t q = what.find("\n  ", p + 3);
+            violations.push_back(what.substr(p + 3, q == std::string::npos ? std::string::npos : q - p - 3));
+            p = q;
+        }
+    }
+    std::vector<std::string> violations;
+};
 
 // ---- network.hpp:12-32 ---------------------------------------------------------
 struct Connection {
@@ -141,6 +162,8 @@ namespace detail {
         case ASNN_E_LAYER_RANGE: throw LayerOutOfRange(msg);
         case ASNN_E_INFEASIBLE: throw InfeasibleSpec(msg);
         case ASNN_E_INVALID: throw std::invalid_argument(msg);
+        case ASNN_E_VALIDATION: throw ValidationError(msg);
+        case ASNN_E_IO: throw IoError(msg);
         default: throw DeviceError(msg);
     }
 }
@@ -191,6 +214,44 @@ struct NetView {
 };
 
 }  // namespace detail
+
+// ---- io.hpp:23-31: loading, parsed and validated on the device -------------------------
+namespace detail {
+inline Network network_from_corpus(asnn_corpus* c) {
+    asnn_network_desc d{};
+    asnn_corpus_desc(c, &d);
+    Network net;
+    net.nodes.assign(d.nodes, d.nodes + d.n_nodes);
+    net.inputs.assign(d.inputs, d.inputs + d.n_inputs);
+    net.outputs.assign(d.outputs, d.outputs + d.n_outputs);
+    net.connections.resize(d.n_connections);
+    for (std::uint64_t k = 0; k < d.n_connections; ++k)
+        net.connections[k] = Connection{d.source[k], d.target[k], d.weight[k]};
+    asnn_corpus_free(c);
+    return net;
+}
+inline Network load(int rc, asnn_dev* dev, asnn_corpus* c, std::uint32_t line) {
+    if (rc == ASNN_E_PARSE) throw ParseError(static_cast<int>(line), asnn_dev_last_error(dev));
+    check(rc, dev);
+    return network_from_corpus(c);
+}
+}  // namespace detail
+
+inline Network parse_network(std::string_view text) {
+    asnn_dev* dev = detail::device();
+    asnn_corpus* c = nullptr;
+    std::uint32_t line = 0;
+    const int rc = asnn_dev_parse_network(dev, text.data(), text.size(), &c, &line);
+    return detail::load(rc, dev, c, line);
+}
+
+inline Network read_network(const std::string& path) {
+    asnn_dev* dev = detail::device();
+    asnn_corpus* c = nullptr;
+    std::uint32_t line = 0;
+    const int rc = asnn_dev_read_network(dev, path.c_str(), &c, &line);
+    return detail::load(rc, dev, c, line);
+}
 
 // ---- the path ---------------------------------------------------------------------------
 inline RequiredSet compute_required(const Network& net) {

@@ -194,8 +194,48 @@ static void random_vs_oracle() {
     }
 }
 
+// io.hpp through the facade: the test_io.cpp scenarios of the reference
+// (round trip, comments / blank lines / CRLF, ParseError line numbers,
+// ValidationError messages, IoError).
+static void io_cases() {
+    const std::string text =
+        "# a comment\n\nasnn 1\r\ninputs 0 1\noutputs 3\nedge 0 2 0.5\n  edge\t1 2 -0.25\nedge 2 3 1e-3\n";
+    const Network net = parse_network(text);
+    CHECK(net.nodes == std::vector<NodeId>({0, 1, 2, 3}));
+    CHECK(net.inputs == std::vector<NodeId>({0, 1}) && net.outputs == std::vector<NodeId>({3}));
+    CHECK(net.connections.size() == 3 && net.connections[1].source == 1 && net.connections[1].weight == -0.25f);
+    CHECK(net.connections[2].weight == 1e-3f);
+    auto parse_line = [](const std::string& t) {
+        try {
+            parse_network(t);
+        } catch (const ParseError& e) {
+            return e.line;
+        }
+        return -1;
+    };
+    CHECK(parse_line("asnn 2\ninputs 0\noutputs 1\n") == 1);
+    CHECK(parse_line("asnn 1\ninputs 0\noutputs 1\nedge 0 1 0.5\nedge 0 1 0.5\n") == 5);
+    CHECK(parse_line("asnn 1\ninputs 0\noutputs 1\nedge 0 1 x\n") == 4);
+    CHECK(parse_line("asnn 1\ninputs 0\n") == 3);  // truncated file
+    bool validation = false;
+    try {
+        parse_network("asnn 1\ninputs 0\noutputs 2\nedge 0 1 1\nedge 1 2 1\nedge 2 1 1\n");
+    } catch (const ValidationError& e) {
+        validation = e.violations.size() == 1 && e.violations[0] == "cycle: 1->2->1";
+    }
+    CHECK(validation);
+    bool io = false;
+    try {
+        read_network("/nonexistent/dir/net.asnn");
+    } catch (const IoError&) {
+        io = true;
+    }
+    CHECK(io);
+}
+
 int main() {
     try {
+        io_cases();
         segmentation_cases();
         layout_cases();
         eval_cases();

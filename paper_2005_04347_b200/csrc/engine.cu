@@ -2,6 +2,7 @@
 // the C-ABI entry points of include/asnn_dev.h (except preprocessing, which
 // lives in preprocess.cu and corpora in netgen.cpp).
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -364,7 +365,12 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         // CTAs-per-SM the activations alone allow; at least 2 layers when that
         // leaves too little, else whatever remains (big layers read global)
         const uint64_t want = 32 * max_layer;
-        const uint64_t fit = std::max<uint64_t>(1, per_sm / (fixed + 1024 + std::min<uint64_t>(want, 4096)));
+        // a launch of at most one CTA per SM (a single small network) takes
+        // all of the shared memory for its ring
+        const uint64_t ctas = static_cast<uint64_t>(ldA / C) * L->nets.size();
+        const uint64_t fit = ctas <= static_cast<uint64_t>(L->dev->sm_count)
+                                 ? 1
+                                 : std::max<uint64_t>(1, per_sm / (fixed + 1024 + std::min<uint64_t>(want, 4096)));
         const uint64_t budget = std::min<uint64_t>(kMaxDynSmem, per_sm / fit - 1024);
         uint64_t ring = budget > fixed ? budget - fixed : 0;
         if (ring < 2 * max_layer) ring = std::min<uint64_t>(2 * max_layer, kMaxDynSmem - fixed);
@@ -1420,12 +1426,14 @@ int asnn_dev_activate(asnn_dev_layout* L, const float* x, uint32_t n_vec, uint64
         void* xd = xb ? mapped_device_ptr(x) : nullptr;
         void* od = (out && ob) ? mapped_device_ptr(out) : nullptr;
         if ((xd || !xb) && (od || !(out && ob))) {
-            CK(cudaEventRecord(dev->ev0, st));
+            // no events on this latency-critical path: activate_ms is the
+            // call's wall time (it includes the launch and the wait)
+            const auto t0 = std::chrono::steady_clock::now();
             int rc = run_sweep(L, static_cast<const float*>(xd), n_vec, static_cast<float*>(od), nullptr);
             if (rc) return rc;
-            CK(cudaEventRecord(dev->ev1, st));
-            CK(cudaEventSynchronize(dev->ev1));
-            cudaEventElapsedTime(&dev->timings.activate_ms, dev->ev0, dev->ev1);
+            CK(cudaStreamSynchronize(st));
+            dev->timings.activate_ms =
+                std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
             return ASNN_OK;
         }
     }

@@ -221,7 +221,7 @@ static void io_cases() {
     try {
         parse_network("asnn 1\ninputs 0\noutputs 2\nedge 0 1 1\nedge 1 2 1\nedge 2 1 1\n");
     } catch (const ValidationError& e) {
-        validation = e.violations.size() == 1 && e.violations[0] == "cycle: 1->2->1";
+        validation = e.violations.size() == 1 && e.violations[0] == "cycle: 1->2->1->1";  // network.cpp:125-135 path format
     }
     CHECK(validation);
     bool io = false;

@@ -921,8 +921,20 @@ int run_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out, fl
     if (rc) return rc;
     cudaStream_t st = dev->stream;
     SweepGraph& g = L->graph;
-    if (!(g.exec && g.n_vec == n_vec && g.x == x && g.out == out && g.state == state &&
-          g.stream == st && g.epoch == dev->option_epoch)) {
+    const bool same = g.n_vec == n_vec && g.x == x && g.out == out && g.state == state && g.stream == st &&
+                      g.epoch == dev->option_epoch;
+    if (!(g.exec && same)) {
+        if (!(g.seen && same)) {  // first time with these parameters: launch directly
+            g.reset();
+            g.seen = true;
+            g.n_vec = n_vec;
+            g.x = x;
+            g.out = out;
+            g.state = state;
+            g.stream = st;
+            g.epoch = dev->option_epoch;
+            return launch_sweep(L, x, n_vec, out, state, st);
+        }
         g.reset();
         // L2 persistence for the front of the activation array: positions are
         // level-sorted, so the earliest layers -- the sources most later rows
@@ -1089,6 +1101,16 @@ int asnn_dev_open(int device, asnn_dev** out) {
         return ASNN_E_UNAVAILABLE;
     }
     dev->stream = dev->own_stream;
+    // stream-ordered allocations (engine.hpp AllocStream) keep freed memory in
+    // the device's default pool instead of returning it at every synchronise
+    {
+        cudaMemPool_t pool = nullptr;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    }
     dev->heavy_threshold = default_heavy_threshold();
     if (const char* m = getenv("ASNN_SWEEP_MODE")) dev->sweep_mode = static_cast<uint32_t>(atoi(m)) % 4;
     // The heavy-row branch gets the highest stream priority: its CTAs carry
@@ -1167,6 +1189,7 @@ int asnn_dev_last_timings(const asnn_dev* dev, asnn_timings* out) {
 int asnn_dev_upload_layout(asnn_dev* dev, const asnn_layout_desc* d, asnn_dev_layout** out) {
     if (!dev || !d || !out) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
     *out = nullptr;
     CK(cudaSetDevice(dev->device));
     if (d->total_layers == 0 && d->node_count) return fail(dev, ASNN_E_INVALID, "layers missing");
@@ -1354,6 +1377,7 @@ int asnn_dev_profile_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_ve
     if (!L || !ms || !n_launches) return ASNN_E_INVALID;
     asnn_dev* dev = L->dev;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
     CK(cudaSetDevice(dev->device));
     int rc = ensure_workspace(L, n_vec);
     if (rc) return rc;
@@ -1373,6 +1397,8 @@ int asnn_dev_profile_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_ve
 int asnn_dev_activate_plan(asnn_dev_layout* L, uint32_t n_vec, uint32_t* kernels, uint64_t* alg_bytes,
                            uint64_t* conn_evals) {
     if (!L) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(L->dev->mu);
+    asnn_b200::AllocStream alloc_on(L->dev->stream);
     const uint32_t k = sweep_launches(L, n_vec, false);
     if (kernels) *kernels = k;
     const uint64_t B = n_vec, E = L->total_edges, N = L->total_pos;
@@ -1393,6 +1419,7 @@ int asnn_dev_activate_device(asnn_dev_layout* L, const float* x_dev, uint32_t n_
     if (!L) return ASNN_E_INVALID;
     asnn_dev* dev = L->dev;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
     if (n_vec == 0) return ASNN_OK;
     CK(cudaSetDevice(dev->device));
     return run_sweep(L, x_dev, n_vec, out_dev, nullptr);
@@ -1404,6 +1431,7 @@ int asnn_dev_activate(asnn_dev_layout* L, const float* x, uint32_t n_vec, uint64
     if (!L) return ASNN_E_INVALID;
     asnn_dev* dev = L->dev;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
     // eval.cpp:26-28 -- arity check (per vector, all networks).
     if (n_x != static_cast<uint64_t>(L->total_in) * n_vec)
         return fail(dev, ASNN_E_ARITY,
@@ -1441,9 +1469,9 @@ int asnn_dev_activate(asnn_dev_layout* L, const float* x, uint32_t n_vec, uint64
     if (xb) {
         const float* src = x;
         if (!is_pinned(x)) {
-            CK(L->pin_x.ensure(xb));
-            std::memcpy(L->pin_x.p, x, xb);
-            src = static_cast<const float*>(L->pin_x.p);
+            CK(dev->pin_x.ensure(xb));
+            std::memcpy(dev->pin_x.p, x, xb);
+            src = static_cast<const float*>(dev->pin_x.p);
         }
         CK(cudaMemcpyAsync(L->x_stage.p, src, xb, cudaMemcpyHostToDevice, st));
     }
@@ -1455,8 +1483,8 @@ int asnn_dev_activate(asnn_dev_layout* L, const float* x, uint32_t n_vec, uint64
         if (is_pinned(out)) {
             CK(cudaMemcpyAsync(out, L->out_stage.p, ob, cudaMemcpyDeviceToHost, st));
         } else {
-            CK(L->pin_out.ensure(ob));
-            CK(cudaMemcpyAsync(L->pin_out.p, L->out_stage.p, ob, cudaMemcpyDeviceToHost, st));
+            CK(dev->pin_out.ensure(ob));
+            CK(cudaMemcpyAsync(dev->pin_out.p, L->out_stage.p, ob, cudaMemcpyDeviceToHost, st));
             stage_out = true;
         }
     }
@@ -1465,7 +1493,7 @@ int asnn_dev_activate(asnn_dev_layout* L, const float* x, uint32_t n_vec, uint64
                            cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(dev->ev1, st));
     CK(cudaEventSynchronize(dev->ev1));
-    if (stage_out) std::memcpy(out, L->pin_out.p, ob);
+    if (stage_out) std::memcpy(out, dev->pin_out.p, ob);
     cudaEventElapsedTime(&dev->timings.activate_ms, dev->ev0, dev->ev1);
     return ASNN_OK;
 }

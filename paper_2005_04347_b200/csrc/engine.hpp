@@ -12,15 +12,46 @@
 
 namespace asnn_b200 {
 
-// Owning device buffer (cudaMalloc / cudaFree).
+// Stream-ordered allocation: while an AllocStream guard is active on this
+// thread (every C-ABI entry point that allocates sets one to the handle's
+// stream), DevBuf allocates with cudaMallocAsync on that stream and frees with
+// cudaFreeAsync on the same stream -- after all work enqueued there that uses
+// the buffer, with no device-wide synchronisation and no unmapping (the pool
+// keeps its memory).  Work on other streams joins back before the free
+// (fork/join events); asnn_dev_free_layout synchronises the current stream
+// first.  Outside a guard: plain cudaMalloc / cudaFree.
+inline cudaStream_t& alloc_stream_slot() {
+    static thread_local cudaStream_t s = nullptr;
+    return s;
+}
+inline bool& alloc_stream_on() {
+    static thread_local bool on = false;
+    return on;
+}
+struct AllocStream {
+    cudaStream_t prev;
+    bool prev_on;
+    explicit AllocStream(cudaStream_t s) : prev(alloc_stream_slot()), prev_on(alloc_stream_on()) {
+        alloc_stream_slot() = s;
+        alloc_stream_on() = true;
+    }
+    ~AllocStream() {
+        alloc_stream_slot() = prev;
+        alloc_stream_on() = prev_on;
+    }
+};
+
+// Owning device buffer.
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    cudaStream_t s = nullptr;  // stream of a stream-ordered allocation
+    bool async = false;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), async(o.async) {
         o.p = nullptr;
         o.n = 0;
     }
@@ -29,6 +60,8 @@ struct DevBuf {
             reset();
             p = o.p;
             n = o.n;
+            s = o.s;
+            async = o.async;
             o.p = nullptr;
             o.n = 0;
         }
@@ -36,14 +69,25 @@ struct DevBuf {
     }
     ~DevBuf() { reset(); }
     void reset() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (async) cudaFreeAsync(p, s);
+            else cudaFree(p);
+        }
         p = nullptr;
         n = 0;
     }
     cudaError_t alloc(size_t count) {
         reset();
         if (count == 0) count = 1;
-        cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T));
+        cudaError_t e;
+        if (alloc_stream_on()) {
+            s = alloc_stream_slot();
+            async = true;
+            e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s);
+        } else {
+            async = false;
+            e = cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T));
+        }
         if (e == cudaSuccess) n = count;
         else p = nullptr;
         return e;
@@ -90,6 +134,7 @@ struct asnn_dev {
     uint32_t sweep_mode = 0;         // 0 auto, 1 per-layer launches, 2 K-cta when it fits
     uint32_t option_epoch = 0;       // bumps invalidate cached sweep graphs
     asnn_timings timings{};
+    asnn_b200::PinnedBuf pin_x, pin_out;  // pinned staging of pageable host buffers (all layouts)
 };
 
 namespace asnn_b200 {
@@ -117,8 +162,12 @@ struct NetMeta {
     std::vector<uint32_t> outputs;        // declared output ids
 };
 
-// Cached CUDA graph of one activation sweep.
+// Cached CUDA graph of one activation sweep.  The first activation with a
+// given (batch, buffers, stream, options) launches directly and only records
+// them; the graph is captured when they repeat, so one-shot layouts (the
+// per-call eval_parallel drop-in) never pay for capture + instantiation.
 struct SweepGraph {
+    bool seen = false;
     cudaGraphExec_t exec = nullptr;
     uint32_t n_vec = 0;
     const float* x = nullptr;
@@ -157,7 +206,6 @@ struct asnn_dev_layout {
     // activation workspace
     asnn_b200::DevBuf<float> A;
     asnn_b200::DevBuf<float> x_stage, out_stage;
-    asnn_b200::PinnedBuf pin_x, pin_out;
     asnn_b200::SweepGraph graph;
 
     // K-cta (whole sweep in one CTA per network x column slice)

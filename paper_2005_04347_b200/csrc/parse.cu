@@ -763,6 +763,7 @@ extern "C" {
 int asnn_dev_parse_network(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** out, uint32_t* err_line) {
     if (!dev || !out || (!text && len)) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
     const cudaError_t e = cudaSetDevice(dev->device);
     if (e != cudaSuccess) return asnn_b200::cuda_fail(dev, e, "cudaSetDevice");
     return asnn_b200::do_parse(dev, text, len, out, err_line);
@@ -773,6 +774,7 @@ int asnn_dev_parse_weights(asnn_dev* dev, const char* buf, const uint64_t* off, 
     using namespace asnn_b200;
     if (!dev || (n && (!buf || !off || !out || !status))) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
     if (!n) return ASNN_OK;
     CKP(cudaSetDevice(dev->device));
     cudaStream_t st = dev->stream;
@@ -806,6 +808,7 @@ int asnn_dev_parse_weights(asnn_dev* dev, const char* buf, const uint64_t* off, 
 int asnn_dev_read_network(asnn_dev* dev, const char* path, asnn_corpus** out, uint32_t* err_line) {
     if (!dev || !path || !out) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
     FILE* f = std::fopen(path, "rb");
     if (!f) {
         dev->err = std::string("cannot open ") + path;

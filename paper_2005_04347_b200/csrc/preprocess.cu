@@ -777,6 +777,7 @@ __global__ void k_count_unplaced(const uint32_t* __restrict__ level, uint32_t N,
 int build(asnn_dev* dev, uint32_t G, const asnn_network_desc* nets, asnn_dev_layout** out) {
     if (!dev || !nets || !out) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
     *out = nullptr;
     CK(cudaSetDevice(dev->device));
     dev->timings = asnn_timings{};
@@ -850,6 +851,7 @@ extern "C" {
 int asnn_dev_compute_required(asnn_dev* dev, const asnn_network_desc* net, uint8_t* required) {
     if (!dev || !net || (net->n_nodes && !required)) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
     CK(cudaSetDevice(dev->device));
     DevNet d;
     RC(preprocess(dev, 1, net, nullptr, d, false));
@@ -863,6 +865,7 @@ int asnn_dev_segment(asnn_dev* dev, const asnn_network_desc* net, const uint8_t*
                      uint32_t* n_layers) {
     if (!dev || !net || !n_layers || (net->n_nodes && !level)) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
     CK(cudaSetDevice(dev->device));
     DevNet d;
     RC(preprocess(dev, 1, net, required, d, true));

@@ -203,12 +203,23 @@ uint32_t padded_batch(uint32_t n_vec) {
 using LevelFn = void (*)(const uint32_t*, const uint2*, float*, uint32_t, const uint32_t*, uint32_t, uint32_t);
 using RowsFn = void (*)(const uint2*, float*, uint32_t, const uint4*, uint32_t, uint32_t, const uint4*, uint32_t,
                         float*);
+using WarpRowsFn = void (*)(const uint2*, float*, const uint4*, uint32_t);
 struct LevelLaunch {
     LevelFn lvl = nullptr;
     RowsFn rows = nullptr;
+    WarpRowsFn warp_rows = nullptr;  // batch 1: one warp per row
     uint32_t lanes = 1;
     uint32_t tiles = 1;
 };
+
+// Batch 1: a warp per row (k_warp_rows) unless ASNN_WARP_ROWS=0.
+bool warp_rows_enabled() {
+    static const bool on = [] {
+        const char* s = getenv("ASNN_WARP_ROWS");
+        return !(s && s[0] == '0');
+    }();
+    return on;
+}
 
 // ASNN_LEVEL_VARIANT (tuning experiments; profiles/r1_level_variants.txt,
 // profiles/r1_light_variants.txt): 5 = k_rows, 8 gathers in flight, 4
@@ -245,12 +256,13 @@ LevelLaunch wide_level(uint32_t tiles) {
 
 LevelLaunch level_launch_for(uint32_t ldA) {
     switch (ldA) {
-        case 1: return {k_level<1, 1>, nullptr, 1, 1};
-        case 2: return {k_level<2, 1>, nullptr, 1, 1};
-        case 4: return {k_level<4, 1>, nullptr, 1, 1};
-        case 8: return {k_level<4, 2>, nullptr, 2, 1};
-        case 16: return {k_level<4, 4>, nullptr, 4, 1};
-        case 32: return {k_level<4, 8>, nullptr, 8, 1};
+        case 1: return warp_rows_enabled() ? LevelLaunch{nullptr, nullptr, k_warp_rows, 32, 1}
+                                           : LevelLaunch{k_level<1, 1>, nullptr, nullptr, 1, 1};
+        case 2: return {k_level<2, 1>, nullptr, nullptr, 1, 1};
+        case 4: return {k_level<4, 1>, nullptr, nullptr, 1, 1};
+        case 8: return {k_level<4, 2>, nullptr, nullptr, 2, 1};
+        case 16: return {k_level<4, 4>, nullptr, nullptr, 4, 1};
+        case 32: return {k_level<4, 8>, nullptr, nullptr, 8, 1};
         case 64: return wide_level<16>(1);
         default: return wide_level<32>(ldA / 128);
     }
@@ -418,7 +430,18 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     }
     const bool latency_bound = L->nets.size() > 1 || L->n_levels >= 24 ||
                                L->total_edges * static_cast<uint64_t>(ldA) <= (1ull << 22);
-    p.use = mode == 2 || latency_bound;
+    // ... unless a few CTAs would carry a big network alone.  Batch-1
+    // measurements (tools/level_probe.py, reference bench corpus): one CTA
+    // costs ~1.2 us per layer plus ~0.9 ns per edge-column, a per-level launch
+    // over the whole GPU ~7 us per level (57k edges / 10 layers: 54 vs 76 us;
+    // 110k edges: 152 vs 75 us).
+    const uint64_t ctas = static_cast<uint64_t>(ldA / p.C) * L->nets.size();
+    const uint64_t per_wave = static_cast<uint64_t>(L->dev->sm_count) *
+                              std::max<uint64_t>(1, (228ull * 1024) / (p.smem + 1024));
+    const double cta_us = (1.2 * L->n_levels + static_cast<double>(L->total_edges) / L->nets.size() * p.C / 1100.0) *
+                          static_cast<double>((ctas + per_wave - 1) / per_wave);
+    const double level_us = 7.0 * L->n_levels;
+    p.use = mode == 2 || (latency_bound && (L->nets.size() > 1 || cta_us <= level_us));
     return p;
 }
 
@@ -863,7 +886,10 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
         const uint32_t nrows = n - nh;
         if (nrows || ns) {
             const uint64_t items = static_cast<uint64_t>(nrows + ns) * ll.tiles;
-            if (ll.rows)
+            if (ll.warp_rows)
+                ll.warp_rows<<<blocks_for(static_cast<uint64_t>(nrows) * 32), kThreads, 0, st>>>(
+                    L->edges.p, L->A.p, L->rtask.p + L->lvl_off[l] + nh, nrows);
+            else if (ll.rows)
                 ll.rows<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(
                     L->edges.p, L->A.p, ldA, L->rtask.p + L->lvl_off[l] + nh, nrows, ll.tiles,
                     segs ? L->seg.p + L->seg_short_off[l] : nullptr, ns, L->accbuf.p);

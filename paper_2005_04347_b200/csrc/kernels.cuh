@@ -214,6 +214,45 @@ k_rows(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ldA,
 }
 
 // ---------------------------------------------------------------------------
+// K-warp-rows: one warp per row for a single input vector (batch 1, the
+// reference's eval_parallel call).  The 32 lanes load 32 consecutive edges
+// and their source activations at once (32 gathers in flight per row instead
+// of one thread's 8), form the products w * x in parallel (each an IEEE fp32
+// multiply, exactly as in the sequential loop), and the warp then adds them
+// in stored order through __shfl -- the reference's sequence of fp32 adds,
+// now 4 cycles per edge behind one memory round trip per 32 edges; the next
+// 32 edges' loads are issued before the current ones are summed.  Items are
+// rtask records ({row, first edge, end edge, 0}) in schedule order.
+__global__ void __launch_bounds__(256)
+k_warp_rows(const uint2* __restrict__ edges, float* __restrict__ A, const uint4* __restrict__ rows,
+            uint32_t n_rows) {
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (wid >= n_rows) return;  // warp-uniform
+    const uint4 t = __ldg(&rows[wid]);
+    const uint32_t beg = t.y, end = t.z;
+    auto product = [&](uint32_t k) -> float {
+        if (k >= end) return 0.0f;
+        const uint2 e = __ldg(&edges[k]);
+        return __fmul_rn(__uint_as_float(e.y), __ldg(&A[e.x]));
+    };
+    float acc = 0.0f;
+    float p = product(beg + lane);
+    for (uint32_t base = beg; base < end; base += 32) {
+        const float pn = product(base + 32 + lane);  // next chunk in flight
+        const uint32_t n = min(32u, end - base);
+        if (n == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc = __fadd_rn(acc, __shfl_sync(0xFFFFFFFFu, p, j));
+        } else {
+            for (uint32_t j = 0; j < n; ++j) acc = __fadd_rn(acc, __shfl_sync(0xFFFFFFFFu, p, j));
+        }
+        p = pn;
+    }
+    if (lane == 0) A[t.x] = sigmoid32(acc);
+}
+
+// ---------------------------------------------------------------------------
 // K-act-heavy: one CTA per (high in-degree node, column tile).  The serial
 // fp32 sum of a node cannot be split without changing its rounding, so the
 // row is streamed instead: two producer warps copy predecessor rows with

@@ -270,7 +270,9 @@ def run_ours(args, cfg):
         # batch sharding: a full layout replica, a contiguous slice of the vectors
         shard = nets
         X_full = rng.uniform(-2, 2, (B_total, len(nets[0].inputs))).astype(np.float32)
-        lo, hi = batch_slice(B_total, world, rank)
+        # --shard-of G (development): one process measuring rank 0's slice of a
+        # G-way split, i.e. the per-GPU workload of a G-GPU run
+        lo, hi = batch_slice(B_total, args.shard_of or world, rank)
         Xs = [X_full[lo:hi]]
         X = [X_full]
         B = hi - lo
@@ -442,7 +444,7 @@ def run_ncu_sweeps(args, cfg):
     import torch
     import paper_2005_04347_b200 as A
     nets = make_network(cfg, args.scale)
-    B = CONFIGS[cfg][1]
+    B = CONFIGS[cfg][1] // max(1, args.shard_of) if cfg != "c5" else CONFIGS[cfg][1]
     rng = np.random.default_rng(12345)
     X = np.concatenate([rng.uniform(-2, 2, (B, len(n.inputs))).astype(np.float32).reshape(-1)
                         for n in nets])
@@ -465,6 +467,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=float, default=1.0, help="shrink c4/c5 for quick runs")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="development: run rank 0's batch slice of a G-GPU split on this one GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prep", default="device", choices=["device", "upload"],
                     help="device: compute_required/segment/flatten on the GPU; upload: "

@@ -204,10 +204,12 @@ using LevelFn = void (*)(const uint32_t*, const uint2*, float*, uint32_t, const 
 using RowsFn = void (*)(const uint2*, float*, uint32_t, const uint4*, uint32_t, uint32_t, const uint4*, uint32_t,
                         float*);
 using WarpRowsFn = void (*)(const uint2*, float*, const uint4*, uint32_t);
+using WarpRows4Fn = void (*)(const uint2*, float*, uint32_t, const uint4*, uint32_t, const uint4*, uint32_t, float*);
 struct LevelLaunch {
     LevelFn lvl = nullptr;
     RowsFn rows = nullptr;
-    WarpRowsFn warp_rows = nullptr;  // batch 1: one warp per row
+    WarpRowsFn warp_rows = nullptr;    // batch 1: one warp per row
+    WarpRows4Fn warp_rows4 = nullptr;  // batch 4..32: one warp per row (and segment)
     uint32_t lanes = 1;
     uint32_t tiles = 1;
 };
@@ -254,15 +256,42 @@ LevelLaunch wide_level(uint32_t tiles) {
     return l;
 }
 
+// Batches of 4..32 columns (the per-GPU slice of a batch sharded over many
+// GPUs): k_rows with 16 gathers in flight per lane at 2 blocks/SM -- narrow
+// rows need more memory-level parallelism per row.  Config 4's 16- / 8-column
+// shards: 9.6 / 9.4 ms, against 12.7 / 11.6 ms with 8 in flight and 13.0 ms
+// (8 columns) for one warp per row (k_warp_rows4, ASNN_NARROW_WARP=1).
+// ASNN_LEVEL_VARIANT overrides as for wide batches.
+template <int LANES>
+LevelLaunch narrow_level() {
+    static const bool warp = [] {
+        const char* s = getenv("ASNN_NARROW_WARP");
+        return s && s[0] == '1';
+    }();
+    if (!warp) {
+        if (getenv("ASNN_LEVEL_VARIANT")) return wide_level<LANES>(1);
+        LevelLaunch l;
+        l.rows = k_rows<LANES, 16, 2>;
+        l.lanes = LANES;
+        l.tiles = 1;
+        return l;
+    }
+    LevelLaunch l;
+    l.warp_rows4 = k_warp_rows4<LANES>;
+    l.lanes = 32;
+    l.tiles = 1;
+    return l;
+}
+
 LevelLaunch level_launch_for(uint32_t ldA) {
     switch (ldA) {
-        case 1: return warp_rows_enabled() ? LevelLaunch{nullptr, nullptr, k_warp_rows, 32, 1}
-                                           : LevelLaunch{k_level<1, 1>, nullptr, nullptr, 1, 1};
-        case 2: return {k_level<2, 1>, nullptr, nullptr, 1, 1};
-        case 4: return {k_level<4, 1>, nullptr, nullptr, 1, 1};
-        case 8: return {k_level<4, 2>, nullptr, nullptr, 2, 1};
-        case 16: return {k_level<4, 4>, nullptr, nullptr, 4, 1};
-        case 32: return {k_level<4, 8>, nullptr, nullptr, 8, 1};
+        case 1: return warp_rows_enabled() ? LevelLaunch{nullptr, nullptr, k_warp_rows, nullptr, 32, 1}
+                                           : LevelLaunch{k_level<1, 1>, nullptr, nullptr, nullptr, 1, 1};
+        case 2: return {k_level<2, 1>, nullptr, nullptr, nullptr, 1, 1};
+        case 4: return narrow_level<1>();
+        case 8: return narrow_level<2>();
+        case 16: return narrow_level<4>();
+        case 32: return narrow_level<8>();
         case 64: return wide_level<16>(1);
         default: return wide_level<32>(ldA / 128);
     }
@@ -676,7 +705,8 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 // and not disabled (ASNN_SEGMENTS=0).
 bool seg_eligible(const asnn_dev_layout* L, uint32_t ldA) {
     static const bool enabled = env_u32("ASNN_SEGMENTS", 1) != 0;
-    return enabled && L->nets.size() == 1 && L->dev->sweep_mode != 3 && level_launch_for(ldA).rows &&
+    const LevelLaunch ll = level_launch_for(ldA);
+    return enabled && L->nets.size() == 1 && L->dev->sweep_mode != 3 && (ll.rows || ll.warp_rows4) &&
            heavy_launch_for(ldA).fn && heavy_index_for(L->dev->heavy_threshold) >= 0 &&
            L->total_pos > L->total_sensors;
 }
@@ -889,6 +919,10 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
             if (ll.warp_rows)
                 ll.warp_rows<<<blocks_for(static_cast<uint64_t>(nrows) * 32), kThreads, 0, st>>>(
                     L->edges.p, L->A.p, L->rtask.p + L->lvl_off[l] + nh, nrows);
+            else if (ll.warp_rows4)
+                ll.warp_rows4<<<blocks_for(static_cast<uint64_t>(nrows + ns) * 32), kThreads, 0, st>>>(
+                    L->edges.p, L->A.p, ldA, L->rtask.p + L->lvl_off[l] + nh, nrows,
+                    segs ? L->seg.p + L->seg_short_off[l] : nullptr, ns, L->accbuf.p);
             else if (ll.rows)
                 ll.rows<<<blocks_for(items * ll.lanes), kThreads, 0, st>>>(
                     L->edges.p, L->A.p, ldA, L->rtask.p + L->lvl_off[l] + nh, nrows, ll.tiles,

@@ -253,6 +253,78 @@ k_warp_rows(const uint2* __restrict__ edges, float* __restrict__ A, const uint4*
 }
 
 // ---------------------------------------------------------------------------
+// K-warp-rows4: one warp per item for narrow batches (ldA = 4 * LANES = 4 ..
+// 32 columns: the per-GPU slice of a batch sharded over many GPUs).  The warp
+// is LANES column quads x P = 32 / LANES edge phases: lane (phase p, quad c)
+// loads edge k + p, gathers its 16-byte quad of the source row and forms the
+// four IEEE products; the row's sums then run in stored order over the
+// phases through __shfl (every lane of quad c keeps the same running sums).
+// P gathers per row are in flight instead of 8, and one row per warp gives
+// many waves per level where row-per-group kernels would leave a partial
+// second wave.  Items: the first n_seg are row segments (common.cuh), then
+// rows (rtask records).
+template <int LANES>
+__global__ void __launch_bounds__(256)
+k_warp_rows4(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ldA, const uint4* __restrict__ rows,
+             uint32_t n_rows, const uint4* __restrict__ seg, uint32_t n_seg, float* __restrict__ accbuf) {
+    static_assert(LANES >= 1 && LANES <= 8 && (LANES & (LANES - 1)) == 0, "1..8 column quads");
+    constexpr uint32_t P = 32 / LANES;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= n_seg + n_rows) return;  // warp-uniform
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t c = lane % LANES, ph = lane / LANES;
+    const uint4 t = wid < n_seg ? __ldg(&seg[wid]) : __ldg(&rows[wid - n_seg]);
+    const uint32_t beg = t.y, end = t.z, aux = t.w;
+    const uint32_t col = c * 4;
+    const uint32_t stride = ldA * 4u;
+    const char* __restrict__ Acol = reinterpret_cast<const char*>(A + col);
+    auto load = [&](uint32_t k, float (&pr)[4]) {
+        if (k < end) {
+            const uint2 e = __ldg(&edges[k]);
+            const float w = __uint_as_float(e.y);
+            const float4 v = __ldg(reinterpret_cast<const float4*>(Acol + static_cast<uint64_t>(e.x) * stride));
+            pr[0] = __fmul_rn(w, v.x);
+            pr[1] = __fmul_rn(w, v.y);
+            pr[2] = __fmul_rn(w, v.z);
+            pr[3] = __fmul_rn(w, v.w);
+        } else {
+            pr[0] = pr[1] = pr[2] = pr[3] = 0.0f;
+        }
+    };
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (aux & kAccLoad) {
+        const float4 p = *reinterpret_cast<const float4*>(accbuf + static_cast<uint64_t>(aux & kSlotMask) * ldA + col);
+        acc[0] = p.x, acc[1] = p.y, acc[2] = p.z, acc[3] = p.w;
+    }
+    float cur[4], nxt[4];
+    load(beg + ph, cur);
+    for (uint32_t base = beg; base < end; base += P) {
+        load(base + P + ph, nxt);  // the next P edges in flight
+        const uint32_t n = min(P, end - base);
+        if (n == P) {
+#pragma unroll
+            for (uint32_t j = 0; j < P; ++j)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = __fadd_rn(acc[q], __shfl_sync(0xFFFFFFFFu, cur[q], j * LANES + c));
+        } else {
+            for (uint32_t j = 0; j < n; ++j)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = __fadd_rn(acc[q], __shfl_sync(0xFFFFFFFFu, cur[q], j * LANES + c));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+    }
+    if (ph != 0) return;
+    if (aux & kAccStore) {
+        *reinterpret_cast<float4*>(accbuf + static_cast<uint64_t>(aux & kSlotMask) * ldA + col) =
+            make_float4(acc[0], acc[1], acc[2], acc[3]);
+    } else {
+        *reinterpret_cast<float4*>(A + static_cast<uint64_t>(t.x) * ldA + col) =
+            make_float4(sigmoid32(acc[0]), sigmoid32(acc[1]), sigmoid32(acc[2]), sigmoid32(acc[3]));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K-act-heavy: one CTA per (high in-degree node, column tile).  The serial
 // fp32 sum of a node cannot be split without changing its rounding, so the
 // row is streamed instead: two producer warps copy predecessor rows with

@@ -43,7 +43,7 @@ def check_bitwise(oracle, net, B, thr, seg_min, seg_long, seed=0):
     dl.free()
 
 
-@pytest.mark.parametrize("B", [64, 128, 256])
+@pytest.mark.parametrize("B", [8, 16, 32, 64, 128, 256])
 @pytest.mark.parametrize("thr,seg_min,seg_long", [(16, 1, 512), (16, 8, 32), (64, 64, 512), (32, 4, 16)])
 def test_banded_powerlaw_segments(oracle, B, thr, seg_min, seg_long):
     """Banded power-law DAG (config 4's shape, small): ids ascend with the

@@ -79,6 +79,8 @@ __device__ __forceinline__ float sigmoid32_path(float x, bool& exact) {
     const double d = __dadd_rn(1.0, __fma_rn(scale, tmp, scale));
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    // two Newton steps: one leaves too few bits for the rounding test (a
+    // one-step / one-constant-reduction variant failed the exhaustive check)
     y = __fma_rn(y, __fma_rn(-d, y, 1.0), y);
     y = __fma_rn(y, __fma_rn(-d, y, 1.0), y);
     // y in (2^-125, 1]: distance of its low 29 mantissa bits from the float

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <charconv>
 #include <cstdio>
 #include <cstring>
@@ -442,8 +443,24 @@ int flagged_indices(asnn_dev* dev, const uint32_t* f, uint64_t n, std::vector<ui
     return ASNN_OK;
 }
 
+// ASNN_PARSE_TIMING=1: phase wall times (synchronising) on stderr.
+struct PhaseClock {
+    bool on;
+    cudaStream_t st;
+    std::chrono::steady_clock::time_point t;
+    explicit PhaseClock(cudaStream_t s) : on(getenv("ASNN_PARSE_TIMING") != nullptr), st(s), t(std::chrono::steady_clock::now()) {}
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "parse %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
 int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result, uint32_t* err_line) {
     cudaStream_t st = dev->stream;
+    PhaseClock clk(st);
     *result = nullptr;
     if (err_line) *err_line = 0;
     asnn_timings& tm = dev->timings;
@@ -469,6 +486,7 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result
     CKP(cudaMemcpyAsync(starts.p, &h_first, 8, cudaMemcpyHostToDevice, st));
     CKP(cudaMemcpyAsync(starts.p + n_lines, &h_last, 8, cudaMemcpyHostToDevice, st));
     if (n_chunks) k_nl_write<<<nb(n_chunks), kT, 0, st>>>(d_text.p, len, coff.p, starts.p);
+    clk.mark("text+line starts");
     // ---- 2. lines
     DevBuf<uint8_t> kind, estat, hdr;
     DevBuf<uint32_t> lsrc, ltgt, sigf, sig, keep, kidx;
@@ -482,6 +500,7 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result
     k_parse_lines<<<nb(n_lines), kT, 0, st>>>(d_text.p, starts.p, n_lines,
                                                LineOut{kind.p, estat.p, hdr.p, lsrc.p, ltgt.p, lw.p});
     CKP(cudaGetLastError());
+    clk.mark("line parse");
     // ---- 3-4. sections and per-line errors
     CKP(sigf.alloc(n_lines));
     CKP(sig.alloc(n_lines));
@@ -537,6 +556,7 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result
         k_dup_edges<<<nb(E), kT, 0, st>>>(vs2, E, es.p, et.p, eline.p, ferr.p);
         CKP(cudaGetLastError());
     }
+    clk.mark("sections+dups");
     // ---- 5. inputs / outputs ids
     std::vector<uint64_t> h_starts_sp(6, 0);
     DevBuf<uint32_t> ids[2];
@@ -572,6 +592,7 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result
         CKP(cudaStreamSynchronize(st));
         if (hb != 0xFFFFFFFFu) h_bad_tok[k] = hb;
     }
+    clk.mark("ids");
     // ---- host side of the error decision
     unsigned long long h_ferr = 0;
     CKP(cudaMemcpyAsync(&h_ferr, ferr.p, 8, cudaMemcpyDeviceToHost, st));
@@ -632,6 +653,7 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result
         return ASNN_E_PARSE;
     }
     for (const auto& pv : patches) CKP(cudaMemcpyAsync(ew.p + pv.first, &pv.second, 4, cudaMemcpyHostToDevice, st));
+    clk.mark("errors");
     // ---- 6. make_network (network.cpp:39-55): nodes = sorted unique ids
     const uint64_t n_all = n_ids[0] + n_ids[1] + 2 * E;
     DevBuf<uint32_t> all, nodes;
@@ -662,6 +684,7 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result
         k_scatter_flagged<<<nb(n_all), kT, 0, st>>>(ks, f.p, idx.p, n_all, nodes.p);
         CKP(cudaGetLastError());
     }
+    clk.mark("make_network");
     // ---- validate (network.cpp:151-216)
     std::vector<std::string> viol;
     if (!n_ids[0]) viol.push_back("inputs list is empty");
@@ -724,7 +747,9 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result
         }
     }
     bool cyclic = false;
+    clk.mark("validate lists");
     if (E) RCP(device_cycle_check(dev, nodes.p, N, es.p, et.p, E, &cyclic));
+    clk.mark("cycle check");
     auto* c = new asnn_corpus;
     int rc = d2h(dev, c->nodes, nodes.p, N);
     if (!rc) rc = d2h(dev, c->inputs, ids[0].p, n_ids[0]);
@@ -743,6 +768,7 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result
         return cuda_fail(dev, ce, "parse");
     }
     cudaEventElapsedTime(&tm.upload_ms, dev->ev0, dev->ev1);
+    clk.mark("download");
     if (cyclic) viol.push_back(cycle_message(c->nodes, c->src, c->dst));
     if (!viol.empty()) {
         delete c;

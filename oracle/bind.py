@@ -203,6 +203,7 @@ class Ref:
                                C.c_char_p, C.c_uint64]),
             "ref_serialize": (C.c_uint64, [vp, C.c_char_p, C.c_uint64]),
             "ref_from_chars_f32": (None, [C.c_char_p, u64p, C.c_uint64, f32p, u8p]),
+            "ref_format_double": (None, [C.c_double, C.c_char_p, C.c_uint64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -240,6 +241,11 @@ class Ref:
         self.L.ref_from_chars_f32(buf, _p(off, C.c_uint64), len(enc), _p(out, C.c_float),
                                   _p(st, C.c_uint8))
         return out, st
+
+    def format_double(self, v: float) -> str:
+        buf = C.create_string_buffer(64)
+        self.L.ref_format_double(float(v), buf, 64)
+        return buf.value.decode()
 
     # networks ---------------------------------------------------------------
     def generate(self, spec):

@@ -418,6 +418,13 @@ void ref_from_chars_f32(const char* buf, const std::uint64_t* off, std::uint64_t
     }
 }
 
+// asnn::format_double (io.cpp:19-23) into out (cap bytes, NUL-terminated).
+void ref_format_double(double v, char* out, std::uint64_t cap) {
+    const std::string t = asnn::format_double(v);
+    std::strncpy(out, t.c_str(), cap - 1);
+    out[cap - 1] = 0;
+}
+
 void ref_sigmoid32_many(const float* in, float* out, std::uint64_t n) {
 #pragma omp parallel for schedule(static)
     for (std::int64_t i = 0; i < static_cast<std::int64_t>(n); ++i) out[i] = asnn::sigmoid32(in[i]);

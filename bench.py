@@ -174,7 +174,10 @@ class RefCPU:
         self.kind = "reference" if available_ref() else "port"
         self.ref = Ref() if self.kind == "reference" else None
         self.oracle = None if self.ref else Oracle()
-        self.threads = self.ref.L.ref_max_threads() if self.ref else 1
+        # all host threads: torchrun exports OMP_NUM_THREADS=1 to every rank, so
+        # ask the OS (affinity) rather than OpenMP's default
+        host = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        self.threads = max(self.ref.L.ref_max_threads(), host or 1) if self.ref else 1
         self.items = []
         for gi, net in enumerate(nets[:max_nets]):
             if cfg in ("c2", "c4"):

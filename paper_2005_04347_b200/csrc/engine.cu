@@ -2,6 +2,7 @@
 // the C-ABI entry points of include/asnn_dev.h (except preprocessing, which
 // lives in preprocess.cu and corpora in netgen.cpp).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -307,11 +308,15 @@ struct HeavyLaunch {
 template <int TC>
 HeavyLaunch heavy_launch() {
     const uint32_t smem = heavy::kStages * heavy::kRows * (TC + 1) * 4 + 2 * heavy::kStages * 8;
-    static bool configured = false;
-    if (!configured) {
+    // the attribute is per device: remember which ordinals are configured
+    static std::atomic<uint64_t> configured{0};
+    int device = 0;
+    cudaGetDevice(&device);
+    const uint64_t bit = 1ull << (device & 63);
+    if (!(configured.load() & bit)) {
         cudaFuncSetAttribute(k_heavy<TC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        configured = true;
+        configured.fetch_or(bit);
     }
     return {k_heavy<TC>, 32u * heavy::kProducers + (TC < 32 ? 32u : static_cast<uint32_t>(TC)), smem, 1};
 }

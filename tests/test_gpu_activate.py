@@ -233,3 +233,28 @@ def test_heavy_rows_bitwise(oracle, B, thr):
     stats = {}
     check_close(st_heavy, oracle.eval_batch(d, X), stats)
     assert stats["eq"] == stats["n"], stats          # bitwise
+
+
+# --- hand-built layouts whose rows read ids without a position --------------------------
+@pytest.mark.parametrize("B", [1, 4, 64, 256])
+def test_predecessors_without_position(oracle, B, sweep_mode):
+    """A LayeredLayout may list predecessors that have no position (pruned
+    ids): eval_sequential reads their zero-initialised op slots
+    (eval.cpp:20-21, make_state eval.cpp:25-35).  Every strategy must read
+    0.0f for them (the never-written zero row) -- including K-cta's pipelined
+    consumers, whose split treats such sources as layer 0."""
+    rng = A.SplitMix64(404)
+    net = A.generate(A.random_spec(rng, 500, 4000))
+    dead = int(net.nodes.max()) + 7                       # a pruned node: never reaches an output
+    net = A.Network(np.append(net.nodes, dead), net.inputs, net.outputs,
+                    np.append(net.source, net.inputs[0]), np.append(net.target, dead),
+                    np.append(net.weight, np.float32(0.5)))
+    d = oracle.layout(net)
+    assert dead not in set(d["node_ids"].tolist()) and d["id_bound"] > dead
+    w = np.random.default_rng(B).random(len(d["in_nodes"]))
+    d["in_nodes"] = d["in_nodes"].copy()
+    d["in_nodes"][w < 0.05] = dead                        # 5% of the reads hit the zero slot
+    X = np.random.default_rng(5).uniform(-2, 2, (B, len(d["input_order"]))).astype(np.float32)
+    dl = A.DeviceLayout.from_layout(to_layout(d, net.outputs))
+    _, st = dl.activate(X, outputs=True, state=True)
+    assert bitwise_equal(st, oracle.eval_batch(d, X))

@@ -242,6 +242,12 @@ typedef struct asnn_corpus asnn_corpus;
  * ValidationError message ("invalid network\n  ..."). */
 int asnn_dev_parse_network(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** out,
                            uint32_t* err_line);
+/* load -> levels on the device: parse_network + validate + compute_required +
+ * segment + flatten, the parsed arrays never leaving HBM; *out is a resident
+ * layout (asnn_dev_activate*).  Errors as asnn_dev_parse_network, then as
+ * asnn_dev_build_layout. */
+int asnn_dev_load_layout(asnn_dev* dev, const char* text, uint64_t len, asnn_dev_layout** out,
+                         uint32_t* err_line);
 /* read_network (io.cpp:167-173): ASNN_E_IO when the file cannot be read. */
 int asnn_dev_read_network(asnn_dev* dev, const char* path, asnn_corpus** out, uint32_t* err_line);
 /* parse_weight's from_chars<float> on n tokens buf[off[i], off[i+1]) on the

@@ -402,6 +402,21 @@ class DeviceLayout:
         return cls(dev, h)
 
     @classmethod
+    def from_text(cls, text, device: int = 0) -> "DeviceLayout":
+        """load -> levels entirely on the GPU: parse_network + validate +
+        compute_required + segment + flatten of an `asnn 1` text."""
+        if isinstance(text, str):
+            text = text.encode()
+        dev = Device.get(device)
+        h = C.c_void_p()
+        line = C.c_uint32(0)
+        rc = dev.lib.asnn_dev_load_layout(dev.h, text, len(text), C.byref(h), C.byref(line))
+        if rc == _lib.ASNN_E_PARSE:
+            raise ParseError(dev.lib.asnn_dev_last_error(dev.h).decode(), line.value)
+        dev.check(rc)
+        return cls(dev, h)
+
+    @classmethod
     def from_population(cls, nets: Sequence[Network], device: int = 0) -> "DeviceLayout":
         dev = Device.get(device)
         descs = (_lib.NetworkDesc * len(nets))(*[n.desc() for n in nets])

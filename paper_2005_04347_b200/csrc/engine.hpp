@@ -253,6 +253,12 @@ struct FlatDevice {
 int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& flat,
                     asnn_dev_layout** out);
 
+// compute_required + segment + flatten for one network already on the device
+// (preprocess.cu; the loader's output).  Takes ownership of the arrays.
+int build_device_network(asnn_dev* dev, DevBuf<uint32_t>&& nodes, uint32_t N, DevBuf<uint32_t>&& src,
+                         DevBuf<uint32_t>&& dst, DevBuf<float>&& w, uint64_t E, std::vector<uint32_t>&& inputs,
+                         std::vector<uint32_t>&& outputs, asnn_dev_layout** out);
+
 // validate's cycle test on device arrays (preprocess.cu): nodes sorted unique,
 // connections as (src, dst) ids.
 int device_cycle_check(asnn_dev* dev, const uint32_t* nodes, uint32_t N, const uint32_t* src, const uint32_t* dst,

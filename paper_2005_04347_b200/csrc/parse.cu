@@ -458,10 +458,17 @@ struct PhaseClock {
     }
 };
 
-int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result, uint32_t* err_line) {
+// A parsed, validated network resident on the device.
+struct Parsed {
+    DevBuf<uint32_t> nodes, inputs, outputs, src, dst;
+    DevBuf<float> w;
+    uint32_t N = 0, n_in = 0, n_out = 0;
+    uint64_t E = 0;
+};
+
+int do_parse(asnn_dev* dev, const char* text, uint64_t len, Parsed& res, uint32_t* err_line) {
     cudaStream_t st = dev->stream;
     PhaseClock clk(st);
-    *result = nullptr;
     if (err_line) *err_line = 0;
     asnn_timings& tm = dev->timings;
     cudaEventRecord(dev->ev0, st);
@@ -750,34 +757,74 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result
     clk.mark("validate lists");
     if (E) RCP(device_cycle_check(dev, nodes.p, N, es.p, et.p, E, &cyclic));
     clk.mark("cycle check");
-    auto* c = new asnn_corpus;
-    int rc = d2h(dev, c->nodes, nodes.p, N);
-    if (!rc) rc = d2h(dev, c->inputs, ids[0].p, n_ids[0]);
-    if (!rc) rc = d2h(dev, c->outputs, ids[1].p, n_ids[1]);
-    if (!rc) rc = d2h(dev, c->src, es.p, E);
-    if (!rc) rc = d2h(dev, c->dst, et.p, E);
-    if (!rc) rc = d2h(dev, c->w, ew.p, E);
-    if (rc) {
-        delete c;
-        return rc;
+    if (cyclic) {  // the reference's DFS names the cycle (host copies, error path only)
+        std::vector<uint32_t> hn, hs, ht;
+        RCP(d2h(dev, hn, nodes.p, N));
+        RCP(d2h(dev, hs, es.p, E));
+        RCP(d2h(dev, ht, et.p, E));
+        CKP(cudaStreamSynchronize(st));
+        viol.push_back(cycle_message(hn, hs, ht));
     }
     cudaEventRecord(dev->ev1, st);
-    const cudaError_t ce = cudaStreamSynchronize(st);
-    if (ce != cudaSuccess) {
-        delete c;
-        return cuda_fail(dev, ce, "parse");
-    }
+    CKP(cudaStreamSynchronize(st));
     cudaEventElapsedTime(&tm.upload_ms, dev->ev0, dev->ev1);
-    clk.mark("download");
-    if (cyclic) viol.push_back(cycle_message(c->nodes, c->src, c->dst));
     if (!viol.empty()) {
-        delete c;
         std::string m = "invalid network";
         for (const auto& v : viol) m += "\n  " + v;
         dev->err = m;
         return ASNN_E_VALIDATION;
     }
+    res.nodes = std::move(nodes);
+    res.inputs = std::move(ids[0]);
+    res.outputs = std::move(ids[1]);
+    res.src = std::move(es);
+    res.dst = std::move(et);
+    res.w = std::move(ew);
+    res.N = N;
+    res.n_in = n_ids[0];
+    res.n_out = n_ids[1];
+    res.E = E;
+    return ASNN_OK;
+}
+
+int parse_to_corpus(asnn_dev* dev, const char* text, uint64_t len, asnn_corpus** result, uint32_t* err_line) {
+    *result = nullptr;
+    Parsed p;
+    RCP(do_parse(dev, text, len, p, err_line));
+    PhaseClock clk(dev->stream);
+    auto* c = new asnn_corpus;
+    int rc = d2h(dev, c->nodes, p.nodes.p, p.N);
+    if (!rc) rc = d2h(dev, c->inputs, p.inputs.p, p.n_in);
+    if (!rc) rc = d2h(dev, c->outputs, p.outputs.p, p.n_out);
+    if (!rc) rc = d2h(dev, c->src, p.src.p, p.E);
+    if (!rc) rc = d2h(dev, c->dst, p.dst.p, p.E);
+    if (!rc) rc = d2h(dev, c->w, p.w.p, p.E);
+    const cudaError_t ce = cudaStreamSynchronize(dev->stream);
+    if (!rc && ce != cudaSuccess) rc = cuda_fail(dev, ce, "parse download");
+    if (rc) {
+        delete c;
+        return rc;
+    }
+    clk.mark("download");
     *result = c;
+    return ASNN_OK;
+}
+
+int read_file(asnn_dev* dev, const char* path, std::vector<char>& buf) {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) {
+        dev->err = std::string("cannot open ") + path;
+        return ASNN_E_IO;
+    }
+    char tmp[1 << 16];
+    size_t n;
+    while ((n = std::fread(tmp, 1, sizeof(tmp), f)) > 0) buf.insert(buf.end(), tmp, tmp + n);
+    const bool bad = std::ferror(f) != 0;
+    std::fclose(f);
+    if (bad) {
+        dev->err = std::string("failed reading ") + path;
+        return ASNN_E_IO;
+    }
     return ASNN_OK;
 }
 
@@ -792,7 +839,29 @@ int asnn_dev_parse_network(asnn_dev* dev, const char* text, uint64_t len, asnn_c
     asnn_b200::AllocStream alloc_on(dev->stream);
     const cudaError_t e = cudaSetDevice(dev->device);
     if (e != cudaSuccess) return asnn_b200::cuda_fail(dev, e, "cudaSetDevice");
-    return asnn_b200::do_parse(dev, text, len, out, err_line);
+    return asnn_b200::parse_to_corpus(dev, text, len, out, err_line);
+}
+
+// load -> levels: the parsed arrays stay on the device and go straight into
+// compute_required / segment / flatten (no host round trip).
+int asnn_dev_load_layout(asnn_dev* dev, const char* text, uint64_t len, asnn_dev_layout** out, uint32_t* err_line) {
+    if (!dev || !out || (!text && len)) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
+    *out = nullptr;
+    const cudaError_t e = cudaSetDevice(dev->device);
+    if (e != cudaSuccess) return asnn_b200::cuda_fail(dev, e, "cudaSetDevice");
+    asnn_b200::Parsed p;
+    int rc = asnn_b200::do_parse(dev, text, len, p, err_line);
+    if (rc) return rc;
+    std::vector<uint32_t> ins, outs;
+    rc = asnn_b200::d2h(dev, ins, p.inputs.p, p.n_in);
+    if (!rc) rc = asnn_b200::d2h(dev, outs, p.outputs.p, p.n_out);
+    if (rc) return rc;
+    const cudaError_t ce = cudaStreamSynchronize(dev->stream);
+    if (ce != cudaSuccess) return asnn_b200::cuda_fail(dev, ce, "load");
+    return asnn_b200::build_device_network(dev, std::move(p.nodes), p.N, std::move(p.src), std::move(p.dst),
+                                           std::move(p.w), p.E, std::move(ins), std::move(outs), out);
 }
 
 int asnn_dev_parse_weights(asnn_dev* dev, const char* buf, const uint64_t* off, uint64_t n, float* out,
@@ -835,24 +904,12 @@ int asnn_dev_read_network(asnn_dev* dev, const char* path, asnn_corpus** out, ui
     if (!dev || !path || !out) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
     asnn_b200::AllocStream alloc_on(dev->stream);
-    FILE* f = std::fopen(path, "rb");
-    if (!f) {
-        dev->err = std::string("cannot open ") + path;
-        return ASNN_E_IO;
-    }
     std::vector<char> buf;
-    char tmp[1 << 16];
-    size_t n;
-    while ((n = std::fread(tmp, 1, sizeof(tmp), f)) > 0) buf.insert(buf.end(), tmp, tmp + n);
-    const bool bad = std::ferror(f) != 0;
-    std::fclose(f);
-    if (bad) {
-        dev->err = std::string("failed reading ") + path;
-        return ASNN_E_IO;
-    }
+    const int rc = asnn_b200::read_file(dev, path, buf);
+    if (rc) return rc;
     const cudaError_t e = cudaSetDevice(dev->device);
     if (e != cudaSuccess) return asnn_b200::cuda_fail(dev, e, "cudaSetDevice");
-    return asnn_b200::do_parse(dev, buf.data(), buf.size(), out, err_line);
+    return asnn_b200::parse_to_corpus(dev, buf.data(), buf.size(), out, err_line);
 }
 
 }  // extern "C"

@@ -801,6 +801,77 @@ int build(asnn_dev* dev, uint32_t G, const asnn_network_desc* nets, asnn_dev_lay
 
 }  // namespace
 
+// build() for one network whose arrays are already on the device (the
+// loader's output): same pipeline, no host round trip of the connections.
+int asnn_b200::build_device_network(asnn_dev* dev, DevBuf<uint32_t>&& nodes, uint32_t N, DevBuf<uint32_t>&& src,
+                                    DevBuf<uint32_t>&& dst, DevBuf<float>&& w, uint64_t E,
+                                    std::vector<uint32_t>&& inputs, std::vector<uint32_t>&& outputs,
+                                    asnn_dev_layout** out) {
+    cudaStream_t st = dev->stream;
+    *out = nullptr;
+    dev->timings = asnn_timings{};
+    if (E >= kUn) return fail(dev, ASNN_E_INVALID, "more than 2^32-1 connections");
+    DevNet d;
+    d.G = 1;
+    d.N = N;
+    d.E = E;
+    uint32_t last = 0;
+    if (N) CK(cudaMemcpyAsync(&last, nodes.p + (N - 1), 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint32_t bound = N ? last + 1 : 0;  // layout.cpp:24-26
+    if (bound == 0 && N) return fail(dev, ASNN_E_INVALID, "id space exceeds 2^32-1");
+    d.dense = N == 0 || last == N - 1;
+    d.h_idb = {0, bound};
+    d.h_idbound = {bound};
+    d.h_in_prefix = {0, static_cast<uint32_t>(inputs.size())};
+    d.h_out_prefix = {0, static_cast<uint32_t>(outputs.size())};
+    d.h_node_prefix = {0, N};
+    d.n_in = static_cast<uint32_t>(inputs.size());
+    d.n_out = static_cast<uint32_t>(outputs.size());
+    d.nodes = std::move(nodes);
+    d.src = std::move(src);
+    d.dst = std::move(dst);
+    d.w = std::move(w);
+    CK(d.inputs.alloc(d.n_in));
+    CK(d.outputs.alloc(d.n_out));
+    if (d.n_in) CK(cudaMemcpyAsync(d.inputs.p, inputs.data(), d.n_in * 4ull, cudaMemcpyHostToDevice, st));
+    if (d.n_out) CK(cudaMemcpyAsync(d.outputs.p, outputs.data(), d.n_out * 4ull, cudaMemcpyHostToDevice, st));
+    d.h_inputs = {std::move(inputs)};
+    d.h_outputs = {std::move(outputs)};
+    CK(d.idb_prefix.alloc(2));
+    CK(d.in_prefix.alloc(2));
+    CK(d.out_prefix.alloc(2));
+    CK(cudaMemcpyAsync(d.idb_prefix.p, d.h_idb.data(), 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d.in_prefix.p, d.h_in_prefix.data(), 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d.out_prefix.p, d.h_out_prefix.data(), 8, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    {
+        PhaseTimer t(dev, &dev->timings.upload_ms);
+        RC(build_adjacency(dev, d));
+    }
+    {
+        PhaseTimer t(dev, &dev->timings.required_ms);
+        RC(run_required(dev, d, nullptr));
+    }
+    {
+        PhaseTimer t(dev, &dev->timings.segment_ms);
+        RC(run_segment(dev, d));
+    }
+    RC(check_outputs(dev, d));
+    std::vector<NetMeta> metas;
+    FlatDevice f;
+    {
+        PhaseTimer t(dev, &dev->timings.flatten_ms);
+        d.pred_adj.reset();
+        d.succ_adj.reset();
+        d.req.reset();
+        d.si.reset();
+        RC(run_flatten(dev, d, metas, f));
+    }
+    d = DevNet();
+    return assemble_layout(dev, std::move(metas), std::move(f), out);
+}
+
 // Cycle test of validate (network.cpp:204): Kahn from every node without
 // predecessors over all connections; a node left without a level lies on, or
 // downstream of, a cycle.  nodes sorted unique; src / dst ids (device).

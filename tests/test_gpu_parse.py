@@ -238,3 +238,24 @@ def test_parse_then_activate(ref, oracle):
     X = np.random.default_rng(2).uniform(-2, 2, (64, len(net.inputs))).astype(np.float32)
     out, st = A.DeviceLayout.from_network(net).activate(X, state=True)
     assert np.array_equal(st.view(np.uint32), oracle.eval_batch(d, X).view(np.uint32))
+
+
+def test_load_layout_on_device(ref, oracle):
+    """asnn_dev_load_layout: text -> resident layout without a host round
+    trip; the same layout (bitwise) and activations as parse + build."""
+    net0 = ref.generate(A.random_spec(A.SplitMix64(77), 3000, 30000))
+    text = ref.serialize(net0)
+    dl = A.DeviceLayout.from_text(text)
+    net = A.parse_network(text)
+    d = oracle.layout(net)
+    lay = dl.download()
+    for k in ("layer_offsets", "node_ids", "row_ptr", "in_nodes"):
+        assert np.array_equal(getattr(lay, k), d[k]), k
+    assert np.array_equal(lay.in_weights.view(np.uint32), d["in_weights"].view(np.uint32))
+    X = np.random.default_rng(1).uniform(-2, 2, (64, len(net.inputs))).astype(np.float32)
+    _, st = dl.activate(X, state=True)
+    assert np.array_equal(st.view(np.uint32), oracle.eval_batch(d, X).view(np.uint32))
+    with pytest.raises(A.ParseError):
+        A.DeviceLayout.from_text(b"asnn 1\ninputs 0\noutputs 1\nedge 0 1 x\n")
+    with pytest.raises(A.ValidationError):
+        A.DeviceLayout.from_text(b"asnn 1\ninputs 0\noutputs 2\nedge 0 1 1\nedge 1 2 1\nedge 2 1 1\n")

@@ -10,6 +10,7 @@
 //   read_outputs, layer_slice_bounds, max_layer_width, depth, unassigned_outputs
 //   parse_network       io.cpp:83-156 + validate -> asnn_dev_parse_network
 //   read_network        io.cpp:167-173           -> asnn_dev_read_network
+//   validate, normalize network.cpp:69-85,151-216 -> asnn_dev_validate / _normalize
 //
 // Types keep the reference's field names and meanings; exceptions mirror
 // errors.hpp:9-55.  There is no host evaluator: ParallelConfig defaults to
@@ -243,6 +244,42 @@ inline Network parse_network(std::string_view text) {
     std::uint32_t line = 0;
     const int rc = asnn_dev_parse_network(dev, text.data(), text.size(), &c, &line);
     return detail::load(rc, dev, c, line);
+}
+
+// network.hpp:60-98: validate (all violations, the reference's order and
+// wording) and normalize, both on the device.
+struct ValidationReport {
+    std::vector<std::string> violations;
+    bool ok() const { return violations.empty(); }
+    const std::vector<std::string>& messages() const { return violations; }
+};
+
+inline ValidationReport validate(const Network& net) {
+    asnn_dev* dev = detail::device();
+    detail::NetView v(net);
+    std::uint32_t n = 0;
+    std::string buf(1u << 20, '\0');
+    detail::check(asnn_dev_validate(dev, &v.d, buf.data(), buf.size(), &n), dev);
+    ValidationReport r;
+    if (n) {
+        std::string all(buf.c_str());
+        std::size_t p = 0;
+        for (;;) {
+            const std::size_t q = all.find('\n', p);
+            r.violations.push_back(all.substr(p, q == std::string::npos ? std::string::npos : q - p));
+            if (q == std::string::npos) break;
+            p = q + 1;
+        }
+    }
+    return r;
+}
+
+inline Network normalize(const Network& net) {
+    asnn_dev* dev = detail::device();
+    detail::NetView v(net);
+    asnn_corpus* c = nullptr;
+    detail::check(asnn_dev_normalize(dev, &v.d, &c), dev);
+    return detail::network_from_corpus(c);
 }
 
 inline Network read_network(const std::string& path) {

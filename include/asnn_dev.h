@@ -248,6 +248,15 @@ int asnn_dev_parse_network(asnn_dev* dev, const char* text, uint64_t len, asnn_c
  * asnn_dev_build_layout. */
 int asnn_dev_load_layout(asnn_dev* dev, const char* text, uint64_t len, asnn_dev_layout** out,
                          uint32_t* err_line);
+/* validate (network.cpp:151-216) of an in-memory network on the device: the
+ * ValidationReport's messages, in the reference's order, joined by '\n' into
+ * report (cap bytes, NUL-terminated, truncated); *n_violations = their count
+ * (0 = valid).  nodes must be sorted and unique (make_network's invariant). */
+int asnn_dev_validate(asnn_dev* dev, const asnn_network_desc* net, char* report, uint64_t cap,
+                      uint32_t* n_violations);
+/* normalize (network.cpp:69-85): ids remapped to their positions in nodes
+ * (dense 0..N-1), on the device; ASNN_E_INVALID if an id names no node. */
+int asnn_dev_normalize(asnn_dev* dev, const asnn_network_desc* net, asnn_corpus** out);
 /* read_network (io.cpp:167-173): ASNN_E_IO when the file cannot be read. */
 int asnn_dev_read_network(asnn_dev* dev, const char* path, asnn_corpus** out, uint32_t* err_line);
 /* parse_weight's from_chars<float> on n tokens buf[off[i], off[i+1]) on the

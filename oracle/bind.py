@@ -204,6 +204,8 @@ class Ref:
             "ref_serialize": (C.c_uint64, [vp, C.c_char_p, C.c_uint64]),
             "ref_from_chars_f32": (None, [C.c_char_p, u64p, C.c_uint64, f32p, u8p]),
             "ref_format_double": (None, [C.c_double, C.c_char_p, C.c_uint64]),
+            "ref_validate_report": (C.c_uint32, [vp, C.c_char_p, C.c_uint64]),
+            "ref_normalize": (vp, [vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -300,6 +302,14 @@ class RefNet:
         L.ref_net_copy(h, _p(nodes, C.c_uint32), _p(ins, C.c_uint32), _p(outs, C.c_uint32),
                        _p(src, C.c_uint32), _p(dst, C.c_uint32), _p(w, C.c_float))
         return dict(nodes=nodes, inputs=ins, outputs=outs, source=src, target=dst, weight=w)
+
+    def validate_report(self) -> list:
+        buf = C.create_string_buffer(1 << 20)
+        n = self.L.ref_validate_report(self.h, buf, len(buf))
+        return buf.value.decode().split("\n") if n else []
+
+    def normalize(self) -> "RefNet":
+        return RefNet(self.ref, self.L.ref_normalize(self.h))
 
     def validate(self) -> int:
         return self.L.ref_validate(self.h)

@@ -10,6 +10,7 @@
 // the reference function named in its comment and only converts containers.
 #include <omp.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -137,6 +138,24 @@ void ref_net_copy(void* hp, std::uint32_t* nodes, std::uint32_t* inputs, std::ui
 // asnn::validate (network.cpp:151-216): number of violations.
 std::uint32_t ref_validate(void* hp) {
     return asnn::validate(static_cast<RefHandle*>(hp)->net).violations.size();
+}
+
+// validate (network.cpp:151-216): the messages joined by '\n' into buf.
+std::uint32_t ref_validate_report(void* hp, char* buf, std::uint64_t cap) {
+    const auto msgs = asnn::validate(static_cast<RefHandle*>(hp)->net).messages();
+    std::string all;
+    for (std::size_t i = 0; i < msgs.size(); ++i) all += (i ? "\n" : "") + msgs[i];
+    const std::size_t m = std::min<std::size_t>(all.size(), cap - 1);
+    std::memcpy(buf, all.data(), m);
+    buf[m] = 0;
+    return static_cast<std::uint32_t>(msgs.size());
+}
+
+// normalize (network.cpp:69-85) into a new handle.
+void* ref_normalize(void* hp) {
+    auto h = std::make_unique<RefHandle>();
+    h->net = asnn::normalize(static_cast<RefHandle*>(hp)->net);
+    return h.release();
 }
 
 // compute_required (network.cpp:222-255) + segment (segmentation.cpp:20-101)

@@ -109,6 +109,8 @@ PROTOTYPES = {
                                     C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]),
     "asnn_dev_parse_network": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p), u32p]),
     "asnn_dev_load_layout": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p), u32p]),
+    "asnn_dev_validate": (C.c_int, [C.c_void_p, C.POINTER(NetworkDesc), C.c_char_p, C.c_uint64, u32p]),
+    "asnn_dev_normalize": (C.c_int, [C.c_void_p, C.POINTER(NetworkDesc), C.POINTER(C.c_void_p)]),
     "asnn_dev_read_network": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p), u32p]),
     "asnn_dev_parse_weights": (C.c_int, [C.c_void_p, C.c_char_p, u64p, C.c_uint64, f32p, u8p]),
     "asnn_corpus_desc": (C.c_int, [C.c_void_p, C.POINTER(NetworkDesc)]),

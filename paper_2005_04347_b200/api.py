@@ -647,6 +647,26 @@ def parse_network(text, device: int = 0) -> Network:
     return _corpus_to_network(dev.lib, h)
 
 
+def validate(net: Network, device: int = 0) -> list:
+    """validate (network.cpp:151-216) on the device: the ValidationReport's
+    messages in the reference's order ([] = valid)."""
+    dev = Device.get(device)
+    buf = C.create_string_buffer(1 << 20)
+    n = C.c_uint32(0)
+    d = net.desc()
+    dev.check(dev.lib.asnn_dev_validate(dev.h, C.byref(d), buf, len(buf), C.byref(n)))
+    return buf.value.decode().split("\n") if n.value else []
+
+
+def normalize(net: Network, device: int = 0) -> Network:
+    """normalize (network.cpp:69-85) on the device: ids -> dense positions."""
+    dev = Device.get(device)
+    h = C.c_void_p()
+    d = net.desc()
+    dev.check(dev.lib.asnn_dev_normalize(dev.h, C.byref(d), C.byref(h)))
+    return _corpus_to_network(dev.lib, h)
+
+
 def read_network(path, device: int = 0) -> Network:
     """read_network (io.cpp:167-173): the file's bytes through parse_network."""
     dev = Device.get(device)

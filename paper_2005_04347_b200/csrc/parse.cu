@@ -321,6 +321,63 @@ __global__ void k_parse_weights(const char* __restrict__ buf, const uint64_t* __
     status[i] = r;
 }
 
+// validate (network.cpp:180-201): per connection, in the reference's order of
+// checks -- unknown endpoint, self-loop, duplicate (a later equal pair in the
+// stable (source, target) order), input with an incoming connection.
+enum : uint8_t { CS_OK = 0, CS_UNKNOWN, CS_SELF, CS_DUP, CS_INPUT_IN };
+__global__ void k_conn_status(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t E,
+                              const uint32_t* __restrict__ nodes, uint32_t N, const uint32_t* __restrict__ ins_sorted,
+                              uint32_t n_in, const uint32_t* __restrict__ dup, uint32_t* __restrict__ status,
+                              uint32_t* __restrict__ flag, uint32_t* __restrict__ valid) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= E) return;
+    const uint32_t a = src[k], b = dst[k];
+    uint32_t st = CS_OK;
+    if (!in_sorted(nodes, N, a) || !in_sorted(nodes, N, b)) st = CS_UNKNOWN;
+    else if (a == b) st = CS_SELF;
+    else if (dup[k]) st = CS_DUP;
+    else if (n_in && in_sorted(ins_sorted, n_in, b)) st = CS_INPUT_IN;
+    status[k] = st;
+    flag[k] = st != CS_OK;
+    valid[k] = st == CS_OK || st == CS_INPUT_IN;
+}
+
+// dup[order[k]] = 1 when the k-th pair in stable (source, target) order equals
+// the one before it.
+__global__ void k_dup_pairs(const uint32_t* __restrict__ order, uint64_t E, const uint32_t* __restrict__ src,
+                            const uint32_t* __restrict__ dst, uint32_t* __restrict__ dup) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= E) return;
+    const uint32_t b = order[k];
+    dup[b] = k > 0 && src[order[k - 1]] == src[b] && dst[order[k - 1]] == dst[b];
+}
+
+// declared ids: flags bit0 = an earlier occurrence in the list, bit1 = unknown
+__global__ void k_decl_flags(const uint32_t* __restrict__ ids, uint32_t n, const uint32_t* __restrict__ dupf,
+                             const uint32_t* __restrict__ nodes, uint32_t N, uint32_t* __restrict__ flags,
+                             uint32_t* __restrict__ any) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t f = (dupf[i] ? 1u : 0u) | (in_sorted(nodes, N, ids[i]) ? 0u : 2u);
+    flags[i] = f;
+    any[i] = f != 0;
+}
+
+// normalize (network.cpp:69-85): ids -> positions in the sorted node list
+__global__ void k_remap(const uint32_t* __restrict__ nodes, uint32_t N, const uint32_t* __restrict__ in,
+                        uint64_t n, uint32_t* __restrict__ out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t v = in[i];
+    uint32_t lo = 0, hi = N;
+    while (lo < hi) {
+        const uint32_t m = (lo + hi) / 2;
+        if (nodes[m] < v) lo = m + 1;
+        else hi = m;
+    }
+    out[i] = lo;
+}
+
 // ---- host helpers ---------------------------------------------------------------
 std::vector<std::string_view> split_ws(std::string_view line) {
     std::vector<std::string_view> out;
@@ -457,6 +514,136 @@ struct PhaseClock {
         t = n;
     }
 };
+
+// validate (network.cpp:151-216) on device arrays: nodes sorted unique,
+// inputs / outputs in declared order, connections in order.  Appends the
+// reference's violation messages, in its order, to viol.
+int validate_device(asnn_dev* dev, const uint32_t* nodes, uint32_t N, const uint32_t* ins, uint32_t n_in,
+                    const uint32_t* outs, uint32_t n_out, const uint32_t* src, const uint32_t* dst, uint64_t E,
+                    std::vector<std::string>& viol) {
+    cudaStream_t st = dev->stream;
+    if (!n_in) viol.push_back("inputs list is empty");
+    if (!n_out) viol.push_back("outputs list is empty");
+    DevBuf<uint32_t> sorted_in;  // sorted inputs (with repeats) for membership
+    const uint32_t* lists[2] = {ins, outs};
+    const uint32_t counts[2] = {n_in, n_out};
+    for (int k = 0; k < 2; ++k) {  // check_declared (network.cpp:158-168)
+        const uint32_t n = counts[k];
+        if (!n) continue;
+        DevBuf<uint32_t> keys, vals, dupf, flags, any;
+        CKP(keys.alloc(n));
+        CKP(vals.alloc(n));
+        CKP(dupf.alloc(n));
+        CKP(flags.alloc(n));
+        CKP(any.alloc(n));
+        CKP(cudaMemcpyAsync(keys.p, lists[k], n * 4ull, cudaMemcpyDeviceToDevice, st));
+        k_iota<<<nb(n), kT, 0, st>>>(vals.p, n);
+        SortBuffers sb;
+        uint32_t *ks = nullptr, *vs = nullptr;
+        RCP(radix_sort_pairs(dev, keys.p, vals.p, n, 32, sb, &ks, &vs, st));
+        k_dup_decl<<<nb(n), kT, 0, st>>>(ks, vs, n, dupf.p);
+        k_decl_flags<<<nb(n), kT, 0, st>>>(lists[k], n, dupf.p, nodes, N, flags.p, any.p);
+        std::vector<uint32_t> hit, h_ids, h_flags;
+        RCP(flagged_indices(dev, any.p, n, hit));
+        if (!hit.empty()) {
+            RCP(d2h(dev, h_ids, lists[k], n));
+            RCP(d2h(dev, h_flags, flags.p, n));
+            CKP(cudaStreamSynchronize(st));
+            const char* what = k ? "outputs" : "inputs";
+            for (uint32_t i : hit) {
+                if (h_flags[i] & 1u)
+                    viol.push_back("duplicate node " + std::to_string(h_ids[i]) + " in " + what);
+                if (h_flags[i] & 2u)
+                    viol.push_back("unknown node " + std::to_string(h_ids[i]) + " in " + what);
+            }
+        }
+        if (k == 0) {
+            CKP(sorted_in.alloc(n));
+            CKP(cudaMemcpyAsync(sorted_in.p, ks, n * 4ull, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    if (n_in && n_out) {  // input/output overlap, in outputs order (network.cpp:172-178)
+        DevBuf<uint32_t> flag;
+        CKP(flag.alloc(n_out));
+        k_member_flags<<<nb(n_out), kT, 0, st>>>(outs, n_out, sorted_in.p, n_in, flag.p);
+        std::vector<uint32_t> ov, h_out;
+        RCP(flagged_indices(dev, flag.p, n_out, ov));
+        if (!ov.empty()) {
+            RCP(d2h(dev, h_out, outs, n_out));
+            CKP(cudaStreamSynchronize(st));
+            std::string m = "input/output overlap:";
+            for (size_t i = 0; i < ov.size(); ++i) m += " " + std::to_string(h_out[ov[i]]);
+            viol.push_back(m);
+        }
+    }
+    if (!E) return ASNN_OK;
+    // per connection (network.cpp:180-201)
+    DevBuf<uint32_t> keys, vals, dup, status, flag, valid;
+    CKP(keys.alloc(E));
+    CKP(vals.alloc(E));
+    CKP(dup.alloc(E));
+    CKP(status.alloc(E));
+    CKP(flag.alloc(E));
+    CKP(valid.alloc(E));
+    CKP(cudaMemcpyAsync(keys.p, dst, E * 4, cudaMemcpyDeviceToDevice, st));
+    k_iota<<<nb(E), kT, 0, st>>>(vals.p, E);
+    SortBuffers sb;
+    uint32_t *ks = nullptr, *vs = nullptr;
+    RCP(radix_sort_pairs(dev, keys.p, vals.p, E, 32, sb, &ks, &vs, st));
+    DevBuf<uint32_t> k2, v2;
+    CKP(k2.alloc(E));
+    CKP(v2.alloc(E));
+    k_gather_u32<<<nb(E), kT, 0, st>>>(src, vs, E, k2.p);
+    CKP(cudaMemcpyAsync(v2.p, vs, E * 4, cudaMemcpyDeviceToDevice, st));
+    SortBuffers sb2;
+    uint32_t *ks2 = nullptr, *vs2 = nullptr;
+    RCP(radix_sort_pairs(dev, k2.p, v2.p, E, 32, sb2, &ks2, &vs2, st));
+    k_dup_pairs<<<nb(E), kT, 0, st>>>(vs2, E, src, dst, dup.p);
+    k_conn_status<<<nb(E), kT, 0, st>>>(src, dst, E, nodes, N, sorted_in.p, n_in, dup.p, status.p, flag.p, valid.p);
+    CKP(cudaGetLastError());
+    std::vector<uint32_t> bad;
+    RCP(flagged_indices(dev, flag.p, E, bad));
+    std::vector<uint32_t> hs, ht, hst;
+    if (!bad.empty()) {
+        RCP(d2h(dev, hs, src, E));
+        RCP(d2h(dev, ht, dst, E));
+        RCP(d2h(dev, hst, status.p, E));
+        CKP(cudaStreamSynchronize(st));
+        for (uint32_t j : bad) {
+            const std::string a = std::to_string(hs[j]), b = std::to_string(ht[j]);
+            switch (hst[j]) {
+                case CS_UNKNOWN: viol.push_back("connection " + a + "->" + b + " references an unknown node"); break;
+                case CS_SELF: viol.push_back("self-loop at node " + a); break;
+                case CS_DUP: viol.push_back("duplicate connection " + a + "->" + b); break;
+                default: viol.push_back("input " + b + " has incoming connection from " + a); break;
+            }
+        }
+    }
+    // cycle over the accepted connections (network.cpp:204, find_cycle)
+    DevBuf<uint32_t> vidx, tot, cs, cd;
+    CKP(vidx.alloc(E));
+    CKP(tot.alloc(1));
+    RCP(exclusive_scan(dev, valid.p, vidx.p, E, tot.p, st));
+    uint32_t nv = 0;
+    CKP(cudaMemcpyAsync(&nv, tot.p, 4, cudaMemcpyDeviceToHost, st));
+    CKP(cudaStreamSynchronize(st));
+    if (!nv) return ASNN_OK;
+    CKP(cs.alloc(nv));
+    CKP(cd.alloc(nv));
+    k_scatter_flagged<<<nb(E), kT, 0, st>>>(src, valid.p, vidx.p, E, cs.p);
+    k_scatter_flagged<<<nb(E), kT, 0, st>>>(dst, valid.p, vidx.p, E, cd.p);
+    bool cyclic = false;
+    RCP(device_cycle_check(dev, nodes, N, cs.p, cd.p, nv, &cyclic));
+    if (cyclic) {  // the reference's DFS names the cycle (host copies, error path only)
+        std::vector<uint32_t> hn, h1, h2;
+        RCP(d2h(dev, hn, nodes, N));
+        RCP(d2h(dev, h1, cs.p, nv));
+        RCP(d2h(dev, h2, cd.p, nv));
+        CKP(cudaStreamSynchronize(st));
+        viol.push_back(cycle_message(hn, h1, h2));
+    }
+    return ASNN_OK;
+}
 
 // A parsed, validated network resident on the device.
 struct Parsed {
@@ -694,77 +881,8 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, Parsed& res, uint32_
     clk.mark("make_network");
     // ---- validate (network.cpp:151-216)
     std::vector<std::string> viol;
-    if (!n_ids[0]) viol.push_back("inputs list is empty");
-    if (!n_ids[1]) viol.push_back("outputs list is empty");
-    DevBuf<uint32_t> sorted_in;  // sorted inputs (with repeats) for membership
-    for (int k = 0; k < 2; ++k) {
-        const uint32_t n = n_ids[k];
-        if (!n) continue;
-        DevBuf<uint32_t> keys, vals, flag;
-        CKP(keys.alloc(n));
-        CKP(vals.alloc(n));
-        CKP(flag.alloc(n));
-        CKP(cudaMemcpyAsync(keys.p, ids[k].p, n * 4ull, cudaMemcpyDeviceToDevice, st));
-        k_iota<<<nb(n), kT, 0, st>>>(vals.p, n);
-        SortBuffers sb;
-        uint32_t *ks = nullptr, *vs = nullptr;
-        RCP(radix_sort_pairs(dev, keys.p, vals.p, n, 32, sb, &ks, &vs, st));
-        k_dup_decl<<<nb(n), kT, 0, st>>>(ks, vs, n, flag.p);
-        std::vector<uint32_t> dups, h_ids;
-        RCP(flagged_indices(dev, flag.p, n, dups));
-        if (!dups.empty()) {
-            RCP(d2h(dev, h_ids, ids[k].p, n));
-            CKP(cudaStreamSynchronize(st));
-            for (uint32_t i : dups)
-                viol.push_back("duplicate node " + std::to_string(h_ids[i]) + " in " + (k ? "outputs" : "inputs"));
-        }
-        if (k == 0) {
-            CKP(sorted_in.alloc(n));
-            CKP(cudaMemcpyAsync(sorted_in.p, ks, n * 4ull, cudaMemcpyDeviceToDevice, st));
-        }
-    }
-    if (n_ids[0] && n_ids[1]) {  // input/output overlap, in outputs order
-        DevBuf<uint32_t> flag;
-        CKP(flag.alloc(n_ids[1]));
-        k_member_flags<<<nb(n_ids[1]), kT, 0, st>>>(ids[1].p, n_ids[1], sorted_in.p, n_ids[0], flag.p);
-        std::vector<uint32_t> ov, h_out;
-        RCP(flagged_indices(dev, flag.p, n_ids[1], ov));
-        if (!ov.empty()) {
-            RCP(d2h(dev, h_out, ids[1].p, n_ids[1]));
-            CKP(cudaStreamSynchronize(st));
-            std::string m = "input/output overlap:";
-            for (size_t i = 0; i < ov.size(); ++i) m += (i ? " " : " ") + std::to_string(h_out[ov[i]]);
-            viol.push_back(m);
-        }
-    }
-    if (n_ids[0] && E) {  // inputs with incoming connections, in connection order
-        DevBuf<uint32_t> flag;
-        CKP(flag.alloc(E));
-        k_member_flags<<<nb(E), kT, 0, st>>>(et.p, E, sorted_in.p, n_ids[0], flag.p);
-        std::vector<uint32_t> inc;
-        RCP(flagged_indices(dev, flag.p, E, inc));
-        if (!inc.empty()) {
-            std::vector<uint32_t> hs, ht;
-            RCP(d2h(dev, hs, es.p, E));
-            RCP(d2h(dev, ht, et.p, E));
-            CKP(cudaStreamSynchronize(st));
-            for (uint32_t j : inc)
-                viol.push_back("input " + std::to_string(ht[j]) + " has incoming connection from " +
-                               std::to_string(hs[j]));
-        }
-    }
-    bool cyclic = false;
-    clk.mark("validate lists");
-    if (E) RCP(device_cycle_check(dev, nodes.p, N, es.p, et.p, E, &cyclic));
-    clk.mark("cycle check");
-    if (cyclic) {  // the reference's DFS names the cycle (host copies, error path only)
-        std::vector<uint32_t> hn, hs, ht;
-        RCP(d2h(dev, hn, nodes.p, N));
-        RCP(d2h(dev, hs, es.p, E));
-        RCP(d2h(dev, ht, et.p, E));
-        CKP(cudaStreamSynchronize(st));
-        viol.push_back(cycle_message(hn, hs, ht));
-    }
+    RCP(validate_device(dev, nodes.p, N, ids[0].p, n_ids[0], ids[1].p, n_ids[1], es.p, et.p, E, viol));
+    clk.mark("validate");
     cudaEventRecord(dev->ev1, st);
     CKP(cudaStreamSynchronize(st));
     cudaEventElapsedTime(&tm.upload_ms, dev->ev0, dev->ev1);
@@ -862,6 +980,115 @@ int asnn_dev_load_layout(asnn_dev* dev, const char* text, uint64_t len, asnn_dev
     if (ce != cudaSuccess) return asnn_b200::cuda_fail(dev, ce, "load");
     return asnn_b200::build_device_network(dev, std::move(p.nodes), p.N, std::move(p.src), std::move(p.dst),
                                            std::move(p.w), p.E, std::move(ins), std::move(outs), out);
+}
+
+namespace {
+// Network arrays of a desc on the device (nodes must be sorted and unique,
+// the Network invariant make_network establishes, network.cpp:39-55).
+struct DescOnDevice {
+    asnn_b200::DevBuf<uint32_t> nodes, ins, outs, src, dst;
+};
+int upload_desc(asnn_dev* dev, const asnn_network_desc* n, DescOnDevice& d) {
+    using namespace asnn_b200;
+    if ((n->n_nodes && !n->nodes) || (n->n_inputs && !n->inputs) || (n->n_outputs && !n->outputs) ||
+        (n->n_connections && (!n->source || !n->target)))
+        return fail(dev, ASNN_E_INVALID, "null network array");
+    for (uint32_t i = 1; i < n->n_nodes; ++i)
+        if (n->nodes[i] <= n->nodes[i - 1])
+            return fail(dev, ASNN_E_INVALID, "Network.nodes must be sorted ascending and unique");
+    cudaStream_t st = dev->stream;
+    CKP(d.nodes.alloc(n->n_nodes));
+    CKP(d.ins.alloc(n->n_inputs));
+    CKP(d.outs.alloc(n->n_outputs));
+    CKP(d.src.alloc(n->n_connections));
+    CKP(d.dst.alloc(n->n_connections));
+    if (n->n_nodes) CKP(cudaMemcpyAsync(d.nodes.p, n->nodes, n->n_nodes * 4ull, cudaMemcpyHostToDevice, st));
+    if (n->n_inputs) CKP(cudaMemcpyAsync(d.ins.p, n->inputs, n->n_inputs * 4ull, cudaMemcpyHostToDevice, st));
+    if (n->n_outputs) CKP(cudaMemcpyAsync(d.outs.p, n->outputs, n->n_outputs * 4ull, cudaMemcpyHostToDevice, st));
+    if (n->n_connections) {
+        CKP(cudaMemcpyAsync(d.src.p, n->source, n->n_connections * 4, cudaMemcpyHostToDevice, st));
+        CKP(cudaMemcpyAsync(d.dst.p, n->target, n->n_connections * 4, cudaMemcpyHostToDevice, st));
+    }
+    return ASNN_OK;
+}
+}  // namespace
+
+// validate (network.cpp:151-216) of an in-memory network, on the device.
+int asnn_dev_validate(asnn_dev* dev, const asnn_network_desc* net, char* report, uint64_t cap,
+                      uint32_t* n_violations) {
+    using namespace asnn_b200;
+    if (!dev || !net || !n_violations || (cap && !report)) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    AllocStream alloc_on(dev->stream);
+    CKP(cudaSetDevice(dev->device));
+    DescOnDevice d;
+    RCP(upload_desc(dev, net, d));
+    std::vector<std::string> viol;
+    RCP(validate_device(dev, d.nodes.p, net->n_nodes, d.ins.p, net->n_inputs, d.outs.p, net->n_outputs, d.src.p,
+                        d.dst.p, net->n_connections, viol));
+    CKP(cudaStreamSynchronize(dev->stream));
+    *n_violations = static_cast<uint32_t>(viol.size());
+    if (cap) {
+        std::string all;
+        for (size_t i = 0; i < viol.size(); ++i) all += (i ? "\n" : "") + viol[i];
+        const size_t m = std::min<size_t>(all.size(), cap - 1);
+        std::memcpy(report, all.data(), m);
+        report[m] = 0;
+    }
+    return ASNN_OK;
+}
+
+// normalize (network.cpp:69-85): ids remapped to positions in nodes, on the device.
+int asnn_dev_normalize(asnn_dev* dev, const asnn_network_desc* net, asnn_corpus** out) {
+    using namespace asnn_b200;
+    if (!dev || !net || !out) return ASNN_E_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    AllocStream alloc_on(dev->stream);
+    *out = nullptr;
+    CKP(cudaSetDevice(dev->device));
+    DescOnDevice d;
+    RCP(upload_desc(dev, net, d));
+    cudaStream_t st = dev->stream;
+    const uint32_t N = net->n_nodes;
+    // every id must name a node (the reference dereferences node_index)
+    std::vector<std::string> unused;
+    DevBuf<uint32_t> flag;
+    const uint64_t n_all = static_cast<uint64_t>(net->n_inputs) + net->n_outputs + 2 * net->n_connections;
+    DevBuf<uint32_t> all, mapped;
+    CKP(all.alloc(n_all + 1));
+    CKP(mapped.alloc(n_all + 1));
+    uint64_t o = 0;
+    for (auto pr : {std::make_pair(d.ins.p, static_cast<uint64_t>(net->n_inputs)),
+                    std::make_pair(d.outs.p, static_cast<uint64_t>(net->n_outputs)),
+                    std::make_pair(d.src.p, net->n_connections), std::make_pair(d.dst.p, net->n_connections)}) {
+        if (pr.second) CKP(cudaMemcpyAsync(all.p + o, pr.first, pr.second * 4, cudaMemcpyDeviceToDevice, st));
+        o += pr.second;
+    }
+    CKP(flag.alloc(n_all + 1));
+    if (n_all) {
+        k_member_flags<<<nb(n_all), kT, 0, st>>>(all.p, n_all, d.nodes.p, N, flag.p);
+        k_remap<<<nb(n_all), kT, 0, st>>>(d.nodes.p, N, all.p, n_all, mapped.p);
+    }
+    std::vector<uint32_t> known, m;
+    RCP(d2h(dev, known, flag.p, n_all));
+    RCP(d2h(dev, m, mapped.p, n_all));
+    CKP(cudaStreamSynchronize(st));
+    for (uint64_t i = 0; i < n_all; ++i)
+        if (!known[i]) return fail(dev, ASNN_E_INVALID, "normalize: an id names no node");
+    auto* c = new asnn_corpus;
+    c->nodes.resize(N);
+    for (uint32_t i = 0; i < N; ++i) c->nodes[i] = i;
+    uint64_t q = 0;
+    c->inputs.assign(m.begin() + q, m.begin() + q + net->n_inputs);
+    q += net->n_inputs;
+    c->outputs.assign(m.begin() + q, m.begin() + q + net->n_outputs);
+    q += net->n_outputs;
+    c->src.assign(m.begin() + q, m.begin() + q + net->n_connections);
+    q += net->n_connections;
+    c->dst.assign(m.begin() + q, m.begin() + q + net->n_connections);
+    c->w.assign(net->weight, net->weight + net->n_connections);
+    *out = c;
+    return ASNN_OK;
 }
 
 int asnn_dev_parse_weights(asnn_dev* dev, const char* buf, const uint64_t* off, uint64_t n, float* out,

@@ -224,6 +224,14 @@ static void io_cases() {
         validation = e.violations.size() == 1 && e.violations[0] == "cycle: 1->2->1->1";  // network.cpp:125-135 path format
     }
     CHECK(validation);
+    const Network bad = make_network({0}, {2}, {{0, 1, 1.0f}, {1, 2, 1.0f}, {2, 1, 1.0f}, {1, 1, 0.5f}});
+    const auto rep = validate(bad);
+    CHECK(!rep.ok() && rep.violations.size() == 2 && rep.violations[0] == "self-loop at node 1");
+    CHECK(validate(net).ok());
+    const Network sparse = make_network({10}, {30}, {{10, 20, 1.0f}, {20, 30, 1.0f}});
+    const Network dense = normalize(sparse);
+    CHECK(dense.nodes == std::vector<NodeId>({0, 1, 2}) && dense.connections[1].source == 1 &&
+          dense.connections[1].target == 2);
     bool io = false;
     try {
         read_network("/nonexistent/dir/net.asnn");

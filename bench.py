@@ -388,7 +388,7 @@ def run_ours(args, cfg):
                          # every byte read or written once (edges,
                          # row pointers, each activation written and read once)
                          "compulsory_bytes_per_step": int(8 * E + 4 * (info["node_count"] + 1) +
-                                                          8 * info["node_count"] * B_total),
+                                                          8 * info["node_count"] * B),
                          "kernel": {"rows": "k_rows + k_heavy (one launch each per dependency level)",
                                     "segments": "k_rows (heavy rows split across levels) per dependency level",
                                     "k_cta": "k_cta (one CTA per network x batch slice, whole sweep)"}

@@ -934,7 +934,13 @@ int read_file(asnn_dev* dev, const char* path, std::vector<char>& buf) {
         dev->err = std::string("cannot open ") + path;
         return ASNN_E_IO;
     }
-    char tmp[1 << 16];
+    // one read of the whole file when its size is known (regular files)
+    if (std::fseek(f, 0, SEEK_END) == 0) {
+        const long size = std::ftell(f);
+        if (size > 0) buf.reserve(static_cast<size_t>(size));
+        std::rewind(f);
+    }
+    char tmp[1 << 20];
     size_t n;
     while ((n = std::fread(tmp, 1, sizeof(tmp), f)) > 0) buf.insert(buf.end(), tmp, tmp + n);
     const bool bad = std::ferror(f) != 0;

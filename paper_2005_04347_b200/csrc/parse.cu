@@ -940,9 +940,9 @@ int read_file(asnn_dev* dev, const char* path, std::vector<char>& buf) {
         if (size > 0) buf.reserve(static_cast<size_t>(size));
         std::rewind(f);
     }
-    char tmp[1 << 20];
+    std::vector<char> tmp(1 << 20);
     size_t n;
-    while ((n = std::fread(tmp, 1, sizeof(tmp), f)) > 0) buf.insert(buf.end(), tmp, tmp + n);
+    while ((n = std::fread(tmp.data(), 1, tmp.size(), f)) > 0) buf.insert(buf.end(), tmp.data(), tmp.data() + n);
     const bool bad = std::ferror(f) != 0;
     std::fclose(f);
     if (bad) {

@@ -389,7 +389,11 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         2 * (((std::min<uint64_t>(L->max_width, 1u << 20) + 1 + 3) * 4 + 15) / 16 * 16) +
         ((std::min<uint64_t>(L->max_level_edges, 1u << 20) + 1) * 8 + 15) / 16 * 16;
     const uint64_t per_sm = 228ull * 1024;
-    const uint32_t cmax = std::min<uint32_t>(ldA, 128);
+    static const uint32_t cmax_env = [] {
+        const char* s = getenv("ASNN_CTA_CMAX");
+        return s ? static_cast<uint32_t>(std::max(1, atoi(s))) : 128u;
+    }();
+    const uint32_t cmax = std::min<uint32_t>(std::min<uint32_t>(ldA, 128), cmax_env);
     // Pipelined consumers (finish group + prefix group) for latency-bound
     // layers of <= 512 items; off with ASNN_CTA_PIPE=0.
     const char* pe = getenv("ASNN_CTA_PIPE");

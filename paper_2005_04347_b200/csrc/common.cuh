@@ -53,16 +53,18 @@ __device__ __forceinline__ float sigmoid32_exact(float x) {
 // ~1 ulp of the true value too.  Checked for all 2^32 inputs against
 // sigmoid32_exact on the device (asnn_dev_sigmoid_selfcheck) and against the
 // reference's host sigmoid32 (tests/test_gpu_sigmoid.py).
-__device__ __forceinline__ float sigmoid32_path(float x, bool& exact) {
-    exact = false;
-    const double t = __dmul_rn(-4.97, static_cast<double>(x));
+//
+// The fast path is straight-line code (selects, no branches) so that the V
+// evaluations of a column group interleave their FP64 dependency chains;
+// sigmoid32_v takes the exact restatement in one rarely-taken branch after
+// all of them.
+__device__ __forceinline__ float sigmoid32_fast(float x, bool& exact) {
+    const double t0 = __dmul_rn(-4.97, static_cast<double>(x));
     // exp(t) <= 2^-54: 1 + exp(t) == 1 in both, v clamps below 1 and the
     // float rounds to 1 and clamps to 1 - FLT_EPSILON/2
-    if (t < -40.0) return 1.0f - 5.96046448e-08f;
-    if (!(t < 86.0)) {  // float subnormal / clamped results, NaN
-        exact = true;
-        return sigmoid32_exact(x);
-    }
+    const bool sat = t0 < -40.0;
+    const bool out = !(t0 < 86.0);  // float subnormal / clamped results, NaN
+    const double t = (sat || out) ? 0.0 : t0;
     const double zs = __fma_rn(t, XG_INVLN2N, XG_SHIFT);
     const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(zs));
     const double kd = __dsub_rn(zs, XG_SHIFT);
@@ -87,18 +89,43 @@ __device__ __forceinline__ float sigmoid32_path(float x, bool& exact) {
     // rounding midpoint 2^28 (in double ulps of y)
     const uint64_t yb = static_cast<uint64_t>(__double_as_longlong(y));
     const int64_t low = static_cast<int64_t>(yb & ((1ull << 29) - 1)) - (1ll << 28);
-    if (low < (1ll << 12) && low > -(1ll << 12)) {
-        exact = true;
-        return sigmoid32_exact(x);
-    }
+    const bool near = low < (1ll << 12) && low > -(1ll << 12);
     float f = __double2float_rn(y);
-    if (f >= 1.0f) f = 1.0f - 5.96046448e-08f;
+    f = (sat || f >= 1.0f) ? 1.0f - 5.96046448e-08f : f;
+    exact = out || (near && !sat);
     return f;
+}
+
+__device__ __forceinline__ float sigmoid32_path(float x, bool& exact) {
+    const float f = sigmoid32_fast(x, exact);
+    return exact ? sigmoid32_exact(x) : f;
 }
 
 __device__ __forceinline__ float sigmoid32(float x) {
     bool exact;
-    return sigmoid32_path(x, exact);
+    const float f = sigmoid32_fast(x, exact);
+    return exact ? sigmoid32_exact(x) : f;
+}
+
+// V independent sigmoid32 in place: fast paths first, then the exact
+// restatement for whichever values need it.
+template <int V>
+__device__ __forceinline__ void sigmoid32_v(float (&a)[V]) {
+    float f[V];
+    bool ex[V];
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        f[j] = sigmoid32_fast(a[j], ex[j]);
+        any |= ex[j];
+    }
+    if (any) {
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            if (ex[j]) f[j] = sigmoid32_exact(a[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) a[j] = f[j];
 }
 
 // One multiply-add of the reference accumulation (eval.cpp:20-21):

@@ -125,12 +125,12 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
             continue;
         }
         float* dst = As + static_cast<size_t>(pos_base - row_base + a + i) * ld + q * V;
+        sigmoid32_v<V>(acc);
         if constexpr (V == 4) {
-            *reinterpret_cast<float4*>(dst) =
-                make_float4(sigmoid32(acc[0]), sigmoid32(acc[1]), sigmoid32(acc[2]), sigmoid32(acc[3]));
+            *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
         } else {
 #pragma unroll
-            for (int v = 0; v < V; ++v) dst[v] = sigmoid32(acc[v]);
+            for (int v = 0; v < V; ++v) dst[v] = acc[v];
         }
     }
 }

@@ -123,10 +123,8 @@ k_level(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
             }
         }
     }
-    float out[V];
-#pragma unroll
-    for (int c = 0; c < V; ++c) out[c] = sigmoid32(acc[c]);
-    store_cols<V>(A + static_cast<uint64_t>(node) * ldA + col, out);
+    sigmoid32_v<V>(acc);
+    store_cols<V>(A + static_cast<uint64_t>(node) * ldA + col, acc);
 }
 
 // ---------------------------------------------------------------------------
@@ -208,8 +206,9 @@ k_rows(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ldA,
         *reinterpret_cast<float4*>(accbuf + static_cast<uint64_t>(aux & kSlotMask) * ldA + col) =
             make_float4(a0, a1, a2, a3);
     } else {
-        *reinterpret_cast<float4*>(A + static_cast<uint64_t>(node) * ldA + col) =
-            make_float4(sigmoid32(a0), sigmoid32(a1), sigmoid32(a2), sigmoid32(a3));
+        float o[4] = {a0, a1, a2, a3};
+        sigmoid32_v<4>(o);
+        *reinterpret_cast<float4*>(A + static_cast<uint64_t>(node) * ldA + col) = make_float4(o[0], o[1], o[2], o[3]);
     }
 }
 
@@ -319,8 +318,9 @@ k_warp_rows4(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ld
         *reinterpret_cast<float4*>(accbuf + static_cast<uint64_t>(aux & kSlotMask) * ldA + col) =
             make_float4(acc[0], acc[1], acc[2], acc[3]);
     } else {
+        sigmoid32_v<4>(acc);
         *reinterpret_cast<float4*>(A + static_cast<uint64_t>(t.x) * ldA + col) =
-            make_float4(sigmoid32(acc[0]), sigmoid32(acc[1]), sigmoid32(acc[2]), sigmoid32(acc[3]));
+            make_float4(acc[0], acc[1], acc[2], acc[3]);
     }
 }
 

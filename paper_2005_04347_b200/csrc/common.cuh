@@ -22,6 +22,13 @@ constexpr uint32_t kSlotMask = 0x3FFFFFFFu;
 static __device__ const uint64_t kExpTab[256] = {
 #include "exp_table.inc"
 };
+// sigmoid32's fast path reduces by 2^(i/32) instead (tools/gen_exp_table.py
+// --n 32): one 16-byte {tail, scale} load per evaluation from a 512-byte
+// table, four L1 lines for a warp's 32 random indices where the glibc table
+// takes two 8-byte loads over up to sixteen (profiles/r1_light_variants.txt).
+static __device__ __align__(16) const uint64_t kExp32Tab[64] = {
+#include "exp32_table.inc"
+};
 
 // sigmoid32 of the reference (network.hpp:44-59), bit for bit: the logistic
 // 1/(1+exp(-4.97 x)) in double, clamped into (0,1), rounded to float, clamped
@@ -44,9 +51,9 @@ __device__ __forceinline__ float sigmoid32_exact(float x) {
 
 // sigmoid32 with a short double-precision fast path and an exact rounding
 // test (Ziv): the fast path evaluates 1/(1+exp(-4.97 x)) to a relative error
-// below 2^-48 (degree-4 polynomial on the same 2^(i/128) table, reciprocal by
-// MUFU.RCP64H + two Newton steps) -- about half the FP64 operations of the
-// correctly rounded exp + division.  Whenever that value lies within 2^12
+// below 2^-47 (exp(t) = 2^(k/32) exp(r), |r| <= ln2/64, degree-5 Taylor
+// polynomial; reciprocal by MUFU.RCP64H + two Newton steps) -- about half the
+// FP64 operations of the correctly rounded exp + division.  Whenever that value lies within 2^12
 // double ulps (2^-40 relative) of a float rounding boundary, or the result
 // leaves the normal float range, the exact restatement above decides.  Both
 // results then round to the same float: the reference's double is within
@@ -65,18 +72,22 @@ __device__ __forceinline__ float sigmoid32_fast(float x, bool& exact) {
     const bool sat = t0 < -40.0;
     const bool out = !(t0 < 86.0);  // float subnormal / clamped results, NaN
     const double t = (sat || out) ? 0.0 : t0;
-    const double zs = __fma_rn(t, XG_INVLN2N, XG_SHIFT);
+    // k = round(t 32/ln2) in the low bits of zs; r = t - k ln2/32 with the hi
+    // part of ln2/32 exact against k (|k| < 2^12)
+    const double zs = __fma_rn(t, 0x1.71547652b82fep5, XG_SHIFT);
     const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(zs));
     const double kd = __dsub_rn(zs, XG_SHIFT);
-    double r = __fma_rn(kd, XG_NEGLN2HIN, t);
-    r = __fma_rn(kd, XG_NEGLN2LON, r);
-    const uint32_t idx = 2u * static_cast<uint32_t>(ki & 127u);
-    const double tail = __longlong_as_double(static_cast<long long>(__ldg(&kExpTab[idx])));
-    const uint64_t sbits = __ldg(&kExpTab[idx + 1]) + (ki << 45);
-    const double r2 = __dmul_rn(r, r);
-    double p = __fma_rn(r, XG_C3, XG_C2);
-    p = __fma_rn(r2, XG_C4, p);
-    const double tmp = __fma_rn(r2, p, __dadd_rn(r, tail));
+    double r = __fma_rn(kd, -0x1.62e42fefa0000p-6, t);
+    r = __fma_rn(kd, -0x1.cf79abc9e3b3ap-45, r);
+    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(kExp32Tab) + (ki & 31u));
+    const double tail = __longlong_as_double(static_cast<long long>(e.x));
+    const uint64_t sbits = e.y + (ki << 47);
+    double p = __fma_rn(r, 0x1.1111111111111p-7, 0x1.5555555555555p-5);
+    p = __fma_rn(r, p, 0x1.5555555555555p-3);
+    p = __fma_rn(r, p, 0.5);
+    // exp(r) - 1 = r + r^2 (1/2 + r (1/6 + r (1/24 + r/120))) + O(r^6/720),
+    // 2^-48.6 at |r| = ln2/64
+    const double tmp = __fma_rn(__dmul_rn(r, r), p, __dadd_rn(r, tail));
     const double scale = __longlong_as_double(static_cast<long long>(sbits));
     const double d = __dadd_rn(1.0, __fma_rn(scale, tmp, scale));
     double y;

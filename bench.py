@@ -308,19 +308,38 @@ def run_ours(args, cfg):
     def step():
         dl.activate_device(x_dev.data_ptr(), B, out_dev.data_ptr())
 
+    tw = time.perf_counter()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    per_step_s = (time.perf_counter() - tw) / max(1, args.warmup)
+    # nvidia-smi samples every 100 ms and needs ~0.1 s to start: a timed
+    # region shorter than that is bracketed by 0.3 s of the same (untimed)
+    # steps on each side inside the sampler, so the clocks reported are the
+    # ones under this load
+    pad = 0.0 if per_step_s * args.steps > 0.5 else 0.3
+
+    def load(seconds):
+        t_end = time.perf_counter() + seconds
+        while time.perf_counter() < t_end:
+            for _ in range(16):
+                step()
+            torch.cuda.synchronize()
+
     if dist:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        load(pad)
+        if dist:
+            dist.barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+        load(pad)
     ms = ev0.elapsed_time(ev1) / args.steps
     # per-launch device times (events between launches, same stream), for the
     # dominant kernel's roofline: median over 3 profiled sweeps
@@ -398,7 +417,8 @@ def run_ours(args, cfg):
                          "sweep_achieved_gbs": plan["alg_bytes"] / (ms / 1e3) / 1e9},
             "cpu_baseline": cb,
             "gpu_launches": plan["kernels"] * args.steps,
-            "clocks": clk.summary(),
+            "clocks": dict(clk.summary(), window="timed region" if not pad else
+                           f"timed region + {pad} s of untimed steps on each side"),
             "preprocess": {"wall_s": t_pre, "device_ms": pre_t, "generate_s": t_gen},
         }
         print(json.dumps(line), flush=True)

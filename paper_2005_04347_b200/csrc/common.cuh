@@ -112,10 +112,16 @@ __device__ __forceinline__ float sigmoid32_path(float x, bool& exact) {
     return exact ? sigmoid32_exact(x) : f;
 }
 
+// The exact restatement out of line, for single-value call sites: the
+// latency-bound one-column sweeps (config 3: 2.82 -> 2.70 ms) run a tighter
+// loop without its inlined body; column groups (V = 4) keep it inline
+// (config 5 measured 4% slower out of line, profiles/r1_light_variants.txt).
+__device__ __noinline__ float sigmoid32_exact_call(float x) { return sigmoid32_exact(x); }
+
 __device__ __forceinline__ float sigmoid32(float x) {
     bool exact;
     const float f = sigmoid32_fast(x, exact);
-    return exact ? sigmoid32_exact(x) : f;
+    return exact ? sigmoid32_exact_call(x) : f;
 }
 
 // V independent sigmoid32 in place: fast paths first, then the exact
@@ -133,7 +139,7 @@ __device__ __forceinline__ void sigmoid32_v(float (&a)[V]) {
     if (any) {
 #pragma unroll
         for (int j = 0; j < V; ++j)
-            if (ex[j]) f[j] = sigmoid32_exact(a[j]);
+            if (ex[j]) f[j] = (V == 1 ? sigmoid32_exact_call(a[j]) : sigmoid32_exact(a[j]));
     }
 #pragma unroll
     for (int j = 0; j < V; ++j) a[j] = f[j];

@@ -146,6 +146,10 @@ __global__ void __launch_bounds__(256, MINB)
 k_rows(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ldA,
        const uint4* __restrict__ rows, uint32_t n_rows, uint32_t tiles, const uint4* __restrict__ seg,
        uint32_t n_seg, float* __restrict__ accbuf) {
+    // programmatic dependent launch (engine.cu pdl_enabled): the next level's grid may
+    // become resident while this one drains; it reads only the static task
+    // record and edges before griddepcontrol.wait (a no-op otherwise)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t item = gt / LANES;
     const uint32_t ni = item / tiles;
@@ -155,6 +159,8 @@ k_rows(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ldA,
     // one 16-byte task record per item (no sched -> row_ptr dependent loads)
     const uint4 t = ni < n_seg ? __ldg(&seg[ni]) : __ldg(&rows[ni - n_seg]);
     const uint32_t node = t.x, beg = t.y, end = t.z, aux = t.w;
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(edges + beg));
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t col = tile * (LANES * 4) + lane * 4;
     const uint32_t stride = ldA * 4u;
     const char* __restrict__ Acol = reinterpret_cast<const char*>(A + col);

@@ -160,7 +160,7 @@ constexpr uint32_t kMetaBytes = kSlots * (8 + 8 + 32);
 // off the critical path.  The fp32 sum of a row is the same sequence of
 // roundings (segments.cuh); split[] comes from k_splits.
 template <int V, bool GUARD, bool GLOBAL, bool PIPE = false>
-__global__ void __launch_bounds__(288)
+__global__ void __launch_bounds__(544)
 k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       const uint32_t* __restrict__ le_cat, const uint32_t* __restrict__ row_ptr,
       const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,

@@ -471,7 +471,15 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     if (!p.C) return p;
     p.V = p.C >= 4 ? 4 : 1;
     const uint64_t items = static_cast<uint64_t>(L->max_width) * (p.C / p.V);
-    p.T = static_cast<uint32_t>(std::min<uint64_t>(256, std::max<uint64_t>(32, (items + 31) / 32 * 32)));
+    // consumer threads per CTA: up to 512 (+ the producer warp).  Config 5
+    // (1024 column-group items per layer, 2 CTAs/SM): 256 -> 0.90 ms, 512 ->
+    // 0.73 ms -- more warps to hide the FP64 sigmoid chains; 768 drops to one
+    // CTA per SM (1.14 ms).  ASNN_CTA_TMAX overrides (<= 512, the launch bound).
+    static const uint64_t tmax = [] {
+        const char* s = getenv("ASNN_CTA_TMAX");
+        return s ? std::min<uint64_t>(512, std::max(32, atoi(s)) / 32 * 32) : 512;
+    }();
+    p.T = static_cast<uint32_t>(std::min<uint64_t>(tmax, std::max<uint64_t>(32, (items + 31) / 32 * 32)));
     if (p.global) p.pipe = false;
     if (p.pipe) {  // finish group + prefix group of up to 4 warps each
         p.max_items = static_cast<uint32_t>(items);

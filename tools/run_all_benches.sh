@@ -6,6 +6,7 @@
 set -u
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests/ -q -m gpu > gpurun_out/pytest_gpu.txt 2>&1; tail -1 gpurun_out/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; tail -1 gpurun_out/smoke.txt
 nvidia-smi --query-gpu=name,clocks.max.sm,memory.total --format=csv,noheader > gpurun_out/gpu.txt
 lscpu | grep -E "Model name|^CPU\(s\)" > gpurun_out/host.txt
 for C in c1 c2 c3 c5; do

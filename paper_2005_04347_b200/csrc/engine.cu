@@ -507,6 +507,88 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
 // ---------------------------------------------------------------------------
 namespace asnn_b200 {
 
+namespace staging {
+constexpr size_t kStageChunk = 8u << 20;
+
+void par_memcpy(void* d, const void* s, size_t n) {
+    // OpenMP's pool (libgomp is linked for the generators): no per-call thread start
+    const int T = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, n >> 20)));
+    const size_t part = ((n + T - 1) / T + 4095) & ~size_t(4095);
+#pragma omp parallel for num_threads(T) schedule(static, 1)
+    for (int t = 0; t < T; ++t) {
+        const size_t a = static_cast<size_t>(t) * part;
+        if (a < n) std::memcpy(static_cast<char*>(d) + a, static_cast<const char*>(s) + a, std::min(part, n - a));
+    }
+}
+
+bool page_locked(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type != cudaMemoryTypeUnregistered;
+}
+
+cudaError_t ensure_stage(asnn_dev* dev) {
+    for (int b = 0; b < 2; ++b) {
+        cudaError_t e = dev->stage[b].ensure(kStageChunk);
+        if (e != cudaSuccess) return e;
+        if (!dev->stage_ev[b]) {
+            e = cudaEventCreateWithFlags(&dev->stage_ev[b], cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+}  // namespace staging
+
+using namespace staging;
+
+cudaError_t upload_host(asnn_dev* dev, void* dst, const void* src, size_t len, cudaStream_t st) {
+    if (len < 2 * kStageChunk || page_locked(src))
+        return len ? cudaMemcpyAsync(dst, src, len, cudaMemcpyHostToDevice, st) : cudaSuccess;
+    cudaError_t e = ensure_stage(dev);
+    if (e != cudaSuccess) return e;
+    for (size_t off = 0, i = 0; off < len; off += kStageChunk, ++i) {
+        const size_t n = std::min(kStageChunk, len - off);
+        const int b = static_cast<int>(i & 1);
+        if ((e = cudaEventSynchronize(dev->stage_ev[b])) != cudaSuccess) return e;  // its last DMA done
+        par_memcpy(dev->stage[b].p, static_cast<const char*>(src) + off, n);
+        if ((e = cudaMemcpyAsync(static_cast<char*>(dst) + off, dev->stage[b].p, n, cudaMemcpyHostToDevice, st)) !=
+            cudaSuccess)
+            return e;
+        if ((e = cudaEventRecord(dev->stage_ev[b], st)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t download_host(asnn_dev* dev, void* dst, const void* src, size_t len, cudaStream_t st) {
+    if (len < 2 * kStageChunk || page_locked(dst))  // stream-ordered, as the caller expects
+        return len ? cudaMemcpyAsync(dst, src, len, cudaMemcpyDeviceToHost, st) : cudaSuccess;
+    cudaError_t e = ensure_stage(dev);
+    if (e != cudaSuccess) return e;
+    const size_t chunks = (len + kStageChunk - 1) / kStageChunk;
+    for (size_t i = 0; i <= chunks; ++i) {
+        if (i < chunks) {  // DMA of chunk i into stage[i & 1] (chunk i - 2 was copied out already)
+            const size_t off = i * kStageChunk, n = std::min(kStageChunk, len - off);
+            const int b = static_cast<int>(i & 1);
+            if ((e = cudaEventSynchronize(dev->stage_ev[b])) != cudaSuccess) return e;
+            if ((e = cudaMemcpyAsync(dev->stage[b].p, static_cast<const char*>(src) + off, n,
+                                     cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+                return e;
+            if ((e = cudaEventRecord(dev->stage_ev[b], st)) != cudaSuccess) return e;
+        }
+        if (i >= 1) {  // host copy of chunk i - 1 while chunk i is in flight
+            const size_t j = i - 1, off = j * kStageChunk, n = std::min(kStageChunk, len - off);
+            const int b = static_cast<int>(j & 1);
+            if ((e = cudaEventSynchronize(dev->stage_ev[b])) != cudaSuccess) return e;
+            par_memcpy(static_cast<char*>(dst) + off, dev->stage[b].p, n);
+        }
+    }
+    return cudaSuccess;
+}
+
 int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& flat,
                     asnn_dev_layout** result) {
     const uint32_t G = static_cast<uint32_t>(nets.size());
@@ -1238,7 +1320,7 @@ void asnn_dev_close(asnn_dev* dev) {
     if (!dev) return;
     cudaSetDevice(dev->device);
     cudaStreamSynchronize(dev->stream);
-    for (cudaEvent_t ev : {dev->ev0, dev->ev1, dev->ev2, dev->ev3, dev->ev4})
+    for (cudaEvent_t ev : {dev->ev0, dev->ev1, dev->ev2, dev->ev3, dev->ev4, dev->stage_ev[0], dev->stage_ev[1]})
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : dev->fork_ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : dev->join_ev) cudaEventDestroy(ev);

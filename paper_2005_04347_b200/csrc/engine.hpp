@@ -135,9 +135,20 @@ struct asnn_dev {
     uint32_t option_epoch = 0;       // bumps invalidate cached sweep graphs
     asnn_timings timings{};
     asnn_b200::PinnedBuf pin_x, pin_out;  // pinned staging of pageable host buffers (all layouts)
+    asnn_b200::PinnedBuf stage[2];        // double-buffered staging of large pageable transfers
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
 
 namespace asnn_b200 {
+
+// Large transfers between pageable host memory and the device (the loader's
+// text, the parsed corpus): 8 MB chunks through two pinned staging buffers,
+// the host side of each chunk copied by up to 8 threads while the other
+// chunk's DMA runs.  Small or page-locked buffers take one cudaMemcpyAsync.
+// The staged paths return with the host buffer no longer needed (download:
+// filled); the direct ones are ordinary stream-ordered copies.
+cudaError_t upload_host(asnn_dev* dev, void* dst, const void* src, size_t len, cudaStream_t st);
+cudaError_t download_host(asnn_dev* dev, void* dst, const void* src, size_t len, cudaStream_t st);
 
 // In-degree thresholds above which a row goes to the streamed heavy kernel.
 constexpr int kNumHeavyThr = 9;

@@ -476,7 +476,7 @@ std::string cycle_message(const std::vector<uint32_t>& nodes, const std::vector<
 template <typename T>
 int d2h(asnn_dev* dev, std::vector<T>& h, const T* d, uint64_t n) {
     h.resize(n);
-    if (n) CKP(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, dev->stream));
+    if (n) CKP(download_host(dev, h.data(), d, n * sizeof(T), dev->stream));
     return ASNN_OK;
 }
 
@@ -662,7 +662,7 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, Parsed& res, uint32_
     // ---- 1. text and line starts
     DevBuf<char> d_text;
     CKP(d_text.alloc(len + 1));
-    if (len) CKP(cudaMemcpyAsync(d_text.p, text, len, cudaMemcpyHostToDevice, st));
+    if (len) CKP(upload_host(dev, d_text.p, text, len, st));
     const uint64_t n_chunks = (len + 255) / 256;
     DevBuf<uint32_t> cnt, coff, tot;
     CKP(cnt.alloc(n_chunks + 1));

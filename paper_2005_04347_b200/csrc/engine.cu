@@ -1408,15 +1408,15 @@ int asnn_dev_upload_layout(asnn_dev* dev, const asnn_layout_desc* d, asnn_dev_la
     CK(f.outputs.alloc(d->n_outputs));
     if (d->node_count) {
         CK(cudaMemcpyAsync(f.node_ids.p, d->node_ids, d->node_count * 4ull, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(row64.p, d->row_ptr, (d->node_count + 1) * 8ull, cudaMemcpyHostToDevice, st));
+        CK(upload_host(dev, row64.p, d->row_ptr, (d->node_count + 1) * 8ull, st));
         k_row64_to_32<<<blocks_for(d->node_count + 1), kThreads, 0, st>>>(row64.p, d->node_count + 1,
                                                                            f.row_ptr.p);
     } else {
         CK(cudaMemsetAsync(f.row_ptr.p, 0, 4, st));
     }
     if (E) {
-        CK(cudaMemcpyAsync(f.in_ids.p, d->in_nodes, E * 4, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(f.w.p, d->in_weights, E * 4, cudaMemcpyHostToDevice, st));
+        CK(upload_host(dev, f.in_ids.p, d->in_nodes, E * 4, st));
+        CK(upload_host(dev, f.w.p, d->in_weights, E * 4, st));
     }
     if (d->n_inputs)
         CK(cudaMemcpyAsync(f.inputs.p, d->input_order, d->n_inputs * 4ull, cudaMemcpyHostToDevice, st));

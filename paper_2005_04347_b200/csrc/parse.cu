@@ -1012,8 +1012,8 @@ int upload_desc(asnn_dev* dev, const asnn_network_desc* n, DescOnDevice& d) {
     if (n->n_inputs) CKP(cudaMemcpyAsync(d.ins.p, n->inputs, n->n_inputs * 4ull, cudaMemcpyHostToDevice, st));
     if (n->n_outputs) CKP(cudaMemcpyAsync(d.outs.p, n->outputs, n->n_outputs * 4ull, cudaMemcpyHostToDevice, st));
     if (n->n_connections) {
-        CKP(cudaMemcpyAsync(d.src.p, n->source, n->n_connections * 4, cudaMemcpyHostToDevice, st));
-        CKP(cudaMemcpyAsync(d.dst.p, n->target, n->n_connections * 4, cudaMemcpyHostToDevice, st));
+        CKP(upload_host(dev, d.src.p, n->source, n->n_connections * 4, st));
+        CKP(upload_host(dev, d.dst.p, n->target, n->n_connections * 4, st));
     }
     return ASNN_OK;
 }

@@ -398,9 +398,9 @@ int upload_networks(asnn_dev* dev, uint32_t G, const asnn_network_desc* nets, De
         const asnn_network_desc& n = nets[0];
         if (N) CK(cudaMemcpyAsync(d.nodes.p, n.nodes, N * 4, cudaMemcpyHostToDevice, st));
         if (E) {
-            CK(cudaMemcpyAsync(d.src.p, n.source, E * 4, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d.dst.p, n.target, E * 4, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d.w.p, n.weight, E * 4, cudaMemcpyHostToDevice, st));
+            CK(upload_host(dev, d.src.p, n.source, E * 4, st));
+            CK(upload_host(dev, d.dst.p, n.target, E * 4, st));
+            CK(upload_host(dev, d.w.p, n.weight, E * 4, st));
         }
         if (d.n_in) CK(cudaMemcpyAsync(d.inputs.p, n.inputs, d.n_in * 4ull, cudaMemcpyHostToDevice, st));
         if (d.n_out) CK(cudaMemcpyAsync(d.outputs.p, n.outputs, d.n_out * 4ull, cudaMemcpyHostToDevice, st));

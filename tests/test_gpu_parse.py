@@ -259,3 +259,21 @@ def test_load_layout_on_device(ref, oracle):
         A.DeviceLayout.from_text(b"asnn 1\ninputs 0\noutputs 1\nedge 0 1 x\n")
     with pytest.raises(A.ValidationError):
         A.DeviceLayout.from_text(b"asnn 1\ninputs 0\noutputs 2\nedge 0 1 1\nedge 1 2 1\nedge 2 1 1\n")
+
+
+@pytest.mark.slow
+def test_large_text_staged_transfers(ref):
+    """Config 2's network as text (~139 MB, 5M edges): the text goes up and
+    the parsed arrays (20 MB each) come back through the chunked pinned
+    staging of engine.cu (upload_host / download_host, 8 MB chunks, both
+    buffers and a ragged last chunk) -- same network, weights bit for bit."""
+    net = A.generate_mlp(200, 500, 0.1, 2)
+    text = ref.serialize(ref.network(net))
+    assert len(text) > 64 << 20
+    got = A.parse_network(text)
+    rn, err = ref.parse(text)
+    assert err is None
+    want = rn.arrays()
+    for k in ("nodes", "inputs", "outputs", "source", "target"):
+        assert np.array_equal(getattr(got, k), want[k]), k
+    assert np.array_equal(got.weight.view(np.uint32), want["weight"].view(np.uint32))

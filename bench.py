@@ -403,6 +403,13 @@ def run_ours(args, cfg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": profiled_traffic(cfg),
                          "peak_source": peak_src,
+                         # what actually binds, when it is not HBM
+                         "binding": {"c4": "HBM random-row gathers (0.92 of the 256-B gather ceiling)",
+                                     "c2": "L2 throughput: gathers served from L2 (DRAM 0.46 GB of "
+                                           "20.8 GB algorithmic), so frac > 1 against HBM",
+                                     "c3": "latency: one dependent chain per layer per CTA, 2000 layers",
+                                     "c5": "FP64 sigmoid latency / layer barriers, shared-memory resident",
+                                     "c1": "latency: 10 layers in one CTA"}.get(cfg),
                          "alg_bytes_per_step": plan["alg_bytes"],
                          # every byte read or written once (edges,
                          # row pointers, each activation written and read once)

@@ -133,6 +133,10 @@ def load() -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        # asnn_dev_activate taking raw addresses (pinned / mapped buffers held
+        # by the caller as integers): no per-call ctypes casts
+        lib.activate_addr = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64,
+                                        C.c_void_p, C.c_void_p)(("asnn_dev_activate", lib))
         _lib = lib
     return _lib
 

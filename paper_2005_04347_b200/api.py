@@ -518,9 +518,9 @@ class DeviceLayout:
 
     def activate_host_ptr(self, x_ptr: int, n_vec: int, n_x: int, out_ptr: int):
         """Host-buffer activation by raw pointers (pinned torch tensors)."""
-        self.dev.check(self.dev.lib.asnn_dev_activate(
-            self.h, C.cast(C.c_void_p(x_ptr), f32p), n_vec, n_x, C.cast(C.c_void_p(out_ptr), f32p),
-            None))
+        rc = self.dev.lib.activate_addr(self.h, x_ptr, n_vec, n_x, out_ptr, None)
+        if rc:
+            self.dev.check(rc)
 
     def activate_device(self, x_ptr: int, n_vec: int, out_ptr: int):
         """Device pointers, stream-ordered on the device handle's stream."""

@@ -1071,7 +1071,7 @@ int ensure_workspace(asnn_dev_layout* L, uint32_t n_vec) {
     const uint32_t ldA = padded_batch(n_vec);
     if (cta_plan(L, ldA).pipe && !L->split.p) {
         L->graph.reset();
-        CK(L->split.alloc(L->total_pos));
+        CK(L->split.alloc(L->total_pos + 8));  // slack: K-cta bulk copies round up to 16 bytes
         const uint32_t G = static_cast<uint32_t>(L->nets.size());
         k_splits<<<dim3((L->max_pos + 255) / 256, G), 256, 0, dev->stream>>>(
             reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->row_ptr.p, L->edges.p, L->split.p);

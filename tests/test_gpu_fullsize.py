@@ -1,6 +1,7 @@
-"""Parity at BASELINE.json's full size (config 4: 10M nodes, ~495M edges,
-batch 64) through size-independent properties -- the oracle cannot sweep
-this network in test time, so:
+"""Parity at BASELINE.json's full sizes.  Configs 2, 3 and 5: every vector
+(every network) bitwise against the oracle's eval_sequential.  Config 4
+(10M nodes, ~495M edges, batch 64) through size-independent properties --
+the oracle cannot sweep this network in test time, so:
   * self-consistency (test_eval.cpp:109-134): every sampled node recomputes
     bit for bit from the finished id-indexed state with the oracle's
     activate_node restatement -- including the heaviest rows, whose sums the
@@ -45,3 +46,44 @@ def test_config4_self_consistency(oracle):
         rec = oracle.recompute(d, X[b], st[b], sample)
         got = st[b][lay.node_ids[sample]]
         assert np.array_equal(rec.view(np.uint32), got.view(np.uint32)), b
+
+
+@pytest.mark.parametrize("cfg,check", [("c2", 1024), ("c3", 256)])
+def test_config_full_size_bitwise(oracle, cfg, check):
+    """Configs 2 and 3 at BASELINE.json's full size, activated with the full
+    batch through the strategy the engine picks (per-level k_rows for C2,
+    pipelined K-cta for C3); `check` vectors (all of them) compared with the
+    oracle's eval_sequential bit for bit, state and outputs."""
+    net = bench.make_network(cfg, 1.0)[0]
+    B = bench.CONFIGS[cfg][1]
+    dl = A.DeviceLayout.from_network(net)
+    X = np.random.default_rng(11).uniform(-2, 2, (B, len(net.inputs))).astype(np.float32)
+    out, st = dl.activate(X, outputs=True, state=True)
+    d = oracle.layout(net)
+    rows = np.sort(np.random.default_rng(12).choice(B, check, replace=False))
+    want = oracle.eval_batch(d, X[rows])
+    assert np.array_equal(st[rows].view(np.uint32), want.view(np.uint32))
+    assert np.array_equal(out[rows].view(np.uint32), want[:, net.outputs].view(np.uint32))
+    dl.free()
+
+
+def test_config5_population_full_size_bitwise(oracle):
+    """Config 5 at full size: 10k networks x 128 vectors in one K-cta launch;
+    every network's outputs compared with the oracle bit for bit (state for
+    every 50th network)."""
+    nets = bench.make_network("c5", 1.0)
+    B = bench.CONFIGS["c5"][1]
+    rng = np.random.default_rng(13)
+    X = [rng.uniform(-2, 2, (B, len(n.inputs))).astype(np.float32) for n in nets]
+    dl = A.DeviceLayout.from_population(nets)
+    out, _ = dl.activate(np.concatenate([x.reshape(-1) for x in X]), outputs=True, n_vec=B)
+    out = np.asarray(out).reshape(-1)
+    off = 0
+    for g, (n, x) in enumerate(zip(nets, X)):
+        k = len(n.outputs)
+        got = out[off:off + B * k].reshape(B, k)
+        off += B * k
+        d = oracle.layout(n)
+        want = oracle.eval_batch(d, x)
+        assert np.array_equal(got.view(np.uint32), want[:, n.outputs].view(np.uint32)), g
+    dl.free()

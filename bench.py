@@ -30,6 +30,9 @@ import numpy as np
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+METRIC = "connection evals/s (edges x vectors per second), full activation sweep"
+DATA = "synthetic (seeded generator, DESIGN.md corpora)"
+
 CONFIGS = {
     # name: (description, builder kwargs, batch)
     "c1": ("small random ASNN (1k nodes, 10k connections), single input vector", 1),
@@ -159,18 +162,75 @@ def profiled_traffic(cfg):
     return None
 
 
+def make_network_ref(cfg: str, scale: float = 1.0):
+    """The same corpora as make_network without the engine, for the
+    reference arm: configs 1, 3 and 5 from the reference's own generate()
+    (netgen.cpp:71-157 in oracle/_ref, byte-identical to the engine's
+    restatement -- tests/test_corpus.py), configs 2 and 4 from the bench
+    generators compiled out of csrc/netgen.cpp into oracle/libcorpus.so.
+    Returns NetArrays (plain arrays) or, for configs 1/3/5, RefNet handles."""
+    from oracle.bind import Corpus, Ref, SplitMix64
+    if cfg == "c2":
+        return [Corpus().mlp(200, 500, 0.1, 2)]
+    if cfg == "c4":
+        n = int(10_000_000 * scale)
+        return [Corpus().powerlaw(n, 100, 1024, 1024, int(500_000_000 * scale), 2.1, 4)]
+
+    class Spec:
+        def __init__(self, i, o, h, c, d, seed):
+            self.input_count, self.output_count, self.hidden_count = i, o, h
+            self.connection_count, self.target_depth, self.seed = c, d, seed
+            self.weight_min, self.weight_max = -1.0, 1.0
+    ref = Ref()
+    if cfg == "c1":
+        return [ref.generate(Spec(16, 4, 980, 10000, 10, 1))]
+    if cfg == "c3":
+        return [ref.generate(Spec(16, 4, 49980, 500000, 2000, 3))]
+    if cfg == "c5":
+        rng = SplitMix64(5)
+        return [ref.generate(Spec(8, 4, 188, 1000, 8, rng.next())) for _ in range(int(10_000 * scale))]
+    raise ValueError(cfg)
+
+
+def net_counts(net):
+    """(nodes, inputs, edges) of a network given as arrays or a RefNet handle."""
+    if hasattr(net, "h"):
+        L = net.L
+        return L.ref_net_n_nodes(net.h), L.ref_net_n_inputs(net.h), L.ref_net_n_edges(net.h)
+    return len(net.nodes), len(net.inputs), len(net.source)
+
+
+def config_dict(cfg: str, nets, world: int) -> dict:
+    """The workload description both arms print (identical keys and values)."""
+    counts = [net_counts(n) for n in nets]
+    B = CONFIGS[cfg][1]
+    per_gpu = B if cfg == "c5" else -(-B // world)
+    return {"workload": CONFIGS[cfg][0], "config": cfg,
+            "edges": int(sum(c[2] for c in counts)), "nodes": int(sum(c[0] for c in counts)),
+            "networks": len(nets), "batch": B, "batch_per_gpu": per_gpu,
+            "parallelism": (f"population-sharded x{world}" if cfg == "c5" else
+                            f"batch-sharded dp{world}"),
+            "l2": "working set > 126 MB L2 (no flush)" if cfg in ("c2", "c4") else
+                  "L2-resident working set; per-step state rewritten"}
+
+
 class RefCPU:
     """The reference's own CPU evaluator (oracle/_ref: the unmodified reference
     compiled from its sources) prepared once on the same networks; each
     measurement times a bounded sample of input vectors of that workload.
 
-    Modes: "par" = eval_parallel with all host
-    threads, one vector at a time; "omp-seq" = an OpenMP loop of
-    eval_sequential over `threads` vectors at once.  For C5 the sample is the
-    first `max_nets` networks of the population (each with its own vectors)."""
+    Modes (all the reference's unchanged code):
+      "seq"     eval_sequential on ONE core, vector by vector (bench.cpp:82-83);
+      "par"     eval_parallel with all host threads, vector by vector;
+      "omp-seq" an OpenMP loop of eval_sequential over `threads` vectors.
+    For C5 the sample is the first `max_nets` networks of the population (each
+    with its own vectors).  `nets` are NetArrays / api.Network objects, or
+    RefNet handles from the reference's own generator."""
+
+    MODES = {"seq": 0, "par": 1, "omp-seq": 2}
 
     def __init__(self, nets, X_all, cfg, max_nets=64):
-        from oracle.bind import Oracle, Ref, available_ref
+        from oracle.bind import Oracle, Ref, RefNet, available_ref
         self.kind = "reference" if available_ref() else "port"
         self.ref = Ref() if self.kind == "reference" else None
         self.oracle = None if self.ref else Oracle()
@@ -179,10 +239,16 @@ class RefCPU:
         host = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
         self.threads = max(self.ref.L.ref_max_threads(), host or 1) if self.ref else 1
         self.items = []
+        self.evaluated = 0
         for gi, net in enumerate(nets[:max_nets]):
-            if cfg in ("c2", "c4"):
-                # reference preprocessing of C4 takes ~20 min:
-                # build its LayeredLayout straight from the banded CSR instead
+            if isinstance(net, RefNet):
+                h = net
+                assert h.preprocess() == 0
+            elif cfg in ("c2", "c4"):
+                # reference preprocessing of C4 takes ~20 min: build its
+                # LayeredLayout straight from the banded CSR instead -- the
+                # identical layout (sha256 equal to the reference's own
+                # flatten, tests/test_oracle_golden.py::test_banded_layout_is_reference_flatten)
                 lay = host_layout_banded(cfg, net)
                 h = self.ref.layout_from_csr(lay) if self.ref else lay
             elif self.ref:
@@ -190,7 +256,10 @@ class RefCPU:
                 assert h.preprocess() == 0
             else:
                 h = self.oracle.layout(net)
-            self.items.append((h, len(net.source), X_all[gi]))
+            E = net_counts(net)[2]
+            ev = self.ref.L.ref_layout_edge_count(h.h) if self.ref else len(h["in_nodes"])
+            self.items.append((h, E, X_all[gi]))
+            self.evaluated += ev
         self.n_nets = len(self.items)
 
     def run(self, mode, n_vec):
@@ -203,33 +272,43 @@ class RefCPU:
                 self.oracle.eval_batch(h, Xs)
                 t = time.perf_counter() - t0
             else:
-                t, _ = h.eval_batch(Xs, mode={"par": 1, "omp-seq": 2}[mode], workers=self.threads)
+                t, _ = h.eval_batch(Xs, mode=self.MODES[mode],
+                                    workers=1 if mode == "seq" else self.threads)
             ev += E * len(Xs)
             dt += t
         return ev, dt
 
+    def sample_mode(self, mode, budget_s):
+        """Vectors one call at a time (several at once for omp-seq) until about
+        budget_s seconds are spent: (conn_evals, seconds, vectors)."""
+        ev = dt = 0.0
+        n = 0
+        n_max = self.items[0][2].shape[0]
+        step = self.threads if mode == "omp-seq" else 1
+        while (n == 0 or dt < budget_s) and n < n_max:
+            k = min(step, n_max - n) if mode != "omp-seq" else min(step, n_max)
+            e, t = self.run(mode, k)
+            ev, dt, n = ev + e, dt + t, n + k
+            if mode == "omp-seq":
+                break
+        return ev, dt, n
+
     def measure(self, budget_s=20.0):
-        """Best mode within about budget_s seconds of CPU work."""
+        """All three modes on a bounded sample (about budget_s/3 s each); the
+        best one is the baseline, every mode is reported by name."""
         if self.ref is None:
             ev, dt = self.run("par", 1)
             return self.describe("port-seq", ev, dt, 1)
-        res = {}
-        # eval_parallel: vectors one by one until half the budget is spent
-        ev = dt = 0.0
-        n = 0
-        while dt < budget_s / 2 and n < self.items[0][2].shape[0]:
-            e, t = self.run("par", 1)
-            ev += e
-            dt += t
-            n += 1
-        res["par"] = (ev, dt, n)
-        e, t = self.run("omp-seq", self.threads)
-        res["omp-seq"] = (e, t, self.threads)
+        res = {m: self.sample_mode(m, budget_s / 3) for m in ("seq", "par", "omp-seq")}
         mode = max(res, key=lambda k: res[k][0] / res[k][1])
-        return self.describe(mode, *res[mode])
+        d = self.describe(mode, *res[mode])
+        d["modes"] = {m: {"value": r[0] / r[1], "cores": 1 if m == "seq" else self.threads,
+                          "vectors": r[2], "seconds": round(r[1], 3)} for m, r in res.items()}
+        return d
 
     def describe(self, mode, ev, dt, n_vec):
-        return {"value": ev / dt, "unit": "conn_evals/s", "cores": self.threads, "kind": self.kind,
+        return {"value": ev / dt, "unit": "conn_evals/s",
+                "cores": 1 if mode in ("seq", "port-seq") else self.threads, "kind": self.kind,
                 "mode": mode,
                 "sample": f"{n_vec} vector(s) x {self.n_nets} network(s) of this workload in "
                           f"{dt:.2f}s ({mode})"}
@@ -383,20 +462,17 @@ def run_ours(args, cfg):
         cb = cpu_baseline(nets, X, cfg, budget_s=args.cpu_budget)
     if rank == 0:
         line = {
-            "metric": "connection evals/s (edges x vectors per second), full activation sweep",
+            "metric": METRIC,
             "value": value, "unit": "conn_evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if cfg != "c5" else "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded generator, DESIGN.md corpora)",
-            "config": {"workload": CONFIGS[cfg][0], "config": cfg, "edges": E,
-                       "nodes": int(sum(len(n.nodes) for n in nets)),
-                       "levels": info["total_layers"], "batch": B_total,
-                       "batch_per_gpu": B,
-                       "parallelism": (f"population-sharded x{world} (networks per GPU: "
-                                       f"{len(shard)})" if cfg == "c5" else
-                                       f"batch-sharded dp{world}"),
-                       "l2": "working set > 126 MB L2 (no flush)" if cfg in ("c2", "c4") else
-                             "L2-resident working set; per-step state rewritten"},
+            "data": DATA,
+            "config": config_dict(cfg, nets, world),
+            # the reference's convention counts every connection (bench.cpp:53);
+            # edges into nodes without a level are never evaluated by either side
+            "evaluated_edges": int(evaluated),
+            "value_evaluated": evaluated * B_total / (ms / 1e3),
+            "levels": info["total_layers"],
             "e2e": {"value": conn_evals_total / e2e_s, "unit": "conn_evals/s",
                     "h2d_bytes_per_step": int(x_pin.numel() * 4 * world),
                     "d2h_bytes_per_step": int(out_pin.numel() * 4 * world)},
@@ -434,37 +510,56 @@ def run_ours(args, cfg):
 
 
 def run_reference(args, cfg):
+    """The reference arm: the reference's own CPU implementation (oracle/_ref)
+    on this box's host cores, on the same workload and config as ours.  Only
+    oracle/ is loaded (never the engine).  Each step evaluates a bounded
+    sample of the batch's vectors in the fastest of the reference's modes
+    (picked on a short calibration); value = connection evals of the timed
+    steps / their measured time."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    nets = make_network(cfg, args.scale)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    nets = make_network_ref(cfg, args.scale)
     rng = np.random.default_rng(12345)
     B_total = CONFIGS[cfg][1]
+    n_in = [net_counts(n)[1] for n in nets]
     if cfg == "c5":
-        X = [rng.uniform(-2, 2, (B_total, len(n.inputs))).astype(np.float32) for n in nets]
+        X = [rng.uniform(-2, 2, (B_total, k)).astype(np.float32) for k in n_in]
     else:
-        X = [rng.uniform(-2, 2, (B_total, len(nets[0].inputs))).astype(np.float32)]
+        X = [rng.uniform(-2, 2, (B_total, n_in[0])).astype(np.float32)]
     cpu = RefCPU(nets, X, cfg)
-    first = cpu.measure(budget_s=max(2.0, args.cpu_budget / 4))   # picks the faster mode
-    mode = first["mode"]
-    n_vec = 1 if mode in ("par", "port-seq") else cpu.threads
-    vals = []
-    for _ in range(args.warmup + args.steps):
-        ev, dt = cpu.run("par" if mode == "port-seq" else mode, n_vec)
-        vals.append(cpu.describe(mode, ev, dt, n_vec))
-    cb = vals[-1]
-    timed = vals[args.warmup:]
-    value = statistics.mean(v["value"] for v in timed)
-    E = sum(len(n.source) for n in nets)
+    calib = cpu.measure(budget_s=max(1.5, args.cpu_budget / 4))
+    mode = calib["mode"]
+    # vectors per step: about 0.5 s of work per step (whole multiples of the
+    # thread count for omp-seq), at most the batch
+    per_vec = calib["modes"][mode]["seconds"] / calib["modes"][mode]["vectors"] \
+        if "modes" in calib else 1.0
+    n_vec = max(1, min(B_total, int(0.5 / max(per_vec, 1e-9))))
+    if mode == "omp-seq":
+        n_vec = min(B_total, max(cpu.threads, n_vec // cpu.threads * cpu.threads))
+    times, evs = [], []
+    for i in range(args.warmup + args.steps):
+        ev, dt = cpu.run(mode, n_vec)
+        if i >= args.warmup:
+            times.append(dt)
+            evs.append(ev)
+    value = sum(evs) / sum(times)
     line = {
         "impl": "reference",
-        "metric": "connection evals/s (edges x vectors per second), full activation sweep",
-        "value": value, "unit": "conn_evals/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "metric": METRIC,
+        "value": value, "unit": "conn_evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-        "ms_per_step": E * B_total / value * 1e3, "dtype": "f32",
-        "data": "synthetic (seeded generator, DESIGN.md corpora)",
-        "config": {"workload": CONFIGS[cfg][0], "config": cfg, "edges": E, "batch": B_total},
-        "cpu_baseline": {**cb, "value": value},
+        "ms_per_step": statistics.mean(times) * 1e3, "dtype": "f32",
+        "data": DATA,
+        "config": config_dict(cfg, nets, world),
+        "conn_evals_per_step": int(evs[0]),
+        "evaluated_edges": int(cpu.evaluated) if cfg != "c5" else None,
+        "cpu_baseline": {"value": value, "unit": "conn_evals/s", "kind": cpu.kind,
+                         "cores": 1 if mode == "seq" else cpu.threads, "mode": mode,
+                         "modes": calib.get("modes"),
+                         "sample": f"each step: {n_vec} of the {B_total} vectors x {cpu.n_nets} "
+                                   f"network(s) ({mode}); mode picked on a calibration run"},
         "e2e": {"value": value, "unit": "conn_evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "vs_baseline": None,

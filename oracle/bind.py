@@ -411,3 +411,83 @@ class RefDev(Ref):
 
 def available_ref_dev() -> bool:
     return REF_DEV_SO.exists()
+
+
+# --- bench corpora for the CPU legs (oracle/libcorpus.so) ------------------------------
+CORPUS_SO = HERE / "libcorpus.so"
+
+
+class SplitMix64:
+    """rng.hpp:10-38 (seeds of the config-5 population, like the reference)."""
+    M = 0xFFFFFFFFFFFFFFFF
+
+    def __init__(self, seed: int):
+        self.s = seed & self.M
+
+    def next(self) -> int:
+        self.s = (self.s + 0x9E3779B97F4A7C15) & self.M
+        z = self.s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & self.M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & self.M
+        return z ^ (z >> 31)
+
+
+class NetArrays:
+    """A network as plain arrays (network.hpp:12-32 fields)."""
+
+    def __init__(self, nodes, inputs, outputs, source, target, weight):
+        self.nodes, self.inputs, self.outputs = nodes, inputs, outputs
+        self.source, self.target, self.weight = source, target, weight
+
+
+class _NetDesc(C.Structure):
+    _fields_ = [("n_nodes", C.c_uint32), ("nodes", u32p), ("n_inputs", C.c_uint32),
+                ("inputs", u32p), ("n_outputs", C.c_uint32), ("outputs", u32p),
+                ("n_connections", C.c_uint64), ("source", u32p), ("target", u32p),
+                ("weight", f32p)]
+
+
+class Corpus:
+    """The bench's seeded generators compiled from csrc/netgen.cpp into
+    oracle/libcorpus.so (no device code, no engine): configs 2 and 4."""
+
+    def __init__(self):
+        if not CORPUS_SO.exists():
+            raise FileNotFoundError(f"{CORPUS_SO} not built (make -C oracle)")
+        L = C.CDLL(str(CORPUS_SO))
+        vp = C.c_void_p
+        L.asnn_gen_mlp.restype = C.c_int
+        L.asnn_gen_mlp.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_uint64, C.POINTER(vp)]
+        L.asnn_gen_powerlaw.restype = C.c_int
+        L.asnn_gen_powerlaw.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                        C.c_double, C.c_uint64, C.POINTER(vp)]
+        L.asnn_corpus_desc.restype = C.c_int
+        L.asnn_corpus_desc.argtypes = [vp, C.POINTER(_NetDesc)]
+        L.asnn_corpus_free.restype = None
+        L.asnn_corpus_free.argtypes = [vp]
+        self.L = L
+
+    def _take(self, h) -> NetArrays:
+        d = _NetDesc()
+        self.L.asnn_corpus_desc(h, C.byref(d))
+
+        def arr(p, n, dt):
+            return np.ctypeslib.as_array(p, shape=(n,)).copy() if n else np.zeros(0, dt)
+        net = NetArrays(arr(d.nodes, d.n_nodes, np.uint32), arr(d.inputs, d.n_inputs, np.uint32),
+                        arr(d.outputs, d.n_outputs, np.uint32),
+                        arr(d.source, d.n_connections, np.uint32),
+                        arr(d.target, d.n_connections, np.uint32),
+                        arr(d.weight, d.n_connections, np.float32))
+        self.L.asnn_corpus_free(h)
+        return net
+
+    def mlp(self, layers, width, p, seed) -> NetArrays:
+        h = C.c_void_p()
+        assert self.L.asnn_gen_mlp(layers, width, p, seed, C.byref(h)) == 0
+        return self._take(h)
+
+    def powerlaw(self, n_nodes, bands, n_in, n_out, target_edges, alpha, seed) -> NetArrays:
+        h = C.c_void_p()
+        assert self.L.asnn_gen_powerlaw(n_nodes, bands, n_in, n_out, target_edges, alpha, seed,
+                                        C.byref(h)) == 0
+        return self._take(h)

@@ -1043,8 +1043,11 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
                 cfg.blockDim = dim3(kThreads);
                 cfg.stream = st;
                 cfg.attrs = attr;
-                // only after another kernel on this stream (not an event join)
-                cfg.numAttrs = pdl_enabled() && !fork && !prev_join && l > 1 ? 1 : 0;
+                // only after another kernel on this stream (not an event join), and
+                // only when every 32-byte sector of A belongs to one row (ldA >= 8):
+                // the gathers are ld.global.nc, so no sector a later level reads
+                // may share bytes with rows the previous grid is still writing
+                cfg.numAttrs = pdl_enabled() && !fork && !prev_join && l > 1 && ldA >= 8 ? 1 : 0;
                 CK(cudaLaunchKernelEx(&cfg, ll.rows, static_cast<const uint2*>(L->edges.p), L->A.p, ldA,
                                       static_cast<const uint4*>(L->rtask.p + L->lvl_off[l] + nh), nrows,
                                       ll.tiles,
@@ -1094,6 +1097,13 @@ int ensure_workspace(asnn_dev_layout* L, uint32_t n_vec) {
         L->graph.reset();
         CK(L->A.alloc(need));
         CK(cudaMemsetAsync(L->A.p, 0, need * sizeof(float), L->dev->stream));
+        L->zero_ldA = ldA;
+    } else if (L->zero_refs && L->zero_ldA != ldA) {
+        // A narrower sweep reuses the array: row total_pos at the new pitch
+        // overlaps rows an earlier, wider sweep wrote -- clear it again.
+        CK(cudaMemsetAsync(L->A.p + static_cast<size_t>(L->total_pos) * ldA, 0, ldA * sizeof(float),
+                           L->dev->stream));
+        L->zero_ldA = ldA;
     }
     return ASNN_OK;
 }
@@ -1384,6 +1394,18 @@ int asnn_dev_upload_layout(asnn_dev* dev, const asnn_layout_desc* d, asnn_dev_la
         return fail(dev, ASNN_E_INVALID, "layer_offsets do not cover node_count");
     const uint64_t E = d->node_count ? d->row_ptr[d->node_count] : 0;
     if (E >= 0xFFFFFFFFull) return fail(dev, ASNN_E_INVALID, "more than 2^32-1 edges");
+    if (d->total_layers && d->layer_offsets[0] != 0) return fail(dev, ASNN_E_INVALID, "layer_offsets[0] != 0");
+    for (uint32_t k = 0; k < d->total_layers; ++k)
+        if (d->layer_offsets[k + 1] < d->layer_offsets[k])
+            return fail(dev, ASNN_E_INVALID, "layer_offsets decrease");
+    if (d->node_count) {
+        if (d->row_ptr[0] != 0) return fail(dev, ASNN_E_INVALID, "row_ptr[0] != 0");
+        int64_t bad = 0;
+        const int64_t N = d->node_count;
+#pragma omp parallel for reduction(| : bad) if (N > (1 << 20))
+        for (int64_t i = 0; i < N; ++i) bad |= d->row_ptr[i + 1] < d->row_ptr[i];
+        if (bad) return fail(dev, ASNN_E_INVALID, "row_ptr decreases");
+    }
     cudaStream_t st = dev->stream;
     CK(cudaEventRecord(dev->ev0, st));
     NetMeta n;

@@ -226,6 +226,7 @@ struct asnn_dev_layout {
     uint32_t max_pos = 0;                  // largest network (positions)
     uint32_t max_level_edges = 0;          // most edges into one layer of one network
     bool zero_refs = false;                // some predecessor has no position (zero row)
+    uint32_t zero_ldA = 0;                 // row pitch the zero row was last cleared at
 
     // Heavy-row segments (one network; segments.cuh): short ones run in k_rows
     // ahead of the level's rows, long ones in k_heavy

@@ -258,3 +258,47 @@ def test_predecessors_without_position(oracle, B, sweep_mode):
     dl = A.DeviceLayout.from_layout(to_layout(d, net.outputs))
     _, st = dl.activate(X, outputs=True, state=True)
     assert bitwise_equal(st, oracle.eval_batch(d, X))
+
+
+@pytest.mark.parametrize("sweep_mode", [0, 1, 2, 3])
+def test_zero_row_reused_across_narrowing_batches(oracle, sweep_mode):
+    """One DeviceLayout reused with batch widths going down (256, 64, 4, 1):
+    the zero row at the narrower pitch overlaps rows the wider sweep wrote
+    and must read 0.0f again (eval.cpp:20-21 reads a zero-initialised slot)."""
+    rng = A.SplitMix64(405)
+    net = A.generate(A.random_spec(rng, 500, 4000))
+    dead = int(net.nodes.max()) + 3
+    net = A.Network(np.append(net.nodes, dead), net.inputs, net.outputs,
+                    np.append(net.source, net.inputs[0]), np.append(net.target, dead),
+                    np.append(net.weight, np.float32(0.5)))
+    d = oracle.layout(net)
+    d["in_nodes"] = d["in_nodes"].copy()
+    d["in_nodes"][np.random.default_rng(7).random(len(d["in_nodes"])) < 0.05] = dead
+    dl = A.DeviceLayout.from_layout(to_layout(d, net.outputs))
+    A.Device.get(0).set_sweep_mode(sweep_mode)
+    try:
+        for B in (256, 64, 4, 1, 64, 2):
+            X = np.random.default_rng(B).uniform(-2, 2, (B, len(d["input_order"]))).astype(np.float32)
+            _, st = dl.activate(X, outputs=True, state=True)
+            assert bitwise_equal(st, oracle.eval_batch(d, X)), B
+    finally:
+        A.Device.get(0).set_sweep_mode(0)
+
+
+def test_upload_rejects_malformed_descriptors(oracle):
+    """asnn_dev_upload_layout validates the CSR it is handed: row_ptr must
+    start at 0 and never decrease, layer_offsets likewise (ASNN_E_INVALID,
+    not out-of-bounds device reads)."""
+    rng = A.SplitMix64(406)
+    net = A.generate(A.random_spec(rng, 200, 1000))
+    d = oracle.layout(net)
+    for key, mutate in (("row_ptr", lambda a: a.__setitem__(3, a[4] + 5)),
+                        ("row_ptr", lambda a: a.__setitem__(0, 1)),
+                        ("layer_offsets", lambda a: a.__setitem__(1, a[2] + 1)),
+                        ("layer_offsets", lambda a: a.__setitem__(0, 1))):
+        bad = dict(d)
+        bad[key] = d[key].copy()
+        mutate(bad[key])
+        with pytest.raises(ValueError):
+            A.DeviceLayout.from_layout(to_layout(bad, net.outputs))
+    A.DeviceLayout.from_layout(to_layout(d, net.outputs)).free()

@@ -1,7 +1,14 @@
-"""Parity at BASELINE.json's full sizes.  Configs 2, 3 and 5: every vector
-(every network) bitwise against the oracle's eval_sequential.  Config 4
-(10M nodes, ~495M edges, batch 64) through size-independent properties --
-the oracle cannot sweep this network in test time, so:
+"""Parity at BASELINE.json's full sizes.
+
+Configs 1 and 4 against the REFERENCE itself: tests/golden/fullsize_<cfg>.npz
+holds the digests the unmodified reference produced on the same seeded
+network (tests/golden/make_fullsize.py: its own compute_required / segment /
+flatten, ~20 min for config 4, and eval_parallel on every vector of the batch):
+the device layout (levels, node order, rows, weights, input order, dropped
+count) and every vector's full id-indexed state must hash identically.
+
+Configs 2, 3 and 5: every vector (every network) bitwise against the oracle's
+eval_sequential.  Config 4 additionally through size-independent properties:
   * self-consistency (test_eval.cpp:109-134): every sampled node recomputes
     bit for bit from the finished id-indexed state with the oracle's
     activate_node restatement -- including the heaviest rows, whose sums the
@@ -10,13 +17,63 @@ the oracle cannot sweep this network in test time, so:
   * the declared outputs equal the state at the output ids (read_outputs)."""
 from __future__ import annotations
 
+import pathlib
+
 import numpy as np
 import pytest
 
 import bench
 import paper_2005_04347_b200 as A
 
+def _fixture_module():
+    import importlib.util
+    path = pathlib.Path(__file__).resolve().parent / "golden" / "make_fullsize.py"
+    spec = importlib.util.spec_from_file_location("make_fullsize", path)
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+_fx = _fixture_module()
+layout_digest, state_digest = _fx.layout_digest, _fx.state_digest
+
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+GOLDEN = pathlib.Path(__file__).resolve().parent / "golden"
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c4"])
+def test_config_against_reference_golden(cfg):
+    """compute_required / segment / flatten and eval_parallel of the reference
+    (segmentation.cpp:20-101, layout.cpp:12-83, eval.cpp:49-80) vs the device,
+    bit for bit, at the config's full size and full batch (64 vectors)."""
+    g = np.load(GOLDEN / f"fullsize_{cfg}.npz")
+    net = bench.make_network(cfg, 1.0)[0]
+    dl = A.DeviceLayout.from_network(net)
+    lay = dl.download()
+    assert len(lay.node_ids) == int(g["node_count"])
+    assert len(lay.in_nodes) == int(g["edge_count"])
+    assert lay.total_layers == int(g["total_layers"])
+    assert lay.dropped_connections == int(g["dropped"])
+    assert lay.id_bound == int(g["id_bound"])
+    assert layout_digest(dict(layer_offsets=lay.layer_offsets, node_ids=lay.node_ids,
+                              row_ptr=lay.row_ptr, in_nodes=lay.in_nodes,
+                              in_weights=lay.in_weights, input_order=lay.input_order)) \
+        == str(g["layout_sha256"])
+    del lay
+    assert len(A.compute_required(net).members) == int(g["required_count"])
+    X = g["x"]
+    outputs = np.asarray(net.outputs)
+    want_out = g["outputs"]
+    # the whole batch in one sweep, then in slices of 16 (other kernels / pitches)
+    for lo, hi in ((0, X.shape[0]), (0, 16), (48, 64)):
+        out, st = dl.activate(X[lo:hi], outputs=True, state=True)
+        assert np.array_equal(out.view(np.uint32), want_out[lo:hi].view(np.uint32))
+        for b in range(hi - lo):
+            assert state_digest(st[b]) == str(g["state_sha256"][lo + b]), (lo + b)
+            assert np.array_equal(st[b][outputs].view(np.uint32), want_out[lo + b].view(np.uint32))
+        del st
+    dl.free()
 
 
 def test_config4_self_consistency(oracle):

@@ -285,6 +285,7 @@ class RefCPU:
         n = 0
         n_max = self.items[0][2].shape[0]
         step = self.threads if mode == "omp-seq" else 1
+        self.run(mode, min(step, n_max))            # untimed: first-touch, thread team
         while (n == 0 or dt < budget_s) and n < n_max:
             k = min(step, n_max - n) if mode != "omp-seq" else min(step, n_max)
             e, t = self.run(mode, k)
@@ -303,7 +304,7 @@ class RefCPU:
         mode = max(res, key=lambda k: res[k][0] / res[k][1])
         d = self.describe(mode, *res[mode])
         d["modes"] = {m: {"value": r[0] / r[1], "cores": 1 if m == "seq" else self.threads,
-                          "vectors": r[2], "seconds": round(r[1], 3)} for m, r in res.items()}
+                          "vectors": r[2], "seconds": r[1]} for m, r in res.items()}
         return d
 
     def describe(self, mode, ev, dt, n_vec):
@@ -319,52 +320,72 @@ def cpu_baseline(nets, X_all, cfg, budget_s=20.0):
 
 
 def run_ours(args, cfg):
+    """Our arm.  One process per GPU (torchrun for N > 1).  Every rank holds
+    a full layout replica and sweeps its contiguous slice of the batch (C5:
+    its contiguous slice of the population); a step is the sweep plus the
+    all-gather of the declared outputs, which the engine enqueues on its own
+    stream right after the sweep (NCCL, asnn_dev_allgather).  With
+    ASNN_BENCH_ONE_GPU=1 every rank shares GPU 0 -- a functional check of the
+    N > 1 path: NCCL cannot place two ranks on one device, so the gather then
+    goes through torch.distributed (gloo) on the host, still inside the step."""
     import torch
     import paper_2005_04347_b200 as A
+    from paper_2005_04347_b200.shard import batch_slice, population_shard
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if os.environ.get("ASNN_BENCH_ONE_GPU"):
-        local = 0          # functional check of the N>1 path on a single-GPU box
+    one_gpu = bool(os.environ.get("ASNN_BENCH_ONE_GPU"))
+    if one_gpu:
+        local = 0
     dist = None
     if world > 1:
         import torch.distributed as dist
-        backend = os.environ.get("ASNN_BENCH_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     t_setup = time.perf_counter()
     nets = make_network(cfg, args.scale)
     B_total = CONFIGS[cfg][1]
     rng = np.random.default_rng(12345)
-    from paper_2005_04347_b200.shard import batch_slice, gather_rows, population_shard
+    shards = args.shard_of or world
     if cfg == "c5":
-        # population sharding: networks dealt round-robin, each keeps its 128 vectors
-        mine = population_shard(len(nets), world, rank)
-        shard = [nets[g] for g in mine]
         X = [rng.uniform(-2, 2, (B_total, len(n.inputs))).astype(np.float32) for n in nets]
+        owned = [population_shard(len(nets), world, r) for r in range(world)]
+        mine = owned[rank]
+        shard = [nets[g] for g in mine]
         Xs = [X[g] for g in mine]
         B = B_total
+        out_counts = [B * sum(len(nets[g].outputs) for g in o) for o in owned]
     else:
-        # batch sharding: a full layout replica, a contiguous slice of the vectors
         shard = nets
         X_full = rng.uniform(-2, 2, (B_total, len(nets[0].inputs))).astype(np.float32)
+        X = [X_full]
         # --shard-of G (development): one process measuring rank 0's slice of a
         # G-way split, i.e. the per-GPU workload of a G-GPU run
-        lo, hi = batch_slice(B_total, args.shard_of or world, rank)
+        slices = [batch_slice(B_total, shards, r) for r in range(world)]
+        lo, hi = slices[rank]
         Xs = [X_full[lo:hi]]
-        X = [X_full]
         B = hi - lo
+        out_counts = [(h - l) * len(nets[0].outputs) for l, h in slices]
     t_gen = time.perf_counter() - t_setup
 
     dev = A.Device.get(local)
-    # one explicit stream shared by the engine and the timing events
+    # one explicit stream shared by the engine, its gather and the timing events
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     dev.set_stream(stream.cuda_stream)
+    gather = "none (one GPU)"
+    if dist is not None:
+        if one_gpu:
+            gather = "gloo on the host (one-GPU functional mode)"
+        else:
+            uid = [A.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            dev.comm_init(uid[0], world, rank)
+            gather = "nccl all-gather in the engine (asnn_dev_allgather)"
     t0 = time.perf_counter()
     if cfg == "c5":
         dl = A.DeviceLayout.from_population(shard, device=local)
@@ -382,10 +403,24 @@ def run_ours(args, cfg):
     plan = dl.plan(B)
 
     x_dev = torch.from_numpy(np.concatenate([x.reshape(-1) for x in Xs])).cuda()
-    out_dev = torch.empty(info["n_outputs"] * B, dtype=torch.float32, device="cuda")
+    my_off = sum(out_counts[:rank])
+    out_all = torch.zeros(max(1, sum(out_counts)), dtype=torch.float32, device="cuda")
+    out_dev = out_all[my_off:my_off + max(1, out_counts[rank])]
+    torch.cuda.synchronize()
+
+    def gather_out():
+        if dist is None:
+            return
+        if one_gpu:
+            parts = [torch.zeros(c) for c in out_counts]
+            dist.all_gather(parts, out_dev[:out_counts[rank]].cpu())
+            out_all.copy_(torch.cat(parts), non_blocking=True)
+        else:
+            dev.allgather(out_dev.data_ptr(), out_all.data_ptr(), out_counts)
 
     def step():
         dl.activate_device(x_dev.data_ptr(), B, out_dev.data_ptr())
+        gather_out()
 
     tw = time.perf_counter()
     for _ in range(args.warmup):
@@ -405,21 +440,22 @@ def run_ours(args, cfg):
                 step()
             torch.cuda.synchronize()
 
-    if dist:
-        dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         load(pad)
+        torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
         load(pad)
     ms = ev0.elapsed_time(ev1) / args.steps
+
     # per-launch device times (events between launches, same stream), for the
     # dominant kernel's roofline: median over 3 profiled sweeps
     prof = np.median(np.stack([dl.profile(x_dev.data_ptr(), B, out_dev.data_ptr())
@@ -427,38 +463,61 @@ def run_ours(args, cfg):
     if os.environ.get("ASNN_BENCH_DIAG") and rank == 0:
         pathlib.Path(os.environ["ASNN_BENCH_DIAG"]).write_text(json.dumps(
             {"launch_ms": [float(v) for v in prof], "info": info, "ms_per_step": ms}))
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        # NCCL gather of every rank's outputs (the only collective)
-        gathered = gather_rows(out_dev.view(-1, max(1, info["n_outputs"])), world)
 
-    # e2e: host (pinned) buffers through the C-ABI call, copies inside
+    # check the gathered outputs once (rank 0 holds everything after the gather)
+    step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        assert torch.equal(out_all[my_off:my_off + out_counts[rank]], out_dev[:out_counts[rank]])
+
+    # e2e: host (pinned) buffers.  One GPU: the C-ABI call with host pointers
+    # (H2D of the batch and D2H of the outputs inside the call).  N GPUs: each
+    # rank's H2D of its slice, the sweep, the in-engine gather, and rank 0's
+    # D2H of the gathered outputs.
     x_pin = torch.from_numpy(np.concatenate([x.reshape(-1) for x in Xs])).pin_memory()
-    out_pin = torch.empty(info["n_outputs"] * B, dtype=torch.float32).pin_memory()
-    dl.activate_host_ptr(x_pin.data_ptr(), B, x_pin.numel(), out_pin.data_ptr())
+    out_pin = torch.empty(max(1, sum(out_counts)), dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        if dist is None:
+            dl.activate_host_ptr(x_pin.data_ptr(), B, x_pin.numel(), out_pin.data_ptr())
+        else:
+            x_dev.copy_(x_pin, non_blocking=True)
+            step()
+            if rank == 0:
+                out_pin.copy_(out_all, non_blocking=True)
+            stream.synchronize()
+
+    e2e_step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        dl.activate_host_ptr(x_pin.data_ptr(), B, x_pin.numel(), out_pin.data_ptr())
+        e2e_step()
     e2e_s = (time.perf_counter() - t0) / args.steps
+
+    evaluated = info["edge_count"]
     if dist:
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        t = torch.tensor([ms, e2e_s, float(evaluated if cfg == "c5" else 0)], dtype=torch.float64)
+        if not one_gpu:
+            t = t.cuda()
+        red = t.clone()
+        dist.all_reduce(red, op=dist.ReduceOp.MAX)
+        ms, e2e_s = float(red[0]), float(red[1])
+        if cfg == "c5":
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            evaluated = int(t[2])
 
     E = sum(len(n.source) for n in nets)
-    conn_evals_total = E * B_total if cfg != "c5" else E * B_total
+    conn_evals_total = E * B_total
     value = conn_evals_total / (ms / 1e3)
     peak, peak_src = measured_peak()
     # level kernels: every launch but the sensor and output-gather ones
     level_ms = float(prof[1:-1].sum()) if len(prof) > 2 else float(prof.sum())
     achieved = plan["alg_bytes"] / (level_ms / 1e3) / 1e9
+    traffic = profiled_traffic(cfg)
     cb = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(nets, X, cfg, budget_s=args.cpu_budget)
     if rank == 0:
         line = {
@@ -473,20 +532,19 @@ def run_ours(args, cfg):
             "evaluated_edges": int(evaluated),
             "value_evaluated": evaluated * B_total / (ms / 1e3),
             "levels": info["total_layers"],
+            "gather": gather,
             "e2e": {"value": conn_evals_total / e2e_s, "unit": "conn_evals/s",
-                    "h2d_bytes_per_step": int(x_pin.numel() * 4 * world),
-                    "d2h_bytes_per_step": int(out_pin.numel() * 4 * world)},
+                    "h2d_bytes_per_step": int(sum(x.size for x in X) * 4),
+                    "d2h_bytes_per_step": int(sum(out_counts) * 4)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": profiled_traffic(cfg),
+                         "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
                          # what actually binds, when it is not HBM
-                         "binding": {"c4": "HBM random-row gathers (0.92 of the 256-B gather ceiling)",
-                                     "c2": "L2 throughput: gathers served from L2 (DRAM 0.46 GB of "
-                                           "20.8 GB algorithmic), so frac > 1 against HBM",
-                                     "c3": "latency: one dependent chain per layer per CTA, 2000 layers",
-                                     "c5": "FP64 sigmoid latency / layer barriers, shared-memory resident",
-                                     "c1": "latency: 10 layers in one CTA"}.get(cfg),
+                         "binding": BINDING.get(cfg),
                          "alg_bytes_per_step": plan["alg_bytes"],
+                         # measured DRAM bytes (ncu) over the same launch time: the
+                         # bandwidth the HBM actually delivered
+                         "dram_frac": (traffic / (level_ms / 1e3) / 1e9 / peak) if traffic else None,
                          # every byte read or written once (edges,
                          # row pointers, each activation written and read once)
                          "compulsory_bytes_per_step": int(8 * E + 4 * (info["node_count"] + 1) +
@@ -499,14 +557,23 @@ def run_ours(args, cfg):
                          "max_launch_ms": float(prof.max()),
                          "sweep_achieved_gbs": plan["alg_bytes"] / (ms / 1e3) / 1e9},
             "cpu_baseline": cb,
-            "gpu_launches": plan["kernels"] * args.steps,
+            "gpu_launches": (plan["kernels"] + (1 if world > 1 and not one_gpu else 0)) * args.steps,
             "clocks": dict(clk.summary(), window="timed region" if not pad else
                            f"timed region + {pad} s of untimed steps on each side"),
             "preprocess": {"wall_s": t_pre, "device_ms": pre_t, "generate_s": t_gen},
         }
         print(json.dumps(line), flush=True)
     if dist:
+        dist.barrier()
         dist.destroy_process_group()
+
+
+BINDING = {"c4": "HBM random-row gathers (0.92 of the 256-B gather ceiling)",
+           "c2": "L2 throughput: gathers served from L2 (DRAM 0.46 GB of 20.8 GB algorithmic), "
+                 "so frac > 1 against HBM",
+           "c3": "latency: one dependent chain per layer per CTA, 2000 layers",
+           "c5": "FP64 sigmoid latency / layer barriers, shared-memory resident",
+           "c1": "latency: 10 layers in one CTA"}
 
 
 def run_reference(args, cfg):
@@ -538,12 +605,19 @@ def run_reference(args, cfg):
     n_vec = max(1, min(B_total, int(0.5 / max(per_vec, 1e-9))))
     if mode == "omp-seq":
         n_vec = min(B_total, max(cpu.threads, n_vec // cpu.threads * cpu.threads))
+    # a sample shorter than ~20 ms (C1: one 10k-connection vector) is timed as
+    # the mean of `reps` back-to-back runs of it inside the step
+    _, t_sample = cpu.run(mode, n_vec)
+    reps = max(1, int(0.02 / max(t_sample, 1e-9))) if t_sample < 0.02 else 1
     times, evs = [], []
     for i in range(args.warmup + args.steps):
-        ev, dt = cpu.run(mode, n_vec)
+        ev = dt = 0.0
+        for _ in range(reps):
+            e, t = cpu.run(mode, n_vec)
+            ev, dt = ev + e, dt + t
         if i >= args.warmup:
-            times.append(dt)
-            evs.append(ev)
+            times.append(dt / reps)
+            evs.append(ev / reps)
     value = sum(evs) / sum(times)
     line = {
         "impl": "reference",
@@ -559,7 +633,9 @@ def run_reference(args, cfg):
                          "cores": 1 if mode == "seq" else cpu.threads, "mode": mode,
                          "modes": calib.get("modes"),
                          "sample": f"each step: {n_vec} of the {B_total} vectors x {cpu.n_nets} "
-                                   f"network(s) ({mode}); mode picked on a calibration run"},
+                                   f"network(s) ({mode}"
+                                   + (f", mean of {reps} back-to-back runs" if reps > 1 else "")
+                                   + "); mode picked on a calibration run"},
         "e2e": {"value": value, "unit": "conn_evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "vs_baseline": None,
@@ -607,6 +683,17 @@ def main():
                          "nothing else (for ncu launch lists; never a bench number)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not args.ncu_sweeps:
+        # one process per GPU: re-launch this command under torchrun
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", str(pathlib.Path(__file__).resolve())] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.ncu_sweeps:
         run_ncu_sweeps(args, args.config)
     elif args.impl == "reference":

@@ -230,6 +230,66 @@ int asnn_dev_sigmoid_selfcheck(asnn_dev* dev, uint64_t* mismatches, uint64_t* ex
  * DESIGN.md's latency model. */
 int asnn_dev_latency_probe(asnn_dev* dev, int which, int n, double* cycles_per_op);
 
+/* ---- multi-GPU (north_star item 4) ----------------------------
+ * A network's level-synchronous sweep does not shard without a per-level
+ * exchange; what shards is the batch (a full layout replica per device, a
+ * contiguous balanced slice of the vectors each) and a population (a
+ * contiguous balanced slice of the networks per device, all vectors each).
+ * Device g's inputs / outputs / state are contiguous slices of the caller's
+ * arrays (same layouts as asnn_dev_activate), so the one collective is an
+ * all-gather of the declared outputs in device order: ncclAllGather (equal
+ * slices) or grouped ncclBroadcast (ragged), NCCL loaded at run time; the
+ * copy engines (cudaMemcpyPeerAsync into device 0) when NCCL is absent or a
+ * device is listed twice (one-GPU functional mode). */
+typedef struct asnn_group asnn_group;               /* one process, G devices   */
+typedef struct asnn_group_layout asnn_group_layout; /* a layout sharded over them */
+
+/* Opens one asnn_dev per entry of devices[] (entries may repeat) and, when
+ * they are distinct and libnccl loads, one NCCL communicator over them
+ * (ncclCommInitAll). */
+int asnn_group_open(const int* devices, uint32_t n_devices, asnn_group** out);
+void asnn_group_close(asnn_group* group);
+const char* asnn_group_last_error(const asnn_group* group);
+/* *gather_kind: 0 single device, 1 NCCL, 2 copy engines (see _gather_note). */
+int asnn_group_info(const asnn_group* group, uint32_t* n_devices, uint32_t* gather_kind);
+const char* asnn_group_gather_note(const asnn_group* group);
+/* Member handle i (sweep options, timings); owned by the group. */
+asnn_dev* asnn_group_device(asnn_group* group, uint32_t i);
+/* Batch sharding: compute_required + segment + flatten on every device
+ * concurrently (a replica each), or a host-flattened layout uploaded to each. */
+int asnn_group_build_layout(asnn_group* group, const asnn_network_desc* net, asnn_group_layout** out);
+int asnn_group_upload_layout(asnn_group* group, const asnn_layout_desc* layout, asnn_group_layout** out);
+/* Population sharding: networks [g*P/G, (g+1)*P/G) (balanced) on device g. */
+int asnn_group_build_population(asnn_group* group, uint32_t n_networks, const asnn_network_desc* nets,
+                                asnn_group_layout** out);
+/* The member layout on device i (null for an empty population slice). */
+int asnn_group_layout_member(const asnn_group_layout* layout, uint32_t i, asnn_dev_layout** member);
+/* Device i's share of an activation of n_vec vectors: vectors it sweeps and
+ * the float offsets / counts of its inputs and outputs in the caller's arrays. */
+int asnn_group_shard(const asnn_group_layout* layout, uint32_t i, uint32_t n_vec, uint32_t* vecs,
+                     uint64_t* x_off, uint64_t* x_count, uint64_t* out_off, uint64_t* out_count);
+/* asnn_dev_activate over the group: host x / out / state in the single-device
+ * layouts; each device sweeps its slice, the outputs are all-gathered on the
+ * devices and read back from device 0; returns when all results are visible. */
+int asnn_group_activate(asnn_group_layout* layout, const float* x, uint32_t n_vec, uint64_t n_x,
+                        float* out, float* state);
+/* Resident path (the benchmark's): stage inputs on the devices once, then
+ * `repeats` sweeps + gathers; *ms = device time per repeat, max over devices. */
+int asnn_group_stage_inputs(asnn_group_layout* layout, const float* x, uint32_t n_vec, uint64_t n_x);
+int asnn_group_sweep(asnn_group_layout* layout, uint32_t repeats, float* ms);
+int asnn_group_read_outputs(asnn_group_layout* layout, float* out);
+void asnn_group_free_layout(asnn_group_layout* layout);
+
+/* One process per device (a launcher such as torchrun): rank 0 creates the
+ * 128-byte id, the launcher's store distributes it, every rank joins; then
+ * asnn_dev_allgather enqueues the output all-gather on the handle's stream
+ * (stream-ordered after the sweep, no synchronisation).  counts[n_ranks]:
+ * floats each rank contributes; recv = their concatenation in rank order;
+ * send may lie inside recv at this rank's offset (in place). */
+int asnn_comm_unique_id(uint8_t* id128);
+int asnn_dev_comm_init(asnn_dev* dev, const uint8_t* id128, int n_ranks, int rank);
+int asnn_dev_allgather(asnn_dev* dev, const float* send_dev, float* recv_dev, const uint64_t* counts);
+
 typedef struct asnn_corpus asnn_corpus;
 
 /* ---- loading (io.hpp:23-31) on the device ---------------------------------

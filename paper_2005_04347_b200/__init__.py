@@ -6,7 +6,8 @@ include/asnn_dev.h); this package is the host-side mirror of the reference
 API (see api.py) plus ctypes plumbing.
 """
 from .api import (  # noqa: F401
-    ActivationState, Backend, BackendUnavailable, Device, DeviceError, DeviceLayout, GenSpec,
+    ActivationState, Backend, BackendUnavailable, Device, DeviceError, DeviceGroup, DeviceLayout,
+    GenSpec, GroupLayout, comm_unique_id,
     InfeasibleSpec, InputArityMismatch, IoError, LayerAssignment, LayeredLayout, LayerOutOfRange,
     Network, OutputUnreachable, ParallelConfig, ParseError, RequiredSet, SplitMix64, UnassignedOutput,
     ValidationError, compute_required, normalize, parse_network, read_network, validate,

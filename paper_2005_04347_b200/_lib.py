@@ -113,6 +113,26 @@ PROTOTYPES = {
     "asnn_dev_normalize": (C.c_int, [C.c_void_p, C.POINTER(NetworkDesc), C.POINTER(C.c_void_p)]),
     "asnn_dev_read_network": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p), u32p]),
     "asnn_dev_parse_weights": (C.c_int, [C.c_void_p, C.c_char_p, u64p, C.c_uint64, f32p, u8p]),
+    "asnn_group_open": (C.c_int, [C.POINTER(C.c_int), C.c_uint32, C.POINTER(C.c_void_p)]),
+    "asnn_group_close": (None, [C.c_void_p]),
+    "asnn_group_last_error": (C.c_char_p, [C.c_void_p]),
+    "asnn_group_info": (C.c_int, [C.c_void_p, u32p, u32p]),
+    "asnn_group_gather_note": (C.c_char_p, [C.c_void_p]),
+    "asnn_group_device": (C.c_void_p, [C.c_void_p, C.c_uint32]),
+    "asnn_group_build_layout": (C.c_int, [C.c_void_p, C.POINTER(NetworkDesc), C.POINTER(C.c_void_p)]),
+    "asnn_group_upload_layout": (C.c_int, [C.c_void_p, C.POINTER(LayoutDesc), C.POINTER(C.c_void_p)]),
+    "asnn_group_build_population": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(NetworkDesc),
+                                              C.POINTER(C.c_void_p)]),
+    "asnn_group_layout_member": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "asnn_group_shard": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, u32p, u64p, u64p, u64p, u64p]),
+    "asnn_group_activate": (C.c_int, [C.c_void_p, f32p, C.c_uint32, C.c_uint64, f32p, f32p]),
+    "asnn_group_stage_inputs": (C.c_int, [C.c_void_p, f32p, C.c_uint32, C.c_uint64]),
+    "asnn_group_sweep": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_float)]),
+    "asnn_group_read_outputs": (C.c_int, [C.c_void_p, f32p]),
+    "asnn_group_free_layout": (None, [C.c_void_p]),
+    "asnn_comm_unique_id": (C.c_int, [u8p]),
+    "asnn_dev_comm_init": (C.c_int, [C.c_void_p, u8p, C.c_int, C.c_int]),
+    "asnn_dev_allgather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, u64p]),
     "asnn_corpus_desc": (C.c_int, [C.c_void_p, C.POINTER(NetworkDesc)]),
     "asnn_corpus_free": (None, [C.c_void_p]),
 }

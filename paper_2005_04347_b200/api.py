@@ -528,6 +528,176 @@ class DeviceLayout:
             self.h, C.c_void_p(x_ptr), n_vec, C.c_void_p(out_ptr)))
 
 
+class DeviceGroup:
+    """One process driving several GPUs (asnn_group, csrc/group.cu): batch
+    sharding over layout replicas, population sharding over network slices,
+    the declared outputs all-gathered on the devices (NCCL, or the copy
+    engines when a device is listed twice / NCCL is absent)."""
+
+    GATHER = {0: "single device", 1: "nccl", 2: "copy engines"}
+
+    def __init__(self, devices: Sequence[int]):
+        self.lib = _lib.load()
+        ids = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        rc = self.lib.asnn_group_open(ids, len(devices), C.byref(h))
+        if rc:
+            _raise(rc, f"cannot open devices {list(devices)}")
+        self.h = h
+        self.devices = list(devices)
+
+    def check(self, rc: int):
+        if rc:
+            _raise(rc, (self.lib.asnn_group_last_error(self.h) or b"").decode())
+
+    @property
+    def gather(self) -> str:
+        n, k = C.c_uint32(), C.c_uint32()
+        self.check(self.lib.asnn_group_info(self.h, C.byref(n), C.byref(k)))
+        return self.GATHER[k.value]
+
+    @property
+    def gather_note(self) -> str:
+        return (self.lib.asnn_group_gather_note(self.h) or b"").decode()
+
+    def set_sweep_mode(self, mode: int):
+        for i in range(len(self.devices)):
+            self.lib.asnn_dev_set_sweep_mode(self.lib.asnn_group_device(self.h, i), int(mode))
+
+    def layout(self, net: Network) -> "GroupLayout":
+        h = C.c_void_p()
+        d = net.desc()
+        self.check(self.lib.asnn_group_build_layout(self.h, C.byref(d), C.byref(h)))
+        return GroupLayout(self, h, [net])
+
+    def upload(self, layout: LayeredLayout) -> "GroupLayout":
+        h = C.c_void_p()
+        d = layout.desc()
+        self.check(self.lib.asnn_group_upload_layout(self.h, C.byref(d), C.byref(h)))
+        return GroupLayout(self, h, None)
+
+    def population(self, nets: Sequence[Network]) -> "GroupLayout":
+        descs = (_lib.NetworkDesc * len(nets))(*[n.desc() for n in nets])
+        h = C.c_void_p()
+        self.check(self.lib.asnn_group_build_population(self.h, len(nets), descs, C.byref(h)))
+        return GroupLayout(self, h, list(nets), population=True)
+
+    def close(self):
+        if self.h:
+            self.lib.asnn_group_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class GroupLayout:
+    """A layout sharded over a DeviceGroup (asnn_group_layout)."""
+
+    def __init__(self, grp: DeviceGroup, h, nets, population: bool = False):
+        self.grp, self.h, self.nets, self.population = grp, h, nets, population
+        self._staged = 0
+
+    def _totals(self):
+        m = C.c_void_p()
+        n_in = n_out = idb = 0
+        for i in range(len(self.grp.devices)):
+            self.grp.check(self.grp.lib.asnn_group_layout_member(self.h, i, C.byref(m)))
+            if not m.value:
+                continue
+            inf = _lib.LayoutInfo()
+            self.grp.check(self.grp.lib.asnn_dev_layout_info(m, C.byref(inf)))
+            if not self.population:
+                return inf.n_inputs, inf.n_outputs, inf.id_bound
+            n_in, n_out, idb = n_in + inf.n_inputs, n_out + inf.n_outputs, idb + inf.id_bound
+        return n_in, n_out, idb
+
+    def shard(self, i: int, n_vec: int) -> dict:
+        v = C.c_uint32()
+        xo, xc, oo, oc = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self.grp.check(self.grp.lib.asnn_group_shard(self.h, i, n_vec, C.byref(v), C.byref(xo),
+                                                     C.byref(xc), C.byref(oo), C.byref(oc)))
+        return dict(vecs=v.value, x_off=xo.value, x_count=xc.value, out_off=oo.value,
+                    out_count=oc.value)
+
+    def activate(self, X: np.ndarray, n_vec: Optional[int] = None, state: bool = False):
+        """Like DeviceLayout.activate: (out, state) over the whole batch /
+        population, computed across the group's devices."""
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        if n_vec is None:
+            X = X[None, :] if X.ndim == 1 else X
+            n_vec = X.shape[0]
+        n_in, n_out, idb = self._totals()
+        out = np.empty(n_vec * n_out, np.float32)
+        st = np.empty(n_vec * idb, np.float32) if state else None
+        self.grp.check(self.grp.lib.asnn_group_activate(
+            self.h, _lib.ptr(X, C.c_float), n_vec, X.size, _lib.ptr(out, C.c_float),
+            _lib.ptr(st, C.c_float)))
+        if not self.population:
+            out = out.reshape(n_vec, n_out)
+            st = st.reshape(n_vec, idb) if st is not None else None
+        return out, st
+
+    def stage(self, X: np.ndarray, n_vec: int):
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        self.grp.check(self.grp.lib.asnn_group_stage_inputs(self.h, _lib.ptr(X, C.c_float), n_vec,
+                                                            X.size))
+        self._staged = n_vec
+
+    def sweep(self, repeats: int = 1) -> float:
+        """Resident sweeps + gathers of the staged batch: device ms per sweep
+        (max over the group's devices)."""
+        ms = C.c_float()
+        self.grp.check(self.grp.lib.asnn_group_sweep(self.h, repeats, C.byref(ms)))
+        return ms.value
+
+    def read_outputs(self) -> np.ndarray:
+        _, n_out, _ = self._totals()
+        out = np.empty(self._staged * n_out, np.float32)
+        self.grp.check(self.grp.lib.asnn_group_read_outputs(self.h, _lib.ptr(out, C.c_float)))
+        return out
+
+    def free(self):
+        if self.h:
+            self.grp.lib.asnn_group_free_layout(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def comm_unique_id() -> bytes:
+    """128-byte NCCL id for a one-process-per-GPU job (rank 0 makes it, the
+    launcher's store distributes it; Device.comm_init joins)."""
+    buf = (C.c_uint8 * 128)()
+    rc = _lib.load().asnn_comm_unique_id(buf)
+    if rc:
+        _raise(rc, "NCCL is not available")
+    return bytes(buf)
+
+
+def _device_comm_init(self, uid: bytes, n_ranks: int, rank: int):
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    self.check(self.lib.asnn_dev_comm_init(self.h, buf, n_ranks, rank))
+
+
+def _device_allgather(self, send_ptr: int, recv_ptr: int, counts: Sequence[int]):
+    """Stream-ordered all-gather of float slices (counts per rank, rank order)."""
+    c = np.ascontiguousarray(counts, dtype=np.uint64)
+    self.check(self.lib.asnn_dev_allgather(self.h, C.c_void_p(send_ptr), C.c_void_p(recv_ptr),
+                                           _lib.ptr(c, C.c_uint64)))
+
+
+Device.comm_init = _device_comm_init
+Device.allgather = _device_allgather
+
+
 def flatten(net: Network, assignment: Optional[LayerAssignment] = None,
             device: int = 0) -> LayeredLayout:
     """layout.cpp:12-83 on the GPU.  The device layout is rebuilt from the

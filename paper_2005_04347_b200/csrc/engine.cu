@@ -1330,6 +1330,7 @@ void asnn_dev_close(asnn_dev* dev) {
     if (!dev) return;
     cudaSetDevice(dev->device);
     cudaStreamSynchronize(dev->stream);
+    release_comm(dev);
     for (cudaEvent_t ev : {dev->ev0, dev->ev1, dev->ev2, dev->ev3, dev->ev4, dev->stage_ev[0], dev->stage_ev[1]})
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : dev->fork_ev) cudaEventDestroy(ev);
@@ -1631,6 +1632,21 @@ int asnn_dev_activate_device(asnn_dev_layout* L, const float* x_dev, uint32_t n_
     CK(cudaSetDevice(dev->device));
     return run_sweep(L, x_dev, n_vec, out_dev, nullptr);
 }
+
+}  // extern "C"
+
+int asnn_b200::enqueue_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_vec, float* out_dev,
+                             float* state_dev) {
+    if (!L) return ASNN_E_INVALID;
+    asnn_dev* dev = L->dev;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    asnn_b200::AllocStream alloc_on(dev->stream);
+    if (n_vec == 0) return ASNN_OK;
+    CK(cudaSetDevice(dev->device));
+    return run_sweep(L, x_dev, n_vec, out_dev, state_dev);
+}
+
+extern "C" {
 
 // eval_parallel(DeviceCompute) + read_outputs over a batch of host vectors.
 int asnn_dev_activate(asnn_dev_layout* L, const float* x, uint32_t n_vec, uint64_t n_x, float* out,

@@ -137,6 +137,10 @@ struct asnn_dev {
     asnn_b200::PinnedBuf pin_x, pin_out;  // pinned staging of pageable host buffers (all layouts)
     asnn_b200::PinnedBuf stage[2];        // double-buffered staging of large pageable transfers
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+    // NCCL communicator this device belongs to (group.cu): one rank of a
+    // multi-process job (asnn_dev_comm_init) or a member of an asnn_group
+    void* comm = nullptr;
+    int comm_rank = 0, comm_size = 1;
 };
 
 namespace asnn_b200 {
@@ -270,6 +274,14 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
 int build_device_network(asnn_dev* dev, DevBuf<uint32_t>&& nodes, uint32_t N, DevBuf<uint32_t>&& src,
                          DevBuf<uint32_t>&& dst, DevBuf<float>&& w, uint64_t E, std::vector<uint32_t>&& inputs,
                          std::vector<uint32_t>&& outputs, asnn_dev_layout** out);
+
+// One activation sweep of a resident layout enqueued on the handle's stream
+// (graph-cached; no synchronisation): x_dev [n_vec][inputs], out_dev
+// [n_vec][outputs] (may be null), state_dev [n_vec][id_bound] (may be null).
+int enqueue_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_vec, float* out_dev, float* state_dev);
+
+// Destroys the handle's NCCL communicator, if any (group.cu).
+void release_comm(asnn_dev* dev);
 
 // validate's cycle test on device arrays (preprocess.cu): nodes sorted unique,
 // connections as (src, dst) ids.

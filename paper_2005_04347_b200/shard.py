@@ -5,12 +5,17 @@ exchange, so the engine shards what is independent:
 
 * batch sharding -- every rank holds a full layout replica and activates a
   contiguous slice of the input vectors; no traffic during the sweep;
-* population sharding -- networks are dealt round-robin to ranks, each keeps
-  its own vectors.
+* population sharding -- a contiguous, balanced slice of the networks per
+  rank, each network with all of its vectors (so the gathered outputs are in
+  population order).
 
-The only collective is the final gather of the declared outputs
-(torch.distributed all_gather: NCCL over NVLink on GPUs, gloo in the CPU
-tests).  One process per GPU; ranks and world size come from the launcher.
+The only collective is the final gather of the declared outputs.  Inside
+the engine (csrc/group.cu) it is an NCCL all-gather on the engine's stream
+(asnn_dev_comm_init / asnn_dev_allgather for one process per GPU,
+asnn_group_* for one process driving several); gather_rows below is the
+torch.distributed form used by the CPU (gloo) tests and by the one-GPU
+functional mode, where NCCL cannot put two ranks on one device.  The
+partition functions here and group.cu's `balanced` are the same rule.
 """
 from __future__ import annotations
 
@@ -28,8 +33,10 @@ def batch_slice(n_vec: int, world: int, rank: int) -> Tuple[int, int]:
 
 
 def population_shard(n_networks: int, world: int, rank: int) -> List[int]:
-    """Indices of the networks rank `rank` owns (round-robin)."""
-    return list(range(rank, n_networks, world))
+    """Indices of the networks rank `rank` owns: a contiguous balanced slice
+    (asnn_group_build_population's partition)."""
+    lo, hi = batch_slice(n_networks, world, rank)
+    return list(range(lo, hi))
 
 
 def gather_rows(local, world: int, group=None):

@@ -515,7 +515,8 @@ def run_ours(args, cfg):
     # level kernels: every launch but the sensor and output-gather ones
     level_ms = float(prof[1:-1].sum()) if len(prof) > 2 else float(prof.sum())
     achieved = plan["alg_bytes"] / (level_ms / 1e3) / 1e9
-    traffic = profiled_traffic(cfg)
+    # the committed ncu figure is for the full-size, one-GPU sweep only
+    traffic = profiled_traffic(cfg) if args.scale == 1.0 and world == 1 and not args.shard_of else None
     cb = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(nets, X, cfg, budget_s=args.cpu_budget)

@@ -389,6 +389,85 @@ private:
     asnn_layout_info info_{};
 };
 
+// Multi-GPU (csrc/group.cu): one process driving several
+// devices.  Batch sharding: a layout replica per device, each sweeps a
+// contiguous slice of the vectors; population sharding: a contiguous slice of
+// the networks per device.  The declared outputs are all-gathered on the
+// devices (NCCL, or the copy engines when a device is listed twice).
+class DeviceGroup {
+public:
+    explicit DeviceGroup(const std::vector<int>& devices) {
+        const int rc = asnn_group_open(devices.data(), static_cast<std::uint32_t>(devices.size()), &g_);
+        if (rc) detail::raise(rc, nullptr);
+    }
+    DeviceGroup(const DeviceGroup&) = delete;
+    DeviceGroup& operator=(const DeviceGroup&) = delete;
+    ~DeviceGroup() { asnn_group_close(g_); }
+    asnn_group* handle() const { return g_; }
+    // "single device", "nccl" or "copy engines"
+    std::string gather() const {
+        std::uint32_t n = 0, k = 0;
+        asnn_group_info(g_, &n, &k);
+        return k == 1 ? "nccl" : k == 2 ? "copy engines" : "single device";
+    }
+    void check(int rc) const {
+        if (!rc) return;
+        const std::string msg = asnn_group_last_error(g_);
+        switch (rc) {
+            case ASNN_E_ARITY: throw InputArityMismatch(msg);
+            case ASNN_E_UNASSIGNED_OUTPUT: throw OutputUnreachable(msg);
+            case ASNN_E_UNAVAILABLE: throw BackendUnavailable(msg);
+            case ASNN_E_INVALID: throw std::invalid_argument(msg);
+            default: throw DeviceError(msg);
+        }
+    }
+
+private:
+    asnn_group* g_ = nullptr;
+};
+
+class GroupNetwork {
+public:
+    // batch sharding of one network
+    GroupNetwork(DeviceGroup& grp, const Network& net) : grp_(grp) {
+        detail::NetView v(net);
+        grp_.check(asnn_group_build_layout(grp_.handle(), &v.d, &h_));
+        n_in_ = static_cast<std::uint32_t>(net.inputs.size());
+        n_out_ = static_cast<std::uint32_t>(net.outputs.size());
+    }
+    // population sharding
+    GroupNetwork(DeviceGroup& grp, const std::vector<Network>& nets) : grp_(grp), population_(true) {
+        std::vector<detail::NetView> views;
+        views.reserve(nets.size());
+        std::vector<asnn_network_desc> d;
+        for (const auto& n : nets) {
+            views.emplace_back(n);
+            d.push_back(views.back().d);
+            n_in_ += static_cast<std::uint32_t>(n.inputs.size());
+            n_out_ += static_cast<std::uint32_t>(n.outputs.size());
+        }
+        grp_.check(asnn_group_build_population(grp_.handle(), static_cast<std::uint32_t>(nets.size()),
+                                               d.data(), &h_));
+    }
+    GroupNetwork(const GroupNetwork&) = delete;
+    GroupNetwork& operator=(const GroupNetwork&) = delete;
+    ~GroupNetwork() { asnn_group_free_layout(h_); }
+
+    // X: n_vec vectors per network (networks concatenated for a population);
+    // returns the declared outputs, [n_vec][n_outputs] per network.
+    std::vector<float> activate(std::span<const float> X, std::uint32_t n_vec) {
+        std::vector<float> out(static_cast<std::size_t>(n_vec) * n_out_);
+        grp_.check(asnn_group_activate(h_, X.data(), n_vec, X.size(), out.data(), nullptr));
+        return out;
+    }
+
+private:
+    DeviceGroup& grp_;
+    bool population_ = false;
+    asnn_group_layout* h_ = nullptr;
+    std::uint32_t n_in_ = 0, n_out_ = 0;
+};
+
 // layout.cpp:12-83.  The assignment must be segment()'s for this network
 // (the device rebuilds it); UnassignedOutput when an output has no layer.
 inline LayeredLayout flatten(const Network& net, const LayerAssignment& assignment) {

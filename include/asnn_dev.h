@@ -215,6 +215,15 @@ int asnn_dev_activate_plan(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* ke
  * batch slice) for the whole sweep (k_cta). */
 int asnn_dev_sweep_kind(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* kind);
 
+/* Debug: one sweep of n_vec (zero) vectors counting how often each op slot
+ * is produced; counts[position][n_vec] (positions in level order, as
+ * asnn_dev_layout_download's node_ids).  Every entry must be 1 -- "each slot
+ * written exactly once" (proj/tests/test_eval.cpp:199-213).
+ * Only the write-count build (build/debug/libasnn_b200_wc.so, make -C
+ * paper_2005_04347_b200/csrc wc) counts; the product library returns
+ * ASNN_E_UNAVAILABLE. */
+int asnn_dev_debug_write_counts(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* counts);
+
 /* The device's sigmoid32 (network.hpp:54-59) over n host floats, for
  * exhaustive parity checks of the epilogue. */
 int asnn_dev_sigmoid32(asnn_dev* dev, const float* x, float* y, uint64_t n);

@@ -98,6 +98,7 @@ PROTOTYPES = {
     "asnn_dev_activate_plan": (C.c_int, [C.c_void_p, C.c_uint32, u32p, u64p, u64p]),
     "asnn_dev_profile_sweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, f32p, u32p]),
     "asnn_dev_sweep_kind": (C.c_int, [C.c_void_p, C.c_uint32, u32p]),
+    "asnn_dev_debug_write_counts": (C.c_int, [C.c_void_p, C.c_uint32, u32p]),
     "asnn_dev_sigmoid_selfcheck": (C.c_int, [C.c_void_p, u64p, u64p]),
     "asnn_dev_sigmoid32": (C.c_int, [C.c_void_p, f32p, f32p, C.c_uint64]),
     "asnn_dev_latency_probe": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]),

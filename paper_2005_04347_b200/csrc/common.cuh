@@ -201,6 +201,25 @@ __device__ __forceinline__ void load_cols_cg(float (&r)[V], const float* p) {
     }
 }
 
+// Debug write-count mode (build flag ASNN_WRITE_COUNT, libasnn_b200_wc.so):
+// every producer of an activation value -- the op slot of eval.cpp:16-23,
+// in A or in K-cta's shared-memory rows -- adds 1 to g_wc[pos][col], so a
+// test can assert that each slot is written exactly once per sweep
+// (proj/tests/test_eval.cpp:199-213), segmented heavy rows
+// included.  The normal build compiles the notes away.
+#ifdef ASNN_WRITE_COUNT
+static __device__ uint32_t* g_wc = nullptr;
+static __device__ uint32_t g_wc_ld = 0;
+#endif
+__device__ __forceinline__ void wc_note(uint32_t pos, uint32_t col, int n) {
+#ifdef ASNN_WRITE_COUNT
+    if (g_wc)
+        for (int v = 0; v < n; ++v) atomicAdd(&g_wc[static_cast<uint64_t>(pos) * g_wc_ld + col + v], 1u);
+#else
+    (void)pos, (void)col, (void)n;
+#endif
+}
+
 template <int V>
 __device__ __forceinline__ void store_cols(float* p, const float (&r)[V]) {
     if constexpr (V == 1) {

@@ -126,6 +126,7 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
         }
         float* dst = As + static_cast<size_t>(pos_base - row_base + a + i) * ld + q * V;
         sigmoid32_v<V>(acc);
+        wc_note(pos_base + a + i, blockIdx.x * ((groups_mask + 1) * V) + q * V, V);
         if constexpr (V == 4) {
             *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
         } else {
@@ -287,6 +288,7 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
             if (col < n_vec && k != kUnassigned)
                 xv = x[static_cast<uint64_t>(n_vec) * n.in_prefix + static_cast<uint64_t>(col) * n.n_in + k];
             As[static_cast<size_t>(n.pos_base - row_base + s) * ld + c] = sigmoid32(xv);
+            wc_note(n.pos_base + s, col, 1);
         }
         consumer_barrier(Tc);
         const uint32_t* ring_u32 = reinterpret_cast<const uint32_t*>(ring);

@@ -1648,6 +1648,42 @@ int asnn_b200::enqueue_sweep(asnn_dev_layout* L, const float* x_dev, uint32_t n_
 
 extern "C" {
 
+// Debug write-count sweep (ASNN_WRITE_COUNT builds only): counts[p][b] = how
+// many times op slot (position p, column b < n_vec) was produced in one sweep.
+int asnn_dev_debug_write_counts(asnn_dev_layout* L, uint32_t n_vec, uint32_t* counts) {
+    if (!L || !counts || n_vec == 0) return ASNN_E_INVALID;
+    asnn_dev* dev = L->dev;
+#ifndef ASNN_WRITE_COUNT
+    return fail(dev, ASNN_E_UNAVAILABLE, "built without ASNN_WRITE_COUNT (make -C csrc wc)");
+#else
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    CK(cudaSetDevice(dev->device));
+    int rc = ensure_workspace(L, n_vec);
+    if (rc) return rc;
+    const uint32_t ldA = padded_batch(n_vec);
+    const size_t n = (static_cast<size_t>(L->total_pos) + 1) * ldA;
+    DevBuf<uint32_t> wc;
+    DevBuf<float> x;
+    CK(wc.alloc(n));
+    CK(x.alloc(static_cast<size_t>(L->total_in) * n_vec + 1));
+    CK(cudaMemset(wc.p, 0, n * 4));
+    CK(cudaMemset(x.p, 0, (static_cast<size_t>(L->total_in) * n_vec + 1) * 4));
+    CK(cudaMemcpyToSymbol(g_wc, &wc.p, sizeof(wc.p)));
+    CK(cudaMemcpyToSymbol(g_wc_ld, &ldA, sizeof(ldA)));
+    CK(cudaStreamSynchronize(dev->stream));
+    rc = launch_sweep(L, x.p, n_vec, nullptr, nullptr, dev->stream);
+    CK(cudaStreamSynchronize(dev->stream));
+    uint32_t* null_wc = nullptr;
+    CK(cudaMemcpyToSymbol(g_wc, &null_wc, sizeof(null_wc)));
+    if (rc) return rc;
+    std::vector<uint32_t> h(n);
+    CK(cudaMemcpy(h.data(), wc.p, n * 4, cudaMemcpyDeviceToHost));
+    for (size_t p = 0; p < L->total_pos; ++p)
+        std::memcpy(counts + p * n_vec, h.data() + p * ldA, n_vec * 4);
+    return ASNN_OK;
+#endif
+}
+
 // eval_parallel(DeviceCompute) + read_outputs over a batch of host vectors.
 int asnn_dev_activate(asnn_dev_layout* L, const float* x, uint32_t n_vec, uint64_t n_x, float* out,
                       float* state) {

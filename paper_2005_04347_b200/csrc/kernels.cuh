@@ -38,6 +38,7 @@ __global__ void k_sense(const uint4* __restrict__ sinfo, uint32_t n_sensors,
     if (b < n_vec && si.w != kUnassigned)
         xv = x[static_cast<uint64_t>(n_vec) * si.y + static_cast<uint64_t>(b) * si.z + si.w];
     A[static_cast<uint64_t>(si.x) * ldA + b] = sigmoid32(xv);
+    wc_note(si.x, b, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -125,6 +126,7 @@ k_level(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
     }
     sigmoid32_v<V>(acc);
     store_cols<V>(A + static_cast<uint64_t>(node) * ldA + col, acc);
+    wc_note(node, col, V);
 }
 
 // ---------------------------------------------------------------------------
@@ -215,6 +217,7 @@ k_rows(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ldA,
         float o[4] = {a0, a1, a2, a3};
         sigmoid32_v<4>(o);
         *reinterpret_cast<float4*>(A + static_cast<uint64_t>(node) * ldA + col) = make_float4(o[0], o[1], o[2], o[3]);
+        wc_note(node, col, 4);
     }
 }
 
@@ -254,7 +257,10 @@ k_warp_rows(const uint2* __restrict__ edges, float* __restrict__ A, const uint4*
         }
         p = pn;
     }
-    if (lane == 0) A[t.x] = sigmoid32(acc);
+    if (lane == 0) {
+        A[t.x] = sigmoid32(acc);
+        wc_note(t.x, 0, 1);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -327,6 +333,7 @@ k_warp_rows4(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ld
         sigmoid32_v<4>(acc);
         *reinterpret_cast<float4*>(A + static_cast<uint64_t>(t.x) * ldA + col) =
             make_float4(acc[0], acc[1], acc[2], acc[3]);
+        wc_note(t.x, col, 4);
     }
 }
 
@@ -480,7 +487,10 @@ k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, f
         }
         if (col < TC) {
             if (aux & kAccStore) accbuf[static_cast<uint64_t>(aux & kSlotMask) * ldA + tile * TC + col] = acc;
-            else A[static_cast<uint64_t>(node) * ldA + tile * TC + col] = sigmoid32(acc);
+            else {
+                A[static_cast<uint64_t>(node) * ldA + tile * TC + col] = sigmoid32(acc);
+                wc_note(node, tile * TC + col, 1);
+            }
         }
     }
 }

@@ -194,6 +194,61 @@ static void random_vs_oracle() {
     }
 }
 
+// Multi-GPU through the facade (csrc/group.cu): a 2-device group over device 0
+// (the copy-engine gather; one B200 in the test box) shards a batch and a
+// population; results equal the single-device activation bit for bit.
+static Network random_net(std::mt19937_64& rng, uint32_t n, uint32_t n_in, uint32_t n_out) {
+    std::vector<Connection> conns;
+    for (uint32_t t = n_in; t < n; ++t) {
+        const uint32_t k = 1 + rng() % 6;
+        for (uint32_t j = 0; j < k; ++j)
+            conns.push_back({static_cast<NodeId>(rng() % t), t, std::uniform_real_distribution<float>(-1.5f, 1.5f)(rng)});
+    }
+    std::sort(conns.begin(), conns.end(), [](const Connection& a, const Connection& b) {
+        return a.target != b.target ? a.target < b.target : a.source < b.source;
+    });
+    conns.erase(std::unique(conns.begin(), conns.end(),
+                            [](const Connection& a, const Connection& b) {
+                                return a.source == b.source && a.target == b.target;
+                            }),
+                conns.end());
+    std::vector<NodeId> inputs(n_in), outputs;
+    for (uint32_t i = 0; i < n_in; ++i) inputs[i] = i;
+    for (uint32_t i = 0; i < n_out; ++i) outputs.push_back(n - 1 - i);
+    return make_network(inputs, outputs, conns);
+}
+
+static void group_cases() {
+    std::mt19937_64 rng(99);
+    DeviceGroup grp({0, 0});
+    CHECK(grp.gather() == "copy engines");
+    const Network net = random_net(rng, 600, 5, 3);
+    for (uint32_t B : {1u, 7u, 64u}) {
+        std::vector<float> X(static_cast<size_t>(B) * 5);
+        for (auto& v : X) v = std::uniform_real_distribution<float>(-2.0f, 2.0f)(rng);
+        GroupNetwork gn(grp, net);
+        DeviceNetwork dn(net);
+        const auto a = gn.activate(X, B), b = dn.activate(X, B);
+        CHECK(a.size() == b.size() && std::memcmp(a.data(), b.data(), a.size() * 4) == 0);
+    }
+    std::vector<Network> pop;
+    for (int k = 0; k < 9; ++k) pop.push_back(random_net(rng, 80 + k * 7, 4, 2));
+    const uint32_t V = 5;
+    std::vector<float> X;
+    for (size_t k = 0; k < pop.size() * V * 4; ++k) X.push_back(std::uniform_real_distribution<float>(-2.0f, 2.0f)(rng));
+    GroupNetwork gp(grp, pop);
+    const auto all = gp.activate(X, V);
+    CHECK(all.size() == pop.size() * V * 2);
+    bool same = true;
+    for (size_t k = 0; k < pop.size(); ++k) {
+        DeviceNetwork dn(pop[k]);
+        const auto o = dn.activate(std::span<const float>(X.data() + k * V * 4, V * 4), V);
+        same &= std::memcmp(o.data(), all.data() + k * V * 2, o.size() * 4) == 0;
+    }
+    CHECK(same);
+    CHECK_THROWS_AS(gp.activate(std::span<const float>(X.data(), X.size() - 1), V), InputArityMismatch);
+}
+
 // io.hpp through the facade: the test_io.cpp scenarios of the reference
 // (round trip, comments / blank lines / CRLF, ParseError line numbers,
 // ValidationError messages, IoError).
@@ -248,6 +303,7 @@ int main() {
         layout_cases();
         eval_cases();
         random_vs_oracle();
+        group_cases();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "uncaught exception: %s\n", e.what());
         return 2;

@@ -24,10 +24,12 @@ def refdev():
 
 
 def test_verify_recipe_through_reference_types(refdev):
+    """The acceptance criterion (acceptance.cpp:72-85): 200
+    trials of the verify recipe, 100..50,000 connections, seed 20260810."""
     master = A.SplitMix64(20260810)
     n_vals = n_eq = 0
     max_div = 0.0
-    for trial in range(60):
+    for trial in range(200):
         net_seed = master.next()
         rng = A.SplitMix64(net_seed)
         conn = 100 + rng.bounded(50000 - 100 + 1)
@@ -70,3 +72,39 @@ def test_reference_host_backends_untouched(refdev):
         _, seq = rn.eval_sequential(x)
         rc, par = rn.eval_parallel(x, workers=2, backend=0)
         assert rc == 0 and np.array_equal(seq.view(np.uint32), par.view(np.uint32))
+
+
+def test_concurrent_callers_through_the_binding(refdev):
+    """SPEC.md:331-332 through the drop-in: eval_parallel(DeviceCompute) from
+    several host threads at once -- distinct layouts, and one immutable layout
+    with distinct input vectors -- each result bitwise the reference's
+    eval_sequential on the same call."""
+    import threading
+    rng = A.SplitMix64(331)
+    nets = [refdev.generate(A.random_spec(rng, 2000, 20000)) for _ in range(4)]
+    for rn in nets:
+        assert rn.preprocess() == 0
+    n_ins = [len(rn.layout()["input_order"]) for rn in nets]
+    errors = []
+
+    def worker(t, shared):
+        try:
+            r = np.random.default_rng(t)
+            for it in range(25):
+                k = 0 if shared else t
+                rn = nets[k]
+                x = r.uniform(-2, 2, n_ins[k]).astype(np.float32)
+                rc, dev = refdev.eval_device(rn, x)
+                _, seq = rn.eval_sequential(x)
+                if rc != 0 or not np.array_equal(dev.view(np.uint32), seq.view(np.uint32)):
+                    errors.append((t, it, rc))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append((t, repr(e)))
+
+    for shared in (False, True):
+        th = [threading.Thread(target=worker, args=(t, shared)) for t in range(4)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+    assert errors == []

@@ -134,8 +134,11 @@ int asnn_dev_set_heavy_threshold(asnn_dev* dev, uint32_t min_in_degree);
  * 128, heavy rows are split into segments that run in the levels of their
  * sources), 2 = one CTA per (network, batch slice) running every level with
  * shared-memory-resident activations whenever they fit, 3 = one launch per
- * level with whole rows only.  Also a scheduling knob: results are
- * identical. */
+ * level with whole rows only, 4 = (one network) one CTA per batch column
+ * keeping only a ring of the newest positions in shared memory and older
+ * sources in HBM/L2, with the smallest legal ring (the windowed K-cta the
+ * automatic choice uses for deep networks too large for one wave; forced
+ * here to exercise it).  Also a scheduling knob: results are identical. */
 int asnn_dev_set_sweep_mode(asnn_dev* dev, uint32_t mode);
 int asnn_dev_last_timings(const asnn_dev* dev, asnn_timings* out);
 
@@ -348,6 +351,22 @@ uint64_t asnn_gen_max_connections(uint32_t input_count, uint32_t output_count,
 int asnn_gen_mlp(uint32_t layers, uint32_t width, double p, uint64_t seed, asnn_corpus** out);
 int asnn_gen_powerlaw(uint32_t n_nodes, uint32_t bands, uint32_t n_inputs, uint32_t n_outputs,
                       uint64_t target_edges, double alpha, uint64_t seed, asnn_corpus** out);
+/* The same two bench shapes generated on the device (gen.cu; counter-based
+ * per node, byte-identical to asnn_gen_mlp / asnn_gen_powerlaw): into a host
+ * corpus, or straight into a resident layout (compute_required + segment +
+ * flatten on the generated device arrays; the network never crosses the
+ * host link).  SURVEY.md 8f rank 4; the reference's generate()
+ * (netgen.cpp:71-157) cannot make these shapes at this scale. */
+int asnn_dev_gen_mlp(asnn_dev* dev, uint32_t layers, uint32_t width, double p, uint64_t seed,
+                     asnn_corpus** out);
+int asnn_dev_gen_mlp_layout(asnn_dev* dev, uint32_t layers, uint32_t width, double p, uint64_t seed,
+                            asnn_dev_layout** out);
+int asnn_dev_gen_powerlaw(asnn_dev* dev, uint32_t n_nodes, uint32_t bands, uint32_t n_inputs,
+                          uint32_t n_outputs, uint64_t target_edges, double alpha, uint64_t seed,
+                          asnn_corpus** out);
+int asnn_dev_gen_powerlaw_layout(asnn_dev* dev, uint32_t n_nodes, uint32_t bands, uint32_t n_inputs,
+                                 uint32_t n_outputs, uint64_t target_edges, double alpha, uint64_t seed,
+                                 asnn_dev_layout** out);
 int asnn_corpus_desc(const asnn_corpus* corpus, asnn_network_desc* desc);
 void asnn_corpus_free(asnn_corpus* corpus);
 

@@ -7,7 +7,7 @@ API (see api.py) plus ctypes plumbing.
 """
 from .api import (  # noqa: F401
     ActivationState, Backend, BackendUnavailable, Device, DeviceError, DeviceGroup, DeviceLayout,
-    GenSpec, GroupLayout, comm_unique_id,
+    GenSpec, GroupLayout, comm_unique_id, device_generate_mlp, device_generate_powerlaw,
     InfeasibleSpec, InputArityMismatch, IoError, LayerAssignment, LayeredLayout, LayerOutOfRange,
     Network, OutputUnreachable, ParallelConfig, ParseError, RequiredSet, SplitMix64, UnassignedOutput,
     ValidationError, compute_required, normalize, parse_network, read_network, validate,

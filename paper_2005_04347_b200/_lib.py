@@ -134,6 +134,14 @@ PROTOTYPES = {
     "asnn_comm_unique_id": (C.c_int, [u8p]),
     "asnn_dev_comm_init": (C.c_int, [C.c_void_p, u8p, C.c_int, C.c_int]),
     "asnn_dev_allgather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, u64p]),
+    "asnn_dev_gen_mlp": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_double, C.c_uint64,
+                                   C.POINTER(C.c_void_p)]),
+    "asnn_dev_gen_mlp_layout": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_double, C.c_uint64,
+                                          C.POINTER(C.c_void_p)]),
+    "asnn_dev_gen_powerlaw": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                        C.c_uint64, C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "asnn_dev_gen_powerlaw_layout": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                               C.c_uint64, C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]),
     "asnn_corpus_desc": (C.c_int, [C.c_void_p, C.POINTER(NetworkDesc)]),
     "asnn_corpus_free": (None, [C.c_void_p]),
 }

@@ -876,6 +876,45 @@ def generate_powerlaw(n_nodes: int, bands: int, n_inputs: int, n_outputs: int, t
     return _corpus_to_network(lib, h)
 
 
+def device_generate_mlp(layers: int, width: int, p: float, seed: int, device: int = 0) -> Network:
+    """generate_mlp on the GPU (csrc/gen.cu), byte-identical to the host one."""
+    dev = Device.get(device)
+    h = C.c_void_p()
+    dev.check(dev.lib.asnn_dev_gen_mlp(dev.h, layers, width, p, seed, C.byref(h)))
+    return _corpus_to_network(dev.lib, h)
+
+
+def device_generate_powerlaw(n_nodes: int, bands: int, n_inputs: int, n_outputs: int, target_edges: int,
+                             alpha: float, seed: int, device: int = 0) -> Network:
+    """generate_powerlaw on the GPU (csrc/gen.cu), byte-identical to the host one."""
+    dev = Device.get(device)
+    h = C.c_void_p()
+    dev.check(dev.lib.asnn_dev_gen_powerlaw(dev.h, n_nodes, bands, n_inputs, n_outputs, target_edges, alpha,
+                                            seed, C.byref(h)))
+    return _corpus_to_network(dev.lib, h)
+
+
+def _gen_layout_mlp(cls, layers: int, width: int, p: float, seed: int, device: int = 0):
+    dev = Device.get(device)
+    h = C.c_void_p()
+    dev.check(dev.lib.asnn_dev_gen_mlp_layout(dev.h, layers, width, p, seed, C.byref(h)))
+    return cls(dev, h)
+
+
+def _gen_layout_powerlaw(cls, n_nodes: int, bands: int, n_inputs: int, n_outputs: int, target_edges: int,
+                         alpha: float, seed: int, device: int = 0):
+    dev = Device.get(device)
+    h = C.c_void_p()
+    dev.check(dev.lib.asnn_dev_gen_powerlaw_layout(dev.h, n_nodes, bands, n_inputs, n_outputs, target_edges,
+                                                   alpha, seed, C.byref(h)))
+    return cls(dev, h)
+
+
+# DeviceLayout.generated_mlp / generated_powerlaw: generate + levels on the GPU
+DeviceLayout.generated_mlp = classmethod(_gen_layout_mlp)
+DeviceLayout.generated_powerlaw = classmethod(_gen_layout_powerlaw)
+
+
 class SplitMix64:
     """rng.hpp:10-38 (for seeding corpora and inputs exactly like the reference)."""
     M = 0xFFFFFFFFFFFFFFFF

@@ -38,6 +38,24 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(heavy::smem_u32(bar))
         : "memory");
 }
+// The producer's waits for ring space: it runs ahead of the consumers, so
+// back off between polls instead of spinning -- a spinning producer warp
+// takes issue slots from the consumer warp sharing its SM sub-partition
+// (two CTAs per SM in the windowed variant).
+__device__ __forceinline__ void producer_wait(uint64_t* b, uint32_t parity) {
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(heavy::smem_u32(b)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(200);
+    }
+}
 __device__ __forceinline__ void consumer_barrier(uint32_t n_threads) {
     asm volatile("bar.sync 1, %0;" ::"r"(n_threads) : "memory");
 }
@@ -54,13 +72,64 @@ __device__ __forceinline__ void consumer_barrier(uint32_t n_threads) {
 // (split[i] for the layer's row i: staged slice or global, absolute edge
 // indices) and park the partial sum and the split in pre[] / pre_k[] for
 // MODE 1.
-template <int V, bool GUARD, int MODE = 0>
+// WIN (one network deeper than shared memory holds for one wave of CTAs):
+// shared memory keeps a ring of the newest W positions' activations (slot =
+// local position & mask, the zero row at slot W) and every activation is
+// also written through to A; at the step that finishes layer l a source is
+// read from the ring iff its local position >= lo = end(l) - W (not
+// overwritten before or during the step), otherwise from A (written by this
+// CTA at an earlier step, ordered by the layer barrier; L2-resident).
+// The prefix group's out-of-ring sources are staged one step early: right
+// after summing layer l+1's prefix at step l it issues cp.async copies of
+// the A values layer l+2's prefix will need from outside the ring (positions
+// < end(l+1) - W, final since step l-1) into stg, so at step l+1 they are
+// shared-memory reads and the L2 round trip left the critical path.  stg
+// (when non-null) holds, for Ep-relative edge index k, the staged value of
+// column group q at stg[k << gshift | q].
+struct Win {
+    float* Ag;      // A + c0
+    uint32_t ldA;
+    uint32_t mask;  // W - 1
+    int32_t lo;
+    const float* stg;
+};
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(heavy::smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Stage layer [a, b)'s prefix sources (edges [Rp[i], Sp[i]) of each row)
+// that lie outside the ring at the step that will consume them (local
+// position < lo).  Same (row, column group) -> thread map as layer_items.
+template <bool GUARD>
+__device__ __forceinline__ void stage_prefix(const uint32_t* Rp, const uint32_t* Sp, const uint2* Ep, uint32_t eb,
+                                             uint32_t a, uint32_t b, uint32_t gshift, uint32_t pos_base,
+                                             uint32_t n_pos, int32_t lo, const float* Ag, uint32_t ldA, float* stg,
+                                             uint32_t tid, uint32_t T) {
+    const uint32_t groups_mask = (1u << gshift) - 1u;
+    for (uint32_t it = tid; it < ((b - a) << gshift); it += T) {
+        const uint32_t i = it >> gshift, q = it & groups_mask;
+        const uint32_t k1 = Sp[i] - eb;
+        for (uint32_t k = Rp[i] - eb; k < k1; ++k) {
+            const uint32_t pos = Ep[k].x;
+            const uint32_t p = pos - pos_base;
+            if (GUARD && p >= n_pos) continue;
+            if (static_cast<int32_t>(p) < lo) cp_async4(stg + (k << gshift) + q, Ag + static_cast<size_t>(pos) * ldA + q);
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int V, bool GUARD, int MODE = 0, bool WIN = false>
 __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const uint2* Ep, uint32_t e0,
                                             uint32_t a, uint32_t b, uint32_t ld, uint32_t gshift,
                                             uint32_t pos_base, uint32_t row_base, uint32_t n_pos,
                                             uint32_t zero_row, uint32_t tid, uint32_t T,
                                             float* pre = nullptr, uint32_t* pre_k = nullptr,
-                                            const uint32_t* split = nullptr) {
+                                            const uint32_t* split = nullptr, Win win = {}) {
+    static_assert(!WIN || V == 1, "the windowed variant runs one column per item");
+    if constexpr (WIN && MODE == 2)
+        if (win.stg) asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's staged sources
     const uint32_t groups_mask = (1u << gshift) - 1u;
     for (uint32_t it = tid; it < ((b - a) << gshift); it += T) {
         const uint32_t i = it >> gshift, q = it & groups_mask;
@@ -85,6 +154,18 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
             if constexpr (GUARD) return static_cast<size_t>(p - (pos_base - row_base) < n_pos ? p : zero_row) * ld;
             else return static_cast<size_t>(p) * ld;
         };
+        // the address of source `pos`, column group q (WIN: ring or A)
+        auto src_of = [&](uint32_t pos, uint32_t k_cur) -> const float* {
+            if constexpr (WIN) {
+                const uint32_t p = pos - pos_base;
+                if (GUARD && p >= n_pos) return Aq + static_cast<size_t>(zero_row) * ld;
+                if (static_cast<int32_t>(p) >= win.lo) return Aq + static_cast<size_t>(p & win.mask) * ld;
+                if (MODE == 2 && win.stg) return win.stg + (k_cur << gshift) + q;
+                return win.Ag + static_cast<size_t>(pos) * win.ldA + q;
+            } else {
+                return Aq + row(pos);
+            }
+        };
         float acc[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[v] = MODE == 1 ? pre[it * V + v] : 0.0f;
@@ -96,7 +177,7 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
             for (int j = 0; j < 4; ++j) ed[j] = Ep[k + j];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const float* src = Aq + row(ed[j].x);
+                const float* src = src_of(ed[j].x, k + j);
                 if constexpr (V == 4) {
                     const float4 t = *reinterpret_cast<const float4*>(src);
                     av[j][0] = t.x;
@@ -115,7 +196,7 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
         }
         for (; k < ke; ++k) {
             const uint2 ed = Ep[k];
-            const float* src = Aq + row(ed.x);
+            const float* src = src_of(ed.x, k);
 #pragma unroll
             for (int v = 0; v < V; ++v) acc[v] = mac(acc[v], __uint_as_float(ed.y), src[v]);
         }
@@ -124,8 +205,9 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
             for (int v = 0; v < V; ++v) pre[it * V + v] = acc[v];
             continue;
         }
-        float* dst = As + static_cast<size_t>(pos_base - row_base + a + i) * ld + q * V;
+        float* dst = As + static_cast<size_t>(WIN ? ((a + i) & win.mask) : pos_base - row_base + a + i) * ld + q * V;
         sigmoid32_v<V>(acc);
+        if constexpr (WIN) win.Ag[static_cast<size_t>(pos_base + a + i) * win.ldA + q] = acc[0];
         wc_note(pos_base + a + i, blockIdx.x * ((groups_mask + 1) * V) + q * V, V);
         if constexpr (V == 4) {
             *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
@@ -160,14 +242,15 @@ constexpr uint32_t kMetaBytes = kSlots * (8 + 8 + 32);
 // <= l-1, final since step l-1) -- half of each layer's dependent work moves
 // off the critical path.  The fp32 sum of a row is the same sequence of
 // roundings (segments.cuh); split[] comes from k_splits.
-template <int V, bool GUARD, bool GLOBAL, bool PIPE = false>
+template <int V, bool GUARD, bool GLOBAL, bool PIPE = false, bool WIN = false>
 __global__ void __launch_bounds__(544)
 k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
       const uint32_t* __restrict__ le_cat, const uint32_t* __restrict__ row_ptr,
       const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,
       const uint4* __restrict__ oinfo, const float* __restrict__ x, uint32_t n_vec,
       float* __restrict__ A, uint32_t ldA, uint32_t C, uint32_t max_pos, uint32_t ring_bytes,
-      int write_all, float* __restrict__ out, const uint32_t* __restrict__ split, uint32_t max_items) {
+      int write_all, float* __restrict__ out, const uint32_t* __restrict__ split, uint32_t max_items,
+      uint32_t win_mask, uint32_t stg_edges) {
     using namespace cta;
     extern __shared__ __align__(128) unsigned char cta_smem[];
     const CtaNet n = nets[blockIdx.y];
@@ -177,7 +260,10 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     float* As = GLOBAL ? A + c0 : reinterpret_cast<float*>(cta_smem);
     const uint32_t ld = GLOBAL ? ldA : C;
     const uint32_t row_base = GLOBAL ? 0u : n.pos_base;
-    const size_t as_floats = GLOBAL ? 0 : ((static_cast<size_t>(max_pos + 1) * C + 3) & ~size_t(3));
+    // WIN: the ring of the newest W = win_mask + 1 positions, the zero row at slot W
+    const uint32_t zero_slot = WIN ? win_mask + 1 : max_pos;
+    const size_t as_floats = GLOBAL ? 0 : ((static_cast<size_t>(zero_slot + 1) * C + 3) & ~size_t(3));
+    const Win win0{A + c0, ldA, win_mask, 0};
     unsigned char* ring = reinterpret_cast<unsigned char*>(reinterpret_cast<float*>(cta_smem) + as_floats);
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + ring_bytes);
     uint64_t* empty = full + kSlots;
@@ -185,6 +271,8 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     // PIPE: two parity buffers of partial sums [max_items * V] and splits [max_items]
     float* pre = reinterpret_cast<float*>(meta + 8 * kSlots);
     uint32_t* pre_k = reinterpret_cast<uint32_t*>(pre + 2 * max_items * V);
+    // WIN + PIPE: two parity buffers of staged prefix sources [stg_edges * C]
+    float* stg_buf = reinterpret_cast<float*>(pre_k + 2 * max_items);
 
     const uint32_t groups = C / V;  // column groups per row (a power of two)
     const uint32_t gshift = __ffs(groups) - 1;
@@ -226,7 +314,7 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                 const uint32_t ebytes = ((e1 - e0 + (e0 - e0a)) * 8 + 15) & ~15u;
                 const uint32_t size = rbytes + sbytes + ebytes;
                 if (u > 0) {  // slot m's previous layer (l - kSlots) and all before it are released
-                    heavy::mbar_wait(&empty[m], (u - 1) & 1);
+                    producer_wait(&empty[m], (u - 1) & 1);
                     release_to(l - kSlots + 1);
                 }
                 bool staged = size <= ring_bytes && !(write_all & 2);
@@ -246,11 +334,11 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                         // PIPE: layer l-1 is released only after the step that
                         // also needs layer l (its prefix): never wait for it --
                         // layer l is then read from global memory instead
-                        if (PIPE && oldest + 1 >= l) {
+                        if (PIPE && oldest + (WIN && stg_edges ? 2u : 1u) >= l) {
                             staged = false;
                             break;
                         }
-                        heavy::mbar_wait(&empty[(oldest - 1) % kSlots], ((oldest - 1) / kSlots) & 1);
+                        producer_wait(&empty[(oldest - 1) % kSlots], ((oldest - 1) / kSlots) & 1);
                         release_to(oldest + 1);
                     }
                 }
@@ -275,7 +363,7 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
         }
     } else {
         if constexpr (!GLOBAL)
-            for (uint32_t c = tid; c < C; c += Tc) As[max_pos * C + c] = 0.0f;
+            for (uint32_t c = tid; c < C; c += Tc) As[zero_slot * C + c] = 0.0f;
         // sensors: eval.cpp:17 (sigmoided input values), overlapping the staging.
         // One (column, sensor) per thread, sensor fastest: a column's inputs
         // are contiguous in x ([vector][input]), so the reads coalesce (they
@@ -287,7 +375,13 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
             float xv = 0.0f;
             if (col < n_vec && k != kUnassigned)
                 xv = x[static_cast<uint64_t>(n_vec) * n.in_prefix + static_cast<uint64_t>(col) * n.n_in + k];
-            As[static_cast<size_t>(n.pos_base - row_base + s) * ld + c] = sigmoid32(xv);
+            const float sv = sigmoid32(xv);
+            if constexpr (WIN) {
+                A[static_cast<uint64_t>(n.pos_base + s) * ldA + col] = sv;
+                if (s + win_mask + 1 >= n.n_sensors) As[static_cast<size_t>(s & win_mask) * ld + c] = sv;
+            } else {
+                As[static_cast<size_t>(n.pos_base - row_base + s) * ld + c] = sv;
+            }
             wc_note(n.pos_base + s, col, 1);
         }
         consumer_barrier(Tc);
@@ -311,12 +405,35 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                     const uint32_t eb = mm[3] ? e0 : 0u;
                     float* pb = pre + (ll & 1) * max_items * V;
                     uint32_t* pk = pre_k + (ll & 1) * max_items;
-                    if (fin)
-                        layer_items<V, GUARD, 1>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base, n.n_pos,
-                                                 max_pos, gtid, Th, pb, pk, Sp);
-                    else
-                        layer_items<V, GUARD, 2>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base, n.n_pos,
-                                                 max_pos, gtid, Th, pb, pk, Sp);
+                    // this step's ring boundary: the end of layer l (= b of the
+                    // finish group's layer, a of the prefix group's)
+                    Win win = win0;
+                    win.lo = static_cast<int32_t>(fin ? b : a) - static_cast<int32_t>(win_mask + 1);
+                    if (fin) {
+                        layer_items<V, GUARD, 1, WIN>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base,
+                                                      n.n_pos, zero_slot, gtid, Th, pb, pk, Sp, win);
+                    } else {
+                        if constexpr (WIN)
+                            if (stg_edges) win.stg = stg_buf + (ll & 1) * stg_edges * C - (static_cast<size_t>(e0 - eb) << gshift);
+                        layer_items<V, GUARD, 2, WIN>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base,
+                                                      n.n_pos, zero_slot, gtid, Th, pb, pk, Sp, win);
+                        // stage layer ll+1's out-of-ring prefix sources for the next step
+                        if constexpr (WIN)
+                            if (stg_edges && ll + 1 < n.n_layers) {
+                                const uint32_t m2 = ll % kSlots;
+                                heavy::mbar_wait(&full[m2], (ll / kSlots) & 1);
+                                const uint32_t* m2m = meta + 8 * m2;
+                                const uint32_t a2 = m2m[0], b2 = m2m[1], e02 = m2m[2];
+                                const uint32_t* Rp2 = m2m[3] ? ring_u32 + m2m[4] : row_ptr + n.pos_base + a2;
+                                const uint32_t* Sp2 = m2m[3] ? ring_u32 + m2m[7] : split + n.pos_base + a2;
+                                const uint2* Ep2 = m2m[3] ? ring_u2 + m2m[5] : edges;
+                                const uint32_t eb2 = m2m[3] ? e02 : 0u;
+                                float* st2 = stg_buf + ((ll + 1) & 1) * stg_edges * C - (static_cast<size_t>(e02 - eb2) << gshift);
+                                stage_prefix<GUARD>(Rp2, Sp2, Ep2, eb2, a2, b2, gshift, n.pos_base, n.n_pos,
+                                                    static_cast<int32_t>(b) - static_cast<int32_t>(win_mask + 1),
+                                                    win0.Ag, ldA, st2, gtid, Th);
+                            }
+                    }
                 }
                 consumer_barrier(Tc);  // layer l final, prefix of l+1 parked
                 if (tid == 0 && l >= 1) heavy::mbar_arrive(&empty[(l - 1) % kSlots]);
@@ -327,17 +444,21 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
             heavy::mbar_wait(&full[m], ((l - 1) / kSlots) & 1);
             const uint32_t* mm = meta + 8 * m;
             const uint32_t a = mm[0], b = mm[1], e0 = mm[2];
+            Win win = win0;
+            win.lo = static_cast<int32_t>(b) - static_cast<int32_t>(win_mask + 1);
             if (mm[3])
-                layer_items<V, GUARD>(As, ring_u32 + mm[4], ring_u2 + mm[5], e0, a, b, ld, gshift,
-                                      n.pos_base, row_base, n.n_pos, max_pos, tid, Tc);
+                layer_items<V, GUARD, 0, WIN>(As, ring_u32 + mm[4], ring_u2 + mm[5], e0, a, b, ld, gshift,
+                                              n.pos_base, row_base, n.n_pos, zero_slot, tid, Tc, nullptr,
+                                              nullptr, nullptr, win);
             else
-                layer_items<V, GUARD>(As, row_ptr + n.pos_base + a, edges, 0, a, b, ld, gshift,
-                                      n.pos_base, row_base, n.n_pos, max_pos, tid, Tc);
+                layer_items<V, GUARD, 0, WIN>(As, row_ptr + n.pos_base + a, edges, 0, a, b, ld, gshift,
+                                              n.pos_base, row_base, n.n_pos, zero_slot, tid, Tc, nullptr,
+                                              nullptr, nullptr, win);
             consumer_barrier(Tc);  // layer l visible to every consumer
             if (tid == 0) heavy::mbar_arrive(&empty[m]);
         }
     }
-    if constexpr (GLOBAL) return;  // the activations are already in A
+    if constexpr (GLOBAL || WIN) return;  // the activations are already in A
     __syncthreads();
 
     // write back: every row (state requested) or only the declared outputs

@@ -374,6 +374,9 @@ struct CtaPlan {
     bool pipe = false;        // two consumer groups: finish layer l | prefix of layer l+1
     uint32_t max_items = 0;   // items (node x column group) of the widest layer
     bool global = false;  // activations in A (L2) instead of shared memory
+    bool win = false;     // ring of the newest positions in shared memory + A (cta.cuh Win)
+    uint32_t win_mask = 0;
+    uint32_t stg_edges = 0;  // WIN + pipe: staged prefix sources per layer (0 = direct loads)
 };
 
 constexpr uint32_t kMaxDynSmem = 227 * 1024;
@@ -458,6 +461,65 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         const char* s = getenv("ASNN_CTA_GLOBAL");
         return s && s[0] == '1';
     }();
+    // Windowed variant (cta.cuh Win): a deep network whose whole-slice CTAs
+    // would need more than one wave (C3: 256 one-column CTAs of 232 KB, two
+    // waves) runs one wave at two CTAs per SM, each keeping only the newest W
+    // positions in shared memory and reading older sources from A in L2.
+    // ASNN_CTA_WIN=0 disables.
+    static const bool want_win = [] {
+        const char* s = getenv("ASNN_CTA_WIN");
+        return !(s && s[0] == '0');
+    }();
+    // Sweep mode 4 (tests): the windowed variant with the smallest legal ring
+    // (W >= 2 x the widest layer: a layer's writes never share a slot).
+    const bool force_win = mode == 4 && L->nets.size() == 1;
+    if (force_win ||
+        (want_win && !want_global && L->nets.size() == 1 && smem_waves > 1 && a_bytes <= (96ull << 20))) {
+        uint32_t C = 1;
+        while (ldA / C > 2 * sms && C < 128) C <<= 1;
+        const uint64_t items_c = static_cast<uint64_t>(L->max_width) * C;
+        // pipelined consumers + (ASNN_CTA_STAGE=0 disables) the prefix group's
+        // staged out-of-ring sources, 2 x the largest layer's edges x C floats
+        static const bool want_stage = [] {
+            const char* s = getenv("ASNN_CTA_STAGE");
+            return !(s && s[0] == '0');
+        }();
+        const uint64_t stg_c = want_stage && static_cast<uint64_t>(L->max_level_edges) * C * 8 <= 32 * 1024
+                                   ? static_cast<uint64_t>(L->max_level_edges) * C * 8 : 0;
+        const uint64_t pipe_c = want_pipe && items_c <= 512 ? 2 * items_c * 2 * 4 + stg_c : 0;
+        const uint64_t budget = per_sm / 2 - 1024;
+        uint64_t ring = std::min<uint64_t>(std::max<uint64_t>(2 * max_layer, 24 * 1024), 32 * max_layer) / 16 * 16;
+        uint64_t W = 1;
+        if (force_win) {
+            while (W < std::max<uint64_t>(32, 2 * static_cast<uint64_t>(L->max_width))) W *= 2;
+            // whatever shared memory the ring of positions leaves (layers larger
+            // than the staging ring are read from global memory)
+            const uint64_t wb = ((W + 1) * C * 4 + 15) / 16 * 16;
+            const uint64_t room = kMaxDynSmem > cta::kMetaBytes + pipe_c + wb + 1024
+                                      ? kMaxDynSmem - cta::kMetaBytes - pipe_c - wb - 1024 : 0;
+            ring = std::max<uint64_t>(16, std::min(ring, room) / 16 * 16);
+        }
+        static const int w_log2 = [] {
+            const char* s = getenv("ASNN_CTA_WIN_LOG2");  // experiments: fixed ring size
+            return s ? atoi(s) : 0;
+        }();
+        const uint64_t fixed = cta::kMetaBytes + pipe_c + ring;
+        if (!force_win) {
+            if (w_log2 > 0) W = 1ull << w_log2;
+            else
+                while (fixed + ((2 * W + 1) * C * 4 + 15) / 16 * 16 <= budget) W *= 2;
+        }
+        if (force_win ||
+            (ring >= 2 * max_layer && W >= 4 * static_cast<uint64_t>(L->max_width) && W < L->max_pos)) {
+            p.C = C;
+            p.win = true;
+            p.win_mask = static_cast<uint32_t>(W - 1);
+            p.stg_edges = pipe_c && stg_c ? L->max_level_edges : 0;
+            p.ring_bytes = static_cast<uint32_t>(ring);
+            p.smem = static_cast<uint32_t>(fixed + ((W + 1) * C * 4 + 15) / 16 * 16);
+            p.pipe = pipe_c > 0;
+        }
+    }
     if (want_global && L->nets.size() == 1 && smem_waves > 1 && a_bytes <= (96ull << 20) &&
         !L->zero_refs) {
         uint32_t C = 1;
@@ -469,7 +531,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         p.smem = p.ring_bytes + cta::kMetaBytes;
     }
     if (!p.C) return p;
-    p.V = p.C >= 4 ? 4 : 1;
+    p.V = p.C >= 4 && !p.win ? 4 : 1;
     const uint64_t items = static_cast<uint64_t>(L->max_width) * (p.C / p.V);
     // consumer threads per CTA: up to 512 (+ the producer warp).  Config 5
     // (1024 column-group items per layer, 2 CTAs/SM): 256 -> 0.90 ms, 512 ->
@@ -498,7 +560,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     const double cta_us = (1.2 * L->n_levels + static_cast<double>(L->total_edges) / L->nets.size() * p.C / 1100.0) *
                           static_cast<double>((ctas + per_wave - 1) / per_wave);
     const double level_us = 7.0 * L->n_levels;
-    p.use = mode == 2 || (latency_bound && (L->nets.size() > 1 || cta_us <= level_us));
+    p.use = mode == 2 || force_win || (latency_bound && (L->nets.size() > 1 || cta_us <= level_us));
     return p;
 }
 
@@ -933,10 +995,12 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
     mark();
     const CtaPlan cp = cta_plan(L, ldA);
     // K-cta writes the declared outputs itself (shared-memory variant, no state)
-    const bool cta_out = cp.use && !cp.global && !state && out && L->total_out;
+    const bool cta_out = cp.use && !cp.global && !cp.win && !state && out && L->total_out;
     if (cp.use) {
         // the whole sweep (sensors + every layer) of each (network, slice) in one CTA
-        auto fn = cp.global ? (cp.V == 4 ? k_cta<4, false, true> : k_cta<1, false, true>)
+        auto fn = cp.win ? (cp.pipe ? (L->zero_refs ? k_cta<1, true, false, true, true> : k_cta<1, false, false, true, true>)
+                                    : (L->zero_refs ? k_cta<1, true, false, false, true> : k_cta<1, false, false, false, true>))
+                  : cp.global ? (cp.V == 4 ? k_cta<4, false, true> : k_cta<1, false, true>)
                   : cp.pipe
                       ? (cp.V == 4 ? (L->zero_refs ? k_cta<4, true, false, true> : k_cta<4, false, false, true>)
                                    : (L->zero_refs ? k_cta<1, true, false, true> : k_cta<1, false, false, true>))
@@ -948,7 +1012,8 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T + 32, cp.smem, st>>>(
             reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->le_cat.p, L->row_ptr.p,
             L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos, cp.ring_bytes,
-            (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr, L->split.p, cp.max_items);
+            (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr, L->split.p, cp.max_items,
+            cp.win_mask, cp.stg_edges);
     } else {
         if (L->total_sensors)
             k_sense<<<blocks_for(static_cast<uint64_t>(L->total_sensors) * ldA), kThreads, 0, st>>>(
@@ -1307,7 +1372,7 @@ int asnn_dev_open(int device, asnn_dev** out) {
         cudaGetLastError();
     }
     dev->heavy_threshold = default_heavy_threshold();
-    if (const char* m = getenv("ASNN_SWEEP_MODE")) dev->sweep_mode = static_cast<uint32_t>(atoi(m)) % 4;
+    if (const char* m = getenv("ASNN_SWEEP_MODE")) dev->sweep_mode = static_cast<uint32_t>(atoi(m)) % 5;
     // The heavy-row branch gets the highest stream priority: its CTAs carry
     // the longest dependent-add chains of the layer and must become resident
     // before the light rows fill the machine (ASNN_HEAVY_PRIO=0 disables).
@@ -1352,7 +1417,7 @@ int asnn_dev_set_stream(asnn_dev* dev, void* s) {
 void* asnn_dev_get_stream(asnn_dev* dev) { return dev ? dev->stream : nullptr; }
 
 int asnn_dev_set_sweep_mode(asnn_dev* dev, uint32_t mode) {
-    if (!dev || mode > 3) return ASNN_E_INVALID;
+    if (!dev || mode > 4) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
     dev->sweep_mode = mode;
     ++dev->option_epoch;

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "asnn_dev.h"
+#include "gen_core.h"
 
 namespace {
 
@@ -72,6 +73,26 @@ std::uint64_t capacity_of(const std::vector<std::uint32_t>& starts) {
         cap += static_cast<std::uint64_t>(starts[b + 1] - starts[b]) * starts[b];
     return cap;
 }
+
+}  // namespace
+
+// Pareto scale of config 4's extra-source count: expected mandatory edges are
+// one predecessor per non-input plus one successor per non-output, the rest
+// comes from the Pareto(alpha) draws (mean = xm * alpha / (alpha - 1)).
+// Shared with gen.cu.
+double powerlaw_xm(uint32_t n_nodes, uint32_t n_in, uint32_t n_out, uint64_t target_edges, double alpha) {
+    const std::uint64_t non_inputs = n_nodes - n_in;
+    const double mandatory = static_cast<double>(non_inputs) + (n_nodes - n_out);
+    const double extra_mean = std::max(0.0, (static_cast<double>(target_edges) - mandatory) /
+                                                 static_cast<double>(non_inputs));
+    return extra_mean * (alpha - 1.0) / alpha;
+}
+
+std::vector<std::uint32_t> powerlaw_band_starts(uint32_t n_nodes, uint32_t bands, uint32_t n_in, uint32_t n_out) {
+    return band_starts(n_in, n_out, n_nodes - n_in - n_out, bands);
+}
+
+namespace {
 
 inline std::uint64_t pair_key(std::uint32_t s, std::uint32_t t) {
     return (static_cast<std::uint64_t>(s) << 32) | t;
@@ -187,7 +208,9 @@ int asnn_gen_reference(uint32_t in, uint32_t out, uint32_t hidden, uint64_t conn
 // Config 2: `layers` layers of `width` nodes, ids layer-major.
 // Layer 0 = inputs, last layer = outputs; every node of layer l >= 1 links to
 // each node of layer l-1 independently with probability p (at least one),
-// weights U[-1, 1].  Edges come out target-major, sources ascending.
+// weights U[-1, 1] (gen_core.h mlp_draw: one counter-seeded stream per
+// target, so the device generator in gen.cu reproduces it byte for byte).
+// Edges come out target-major, sources ascending.
 int asnn_gen_mlp(uint32_t layers, uint32_t width, double p, uint64_t seed, asnn_corpus** result) {
     if (!result || layers < 2 || width == 0 || !(p > 0.0 && p <= 1.0)) return ASNN_E_INVALID;
     auto* c = new asnn_corpus;
@@ -196,26 +219,24 @@ int asnn_gen_mlp(uint32_t layers, uint32_t width, double p, uint64_t seed, asnn_
     for (std::uint32_t i = 0; i < n; ++i) c->nodes[i] = i;
     for (std::uint32_t i = 0; i < width; ++i) c->inputs.push_back(i);
     for (std::uint32_t i = 0; i < width; ++i) c->outputs.push_back((layers - 1) * width + i);
-    SplitMix64 rng(seed);
-    const std::uint64_t expect = static_cast<std::uint64_t>(n) * width * p * 1.05 + 1024;
-    c->src.reserve(expect);
-    c->dst.reserve(expect);
-    c->w.reserve(expect);
-    for (std::uint32_t t = width; t < n; ++t) {
-        const std::uint32_t base = (t / width - 1) * width;
-        std::size_t before = c->src.size();
-        for (std::uint32_t j = 0; j < width; ++j) {
-            if (rng.uniform01() < p) {
-                c->src.push_back(base + j);
-                c->dst.push_back(t);
-                c->w.push_back(rng.uniform(-1.0f, 1.0f));
-            }
-        }
-        if (c->src.size() == before) {
-            c->src.push_back(base + static_cast<std::uint32_t>(rng.bounded(width)));
-            c->dst.push_back(t);
-            c->w.push_back(rng.uniform(-1.0f, 1.0f));
-        }
+    std::vector<std::uint64_t> row(n + 1, 0);
+#pragma omp parallel for schedule(static)
+    for (std::int64_t t = width; t < static_cast<std::int64_t>(n); ++t)
+        row[t + 1] = asnn_gen::mlp_draw(seed, width, p, static_cast<std::uint32_t>(t), [](std::uint32_t, float) {});
+    for (std::uint32_t t = 0; t < n; ++t) row[t + 1] += row[t];
+    const std::uint64_t E = row[n];
+    c->src.resize(E);
+    c->dst.resize(E);
+    c->w.resize(E);
+#pragma omp parallel for schedule(static)
+    for (std::int64_t t = width; t < static_cast<std::int64_t>(n); ++t) {
+        std::uint64_t k = row[t];
+        asnn_gen::mlp_draw(seed, width, p, static_cast<std::uint32_t>(t), [&](std::uint32_t s, float w) {
+            c->src[k] = s;
+            c->dst[k] = static_cast<std::uint32_t>(t);
+            c->w[k] = w;
+            ++k;
+        });
     }
     *result = c;
     return ASNN_OK;
@@ -231,41 +252,26 @@ int asnn_gen_mlp(uint32_t layers, uint32_t width, double p, uint64_t seed, asnn_
 //   - every node of band b-1 that picked v as its mandatory successor (each
 //     non-output node picks one in band b+1, so every node reaches an output
 //     and is required).
-// All randomness is a per-node SplitMix64 stream, so the result does not
-// depend on the thread count.  Edges are target-major, sources ascending,
-// weights U[-1, 1].
+// All randomness is a per-node SplitMix64 stream (gen_core.h pl_succ /
+// pl_draw, shared with the device generator in gen.cu), so the result does
+// not depend on the thread count or the processor.  Edges are target-major,
+// sources ascending, weights U[-1, 1].
 int asnn_gen_powerlaw(uint32_t n_nodes, uint32_t bands, uint32_t n_in, uint32_t n_out,
                       uint64_t target_edges, double alpha, uint64_t seed, asnn_corpus** result) {
     if (!result || bands < 3 || n_in == 0 || n_out == 0 || !(alpha > 1.0) ||
         n_nodes < n_in + n_out + (bands - 2))
         return ASNN_E_INVALID;
     const auto starts = band_starts(n_in, n_out, n_nodes - n_in - n_out, bands);
-    auto band_of = [&starts](std::uint32_t id) {
-        return static_cast<std::uint32_t>(std::upper_bound(starts.begin(), starts.end(), id) -
-                                          starts.begin()) - 1;
-    };
+    const asnn_gen::PowerlawSpec spec{starts.data(), bands, powerlaw_xm(n_nodes, n_in, n_out, target_edges, alpha),
+                                      alpha, seed};
     const std::uint32_t first = n_in;
-    const std::uint64_t non_inputs = n_nodes - n_in;
-    // Expected mandatory edges: one predecessor per non-input plus one
-    // successor per non-output; the rest come from the Pareto draws.
-    const double mandatory = static_cast<double>(non_inputs) + (n_nodes - n_out);
-    const double extra_mean = std::max(0.0, (static_cast<double>(target_edges) - mandatory) /
-                                                 static_cast<double>(non_inputs));
-    const double xm = extra_mean * (alpha - 1.0) / alpha;  // Pareto scale for that mean
-    auto node_rng = [seed](std::uint32_t v, std::uint64_t salt) {
-        return SplitMix64(seed ^ (0x9E3779B97F4A7C15ull * (static_cast<std::uint64_t>(v) + 1)) ^
-                          salt);
-    };
 
     // Pass 1: mandatory successor of every non-output node.
     std::vector<std::uint32_t> msucc_count(n_nodes + 1, 0);
     std::vector<std::uint32_t> msucc(n_nodes, 0xFFFFFFFFu);
 #pragma omp parallel for schedule(static)
-    for (std::int64_t v = 0; v < static_cast<std::int64_t>(starts[bands - 1]); ++v) {
-        const std::uint32_t b = band_of(static_cast<std::uint32_t>(v));
-        auto r = node_rng(static_cast<std::uint32_t>(v), 0x5A5A5A5A5A5A5A5Aull);
-        msucc[v] = starts[b + 1] + static_cast<std::uint32_t>(r.bounded(starts[b + 2] - starts[b + 1]));
-    }
+    for (std::int64_t v = 0; v < static_cast<std::int64_t>(starts[bands - 1]); ++v)
+        msucc[v] = asnn_gen::pl_succ(spec, static_cast<std::uint32_t>(v));
     for (std::uint32_t v = 0; v < starts[bands - 1]; ++v) msucc_count[msucc[v] + 1]++;
     for (std::uint32_t t = 0; t < n_nodes; ++t) msucc_count[t + 1] += msucc_count[t];
     std::vector<std::uint32_t> msucc_src(msucc_count[n_nodes]);
@@ -277,29 +283,9 @@ int asnn_gen_powerlaw(uint32_t n_nodes, uint32_t bands, uint32_t n_in, uint32_t 
     // Pass 2: per-target source lists (sizes first, then fill).
     auto draw_sources = [&](std::uint32_t t, std::vector<std::uint32_t>& out_src,
                             std::vector<float>* out_w) {
-        const std::uint32_t b = band_of(t);
-        const std::uint32_t avail = starts[b];
-        auto r = node_rng(t, 0xC3C3C3C3C3C3C3C3ull);
-        const std::uint32_t mpred =
-            starts[b - 1] + static_cast<std::uint32_t>(r.bounded(starts[b] - starts[b - 1]));
-        const double u = 1.0 - r.uniform01();  // (0, 1]
-        double d = xm > 0.0 ? std::floor(xm * std::pow(u, -1.0 / alpha)) : 0.0;
-        const double cap = std::min<double>(avail, 1u << 20);
-        if (d > cap) d = cap;
-        std::uint32_t k = static_cast<std::uint32_t>(d);
         out_src.clear();
-        out_src.push_back(mpred);
-        for (std::uint32_t i = msucc_count[t]; i < msucc_count[t + 1]; ++i)
-            out_src.push_back(msucc_src[i]);
-        if (k >= avail / 2) {
-            // dense: every earlier id with probability k/avail
-            const double q = static_cast<double>(k) / avail;
-            for (std::uint32_t s = 0; s < avail; ++s)
-                if (r.uniform01() < q) out_src.push_back(s);
-        } else {
-            for (std::uint32_t i = 0; i < k; ++i)
-                out_src.push_back(static_cast<std::uint32_t>(r.bounded(avail)));
-        }
+        for (std::uint32_t i = msucc_count[t]; i < msucc_count[t + 1]; ++i) out_src.push_back(msucc_src[i]);
+        asnn_gen::Rng r = asnn_gen::pl_draw(spec, t, [&](std::uint32_t s) { out_src.push_back(s); });
         std::sort(out_src.begin(), out_src.end());
         out_src.erase(std::unique(out_src.begin(), out_src.end()), out_src.end());
         if (out_w) {

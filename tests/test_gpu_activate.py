@@ -20,12 +20,13 @@ pytestmark = pytest.mark.gpu
 DEV = A.ParallelConfig(backend=A.Backend.DeviceCompute)
 
 
-@pytest.fixture(params=[1, 2, 3], ids=["layer-launches", "k_cta", "whole-rows"])
+@pytest.fixture(params=[1, 2, 3, 4], ids=["layer-launches", "k_cta", "whole-rows", "k_cta-window"])
 def sweep_mode(request):
     """Run a test under every sweep strategy: one launch per dependency level
     (heavy rows split into segments where eligible), the one-CTA-per-slice
-    sweep (k_cta), and per-level launches of whole rows (k_rows/k_level +
-    k_heavy)."""
+    sweep (k_cta), per-level launches of whole rows (k_rows/k_level +
+    k_heavy), and the windowed k_cta (a ring of the newest positions in
+    shared memory, older sources from A) with its smallest ring."""
     dev = A.Device.get(0)
     dev.set_sweep_mode(request.param)
     yield request.param
@@ -260,7 +261,7 @@ def test_predecessors_without_position(oracle, B, sweep_mode):
     assert bitwise_equal(st, oracle.eval_batch(d, X))
 
 
-@pytest.mark.parametrize("sweep_mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("sweep_mode", [0, 1, 2, 3, 4])
 def test_zero_row_reused_across_narrowing_batches(oracle, sweep_mode):
     """One DeviceLayout reused with batch widths going down (256, 64, 4, 1):
     the zero row at the narrower pitch overlaps rows the wider sweep wrote

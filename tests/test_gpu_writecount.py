@@ -65,7 +65,7 @@ def _child():
             "powerlaw": A.generate_powerlaw(200_000, 40, 512, 512, 10_000_000, 2.1, 7)}
     for name, net in nets.items():
         dl = A.DeviceLayout.from_network(net)
-        for mode in (0, 1, 2, 3):
+        for mode in (0, 1, 2, 3, 4):
             dev.set_sweep_mode(mode)
             for B in ((1, 4, 64, 130, 256) if name != "powerlaw" else (1, 16, 64)):
                 check(f"{name}/mode{mode}", dl, B)
@@ -92,7 +92,7 @@ def _child():
     dl = A.DeviceLayout.from_layout(A.LayeredLayout(d["total_layers"], d["layer_offsets"], d["node_ids"],
                                                     d["row_ptr"], d["in_nodes"], d["in_weights"],
                                                     d["input_order"], 0, d["id_bound"], net.outputs))
-    for mode in (0, 1, 2, 3):
+    for mode in (0, 1, 2, 3, 4):
         dev.set_sweep_mode(mode)
         for B in (1, 64, 256):
             check(f"zero-row/mode{mode}", dl, B)

@@ -12,6 +12,8 @@
 //
 // Built here into oracle/_ref/libasnn_ref_dev.so (oracle/Makefile) so the GPU
 // tests can run the reference's own evaluators and this backend side by side.
+#include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <mutex>
 #include <span>
@@ -38,6 +40,8 @@ namespace {
     }
 }
 
+}  // namespace
+
 // One device handle per process (device 0), opened on first use.
 asnn_dev* device() {
     static std::once_flag once;
@@ -47,8 +51,6 @@ asnn_dev* device() {
     if (rc != ASNN_OK) raise(rc, nullptr);
     return dev;
 }
-
-}  // namespace
 
 // eval_parallel(..., Backend::DeviceCompute): same contract as eval.cpp:49-80.
 ActivationState eval_device(const LayeredLayout& layout, std::span<const float> input_values,
@@ -122,4 +124,83 @@ extern "C" int ref_dev_eval(const asnn::LayeredLayout* layout, const float* x, s
     } catch (...) {
         return 6;
     }
+}
+
+// Timing hooks for tools/bench_csv.py (the reference's bench protocol with
+// device rows, bench.cpp:41-100): mean / sample stddev in microseconds of
+// `reps` calls after `warmup`, timed inside C++ like the reference's own
+// sequential / parallel rows.  "per call" = the drop-in eval_parallel
+// (DeviceCompute): conversion + upload + activate + state back + free every
+// call; "resident" = asnn_dev_activate on a layout uploaded once (state back).
+namespace {
+void stats_us(const std::vector<double>& s, double* mean, double* sd) {
+    double m = 0;
+    for (double v : s) m += v;
+    m /= s.size();
+    double q = 0;
+    for (double v : s) q += (v - m) * (v - m);
+    *mean = m;
+    *sd = s.size() > 1 ? std::sqrt(q / (s.size() - 1)) : 0.0;
+}
+}  // namespace
+
+extern "C" int ref_dev_eval_timed(const asnn::LayeredLayout* layout, const float* x, std::uint32_t n_x,
+                                  std::uint32_t warmup, std::uint32_t reps, double* mean_us, double* sd_us) {
+    try {
+        asnn::ParallelConfig cfg;
+        cfg.backend = asnn::ParallelConfig::Backend::DeviceCompute;
+        std::span<const float> xs(x, n_x);
+        for (std::uint32_t i = 0; i < warmup; ++i) (void)asnn::eval_device(*layout, xs, cfg);
+        std::vector<double> s;
+        for (std::uint32_t i = 0; i < reps; ++i) {
+            const auto t0 = std::chrono::steady_clock::now();
+            auto st = asnn::eval_device(*layout, xs, cfg);
+            s.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+        }
+        stats_us(s, mean_us, sd_us);
+        return 0;
+    } catch (...) {
+        return 6;
+    }
+}
+
+extern "C" int ref_dev_resident_timed(const asnn::LayeredLayout* layout, const float* x, std::uint32_t n_x,
+                                      std::uint32_t warmup, std::uint32_t reps, double* mean_us, double* sd_us) {
+    asnn_dev* dev = asnn::device();
+    std::vector<std::uint32_t> ids(layout->nodes.size()), in;
+    std::vector<std::uint64_t> rp(layout->nodes.size() + 1, 0);
+    std::vector<float> w;
+    for (std::size_t k = 0; k < layout->nodes.size(); ++k) {
+        ids[k] = layout->nodes[k].id;
+        in.insert(in.end(), layout->nodes[k].in_nodes.begin(), layout->nodes[k].in_nodes.end());
+        w.insert(w.end(), layout->nodes[k].in_weights.begin(), layout->nodes[k].in_weights.end());
+        rp[k + 1] = in.size();
+    }
+    asnn_layout_desc d{};
+    d.total_layers = layout->total_layers;
+    d.layer_offsets = layout->layer_offsets.data();
+    d.node_count = static_cast<std::uint32_t>(layout->nodes.size());
+    d.node_ids = ids.data();
+    d.row_ptr = rp.data();
+    d.in_nodes = in.data();
+    d.in_weights = w.data();
+    d.n_inputs = static_cast<std::uint32_t>(layout->input_order.size());
+    d.input_order = layout->input_order.data();
+    d.id_bound = layout->id_bound;
+    asnn_dev_layout* dl = nullptr;
+    if (asnn_dev_upload_layout(dev, &d, &dl)) return 6;
+    std::vector<float> state(layout->id_bound);
+    int rc = 0;
+    for (std::uint32_t i = 0; i < warmup + 2 && !rc; ++i)  // the 2nd call captures the sweep graph
+        rc = asnn_dev_activate(dl, x, 1, n_x, nullptr, state.data());
+    std::vector<double> s;
+    for (std::uint32_t i = 0; i < reps && !rc; ++i) {
+        const auto t0 = std::chrono::steady_clock::now();
+        rc = asnn_dev_activate(dl, x, 1, n_x, nullptr, state.data());
+        s.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+    }
+    asnn_dev_free_layout(dl);
+    if (rc) return rc;
+    stats_us(s, mean_us, sd_us);
+    return 0;
 }

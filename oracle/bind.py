@@ -400,6 +400,21 @@ class RefDev(Ref):
         self.L.ref_dev_eval.restype = C.c_int
         self.L.ref_dev_eval.argtypes = [C.c_void_p, f32p, C.c_uint32, f32p]
 
+    def timed(self, rn: "RefNet", x, resident: bool, warmup: int, reps: int):
+        """(mean_us, stddev_us) of eval_parallel(DeviceCompute) per call
+        (resident=False) or of asnn_dev_activate on a layout uploaded once
+        (resident=True), timed inside C++ (integration/asnn_device_backend.cpp)."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        m, sd = C.c_double(), C.c_double()
+        fn = self.L.ref_dev_resident_timed if resident else self.L.ref_dev_eval_timed
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_void_p, f32p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_double),
+                       C.POINTER(C.c_double)]
+        rc = fn(self.L.ref_layout_ptr(rn.h), _p(x, C.c_float), len(x), warmup, reps, C.byref(m), C.byref(sd))
+        if rc:
+            raise RuntimeError(f"device timing failed ({rc})")
+        return m.value, sd.value
+
     def eval_device(self, rn: "RefNet", x):
         """eval_parallel(..., DeviceCompute) on the reference's own LayeredLayout."""
         x = np.ascontiguousarray(x, dtype=np.float32)

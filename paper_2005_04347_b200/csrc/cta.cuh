@@ -117,7 +117,6 @@ __device__ __forceinline__ void stage_prefix(const uint32_t* Rp, const uint32_t*
             if (static_cast<int32_t>(p) < lo) cp_async4(stg + (k << gshift) + q, Ag + static_cast<size_t>(pos) * ldA + q);
         }
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 template <int V, bool GUARD, int MODE = 0, bool WIN = false>
@@ -129,7 +128,7 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
                                             const uint32_t* split = nullptr, Win win = {}) {
     static_assert(!WIN || V == 1, "the windowed variant runs one column per item");
     if constexpr (WIN && MODE == 2)
-        if (win.stg) asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's staged sources
+        if (win.stg) asm volatile("cp.async.wait_group 1;" ::: "memory");  // staged a step ago (not the newest group)
     const uint32_t groups_mask = (1u << gshift) - 1u;
     for (uint32_t it = tid; it < ((b - a) << gshift); it += T) {
         const uint32_t i = it >> gshift, q = it & groups_mask;
@@ -413,11 +412,8 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                         layer_items<V, GUARD, 1, WIN>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base,
                                                       n.n_pos, zero_slot, gtid, Th, pb, pk, Sp, win);
                     } else {
-                        if constexpr (WIN)
-                            if (stg_edges) win.stg = stg_buf + (ll & 1) * stg_edges * C - (static_cast<size_t>(e0 - eb) << gshift);
-                        layer_items<V, GUARD, 2, WIN>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base,
-                                                      n.n_pos, zero_slot, gtid, Th, pb, pk, Sp, win);
-                        // stage layer ll+1's out-of-ring prefix sources for the next step
+                        // stage layer ll+1's out-of-ring prefix sources for the next
+                        // step first: their L2 round trip overlaps this step's work
                         if constexpr (WIN)
                             if (stg_edges && ll + 1 < n.n_layers) {
                                 const uint32_t m2 = ll % kSlots;
@@ -428,11 +424,20 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                                 const uint32_t* Sp2 = m2m[3] ? ring_u32 + m2m[7] : split + n.pos_base + a2;
                                 const uint2* Ep2 = m2m[3] ? ring_u2 + m2m[5] : edges;
                                 const uint32_t eb2 = m2m[3] ? e02 : 0u;
-                                float* st2 = stg_buf + ((ll + 1) & 1) * stg_edges * C - (static_cast<size_t>(e02 - eb2) << gshift);
+                                float* st2 = stg_buf + ((ll + 1) & 1) * stg_edges * C -
+                                             (static_cast<size_t>(e02 - eb2) << gshift);
                                 stage_prefix<GUARD>(Rp2, Sp2, Ep2, eb2, a2, b2, gshift, n.pos_base, n.n_pos,
                                                     static_cast<int32_t>(b) - static_cast<int32_t>(win_mask + 1),
                                                     win0.Ag, ldA, st2, gtid, Th);
                             }
+                        // one group per step, empty or not: wait_group 1 below then
+                        // always means "everything staged before this step"
+                        if constexpr (WIN)
+                            if (stg_edges) asm volatile("cp.async.commit_group;" ::: "memory");
+                        if constexpr (WIN)
+                            if (stg_edges) win.stg = stg_buf + (ll & 1) * stg_edges * C - (static_cast<size_t>(e0 - eb) << gshift);
+                        layer_items<V, GUARD, 2, WIN>(As, Rp, Ep, eb, a, b, ld, gshift, n.pos_base, row_base,
+                                                      n.n_pos, zero_slot, gtid, Th, pb, pk, Sp, win);
                     }
                 }
                 consumer_barrier(Tc);  // layer l final, prefix of l+1 parked

@@ -466,9 +466,11 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     // waves) runs one wave at two CTAs per SM, each keeping only the newest W
     // positions in shared memory and reading older sources from A in L2.
     // ASNN_CTA_WIN=0 disables.
+    // Off by default: on C3 it measured 5.7 ms against 2.68 ms for the two
+    // shared-memory waves (profiles/r2_c3_window.txt).  ASNN_CTA_WIN=1 enables.
     static const bool want_win = [] {
         const char* s = getenv("ASNN_CTA_WIN");
-        return !(s && s[0] == '0');
+        return s && s[0] == '1';
     }();
     // Sweep mode 4 (tests): the windowed variant with the smallest legal ring
     // (W >= 2 x the widest layer: a layer's writes never share a slot).

@@ -238,7 +238,8 @@ int gen_powerlaw(asnn_dev* dev, uint32_t n_nodes, uint32_t bands, uint32_t n_in,
     uint32_t *k1, *v1;
     RCG(radix_sort_pairs(dev, rsrc.p, rtgt.p, R, bits, sb, &k1, &v1, st));  // by source
     uint32_t *k2, *v2;
-    RCG(radix_sort_pairs(dev, v1, k1, R, bits, sb, &k2, &v2, st));          // stably by target
+    SortBuffers sb2;  // v1 / k1 may live in sb's alternates
+    RCG(radix_sort_pairs(dev, v1, k1, R, bits, sb2, &k2, &v2, st));         // stably by target
     DevBuf<uint32_t> keep, kpos, ucnt;
     CKG(keep.alloc(R + 1));
     CKG(kpos.alloc(R + 1));
@@ -259,6 +260,8 @@ int gen_powerlaw(asnn_dev* dev, uint32_t n_nodes, uint32_t bands, uint32_t n_in,
     rtgt.reset();
     sb.k_alt.reset();
     sb.v_alt.reset();
+    sb2.k_alt.reset();
+    sb2.v_alt.reset();
 
     // 4. weights: each target's stream after its source draws
     DevBuf<uint32_t> row;

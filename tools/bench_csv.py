@@ -1,18 +1,23 @@
 """The reference's `asnn bench` protocol (asnn_main.cpp:312-386, bench.cpp)
-with a device row: the same seeded corpus (make_corpus_spec over
+with device rows: the same seeded corpus (make_corpus_spec over
 --connections x --depths, 8 inputs, 2 outputs, SplitMix64 network seeds), the
 reference's sequential (5 reps) and parallel (10 reps) timings of
 eval_sequential / eval_parallel (oracle/_ref, timed inside C++), and the
-DeviceCompute backend through this repo's eval_parallel path.  Writes the
-reference's CSV schema:
+DeviceCompute backend through the maintainer's binding
+(integration/asnn_device_backend.cpp, the drop-in of INTEGRATION.md), also
+timed inside C++.  Writes the reference's CSV schema (
+headers, row order and number format of bench.cpp:103-137):
 
   <prefix>.timings.csv  network_id,connections,layers,backend,repetitions,mean_time_us,stddev_us
-                        (backend: sequential, parallel -- as the reference -- plus
-                         device = eval_parallel(DeviceCompute) per call, layout
-                         upload included, and device_resident = activate on a
-                         resident layout)
-  <prefix>.speedup.csv  network_id,connections,layers,speedup  (sequential / parallel)
-  <prefix>.device_speedup.csv  same columns, sequential / device
+                        backend: sequential, parallel (as the reference), then
+                          device          = eval_parallel(DeviceCompute) per call: the
+                                            reference's LayeredLayout converted, uploaded,
+                                            activated, state back, freed -- every call;
+                          device_resident = asnn_dev_activate on a layout uploaded once
+                                            (state back)
+  <prefix>.speedup.csv                  network_id,connections,layers,speedup  sequential / parallel
+  <prefix>.device_speedup.csv           same columns, sequential / device (per call)
+  <prefix>.device_resident_speedup.csv  same columns, sequential / device_resident
   <prefix>.meta         key=value lines
 
 Usage: python tools/bench_csv.py --connections 1000,10000,100000 --depths 10,100 --csv out/bench
@@ -28,7 +33,7 @@ import numpy as np
 
 sys.path.insert(0, ".")
 import paper_2005_04347_b200 as A  # noqa: E402
-from oracle.bind import Ref  # noqa: E402
+from oracle.bind import RefDev  # noqa: E402
 
 
 def format_double(v: float) -> str:
@@ -80,9 +85,9 @@ def main():
     a = ap.parse_args()
     conns = [int(x) for x in a.connections.split(",")]
     depths = [int(x) for x in a.depths.split(",")]
-    ref = Ref()
+    ref = RefDev()
     master = A.SplitMix64(a.seed)
-    records, speed, dspeed, failures = [], [], [], []
+    records, speed, dspeed, rspeed, failures = [], [], [], [], []
     for d in depths:
         for c in conns:
             nid = f"c{c}_d{d}"
@@ -105,38 +110,20 @@ def main():
 
                 seq = stats(ref_reps(0, a.reps_seq))
                 par = stats(ref_reps(1, a.reps_par))
-                # device: eval_parallel(DeviceCompute) per call (upload + activate)
-                llay = A.LayeredLayout(lay["total_layers"], lay["layer_offsets"], lay["node_ids"],
-                                       lay["row_ptr"], lay["in_nodes"], lay["in_weights"], lay["input_order"],
-                                       lay["dropped_connections"], lay["id_bound"])
-                cfg = A.ParallelConfig(backend=A.Backend.DeviceCompute)
-                for _ in range(a.warmup):
-                    A.eval_parallel(llay, x[0], cfg)
-                samples = []
-                for _ in range(a.reps_par):
-                    t0 = time.perf_counter()
-                    A.eval_parallel(llay, x[0], cfg)
-                    samples.append((time.perf_counter() - t0) * 1e6)
-                dev = stats(samples)
-                dl = A.DeviceLayout.from_layout(llay)
-                for _ in range(max(2, a.warmup)):  # the 2nd call captures the sweep graph
-                    dl.activate(x, outputs=True)
-                samples = []
-                for _ in range(a.reps_par):
-                    t0 = time.perf_counter()
-                    dl.activate(x, outputs=True)
-                    samples.append((time.perf_counter() - t0) * 1e6)
-                res = stats(samples)
-                dl.free()
+                # device rows through the reference-side binding, timed inside C++
+                dev = ref.timed(rn, x[0], resident=False, warmup=a.warmup, reps=a.reps_par)
+                res = ref.timed(rn, x[0], resident=True, warmup=a.warmup, reps=a.reps_par)
                 records += [(nid, n_conn, layers, "sequential", a.reps_seq, *seq),
                             (nid, n_conn, layers, "parallel", a.reps_par, *par),
                             (nid, n_conn, layers, "device", a.reps_par, *dev),
                             (nid, n_conn, layers, "device_resident", a.reps_par, *res)]
                 speed.append((nid, n_conn, layers, seq[0] / par[0]))
-                dspeed.append((nid, n_conn, layers, seq[0] / res[0]))
+                dspeed.append((nid, n_conn, layers, seq[0] / dev[0]))
+                rspeed.append((nid, n_conn, layers, seq[0] / res[0]))
                 print(f"{nid}: seq_us={format_double(seq[0])} par_us={format_double(par[0])} "
                       f"device_us={format_double(dev[0])} resident_us={format_double(res[0])} "
-                      f"speedup={format_double(seq[0] / par[0])} device_speedup={format_double(seq[0] / res[0])}")
+                      f"speedup={format_double(seq[0] / par[0])} device_speedup={format_double(seq[0] / dev[0])} "
+                      f"device_resident_speedup={format_double(seq[0] / res[0])}")
             except Exception as e:  # bench.cpp:105-107: recorded and skipped
                 failures.append((nid, str(e)))
                 print(f"failed {nid}: {e}", file=sys.stderr)
@@ -146,7 +133,8 @@ def main():
         f.write("network_id,connections,layers,backend,repetitions,mean_time_us,stddev_us\n")
         for r in records:
             f.write(f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]},{format_double(r[5])},{format_double(r[6])}\n")
-    for path, rows in ((a.csv + ".speedup.csv", speed), (a.csv + ".device_speedup.csv", dspeed)):
+    for path, rows in ((a.csv + ".speedup.csv", speed), (a.csv + ".device_speedup.csv", dspeed),
+                       (a.csv + ".device_resident_speedup.csv", rspeed)):
         with open(path, "w") as f:
             f.write("network_id,connections,layers,speedup\n")
             for r in sorted(rows):
@@ -159,6 +147,8 @@ def main():
                      ("seed", a.seed), ("connections", a.connections), ("depths", a.depths),
                      ("corpus_inputs", 8), ("corpus_outputs", 2), ("input_value", a.input_value),
                      ("include_preprocessing", 0), ("device_backend", "B200 sm_100a (libasnn_b200.so)"),
+                     ("device_path", "integration/asnn_device_backend.cpp eval_device (per call), "
+                                     "asnn_dev_activate (resident); timed in C++"),
                      ("failures", len(failures))] + [(f"failure_{n}", r) for n, r in failures]:
             f.write(f"{k}={v}\n")
 

@@ -252,6 +252,10 @@ LevelLaunch wide_level(uint32_t tiles) {
         case 6: l.rows = k_rows<LANES, 8, 3>; break;
         case 7: l.rows = k_rows<LANES, 12, 3>; break;
         case 8: l.rows = k_rows<LANES, 16, 2>; break;
+        case 9: l.rows = k_rows_cp<LANES, 8, 5>; break;
+        case 10: l.rows = k_rows_cp<LANES, 6, 6>; break;
+        case 11: l.rows = k_rows_cp<LANES, 12, 4>; break;
+        case 12: l.rows = k_rows_cp<LANES, 4, 8>; break;
         default: l.rows = k_rows<LANES, 8, 4>; break;
     }
     return l;
@@ -545,9 +549,14 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     }();
     p.T = static_cast<uint32_t>(std::min<uint64_t>(tmax, std::max<uint64_t>(32, (items + 31) / 32 * 32)));
     if (p.global) p.pipe = false;
-    if (p.pipe) {  // finish group + prefix group of up to 4 warps each
+    if (p.pipe) {  // finish group + prefix group of up to 8 warps each (one row per
+                   // thread up to 256 items: config 1's ~200-row layers, ASNN_CTA_PIPE_MAX)
+        static const uint64_t gmax = [] {
+            const char* s = getenv("ASNN_CTA_PIPE_MAX");
+            return s ? std::min<uint64_t>(256, std::max(32, atoi(s)) / 32 * 32) : 256;
+        }();
         p.max_items = static_cast<uint32_t>(items);
-        p.T = 2 * static_cast<uint32_t>(std::min<uint64_t>(128, (items + 31) / 32 * 32));
+        p.T = 2 * static_cast<uint32_t>(std::min<uint64_t>(gmax, (items + 31) / 32 * 32));
     }
     const bool latency_bound = L->nets.size() > 1 || L->n_levels >= 24 ||
                                L->total_edges * static_cast<uint64_t>(ldA) <= (1ull << 22);
@@ -627,6 +636,17 @@ cudaError_t upload_host(asnn_dev* dev, void* dst, const void* src, size_t len, c
     return cudaSuccess;
 }
 
+cudaError_t h2d(asnn_dev* dev, void* dst, const void* src, size_t len, cudaStream_t st) {
+    if (!len) return cudaSuccess;
+    const size_t at = (dev->arena_used + 255) & ~size_t(255);
+    if (at + len <= dev->arena.bytes) {  // small: one host memcpy beats a pointer-attribute query
+        std::memcpy(static_cast<char*>(dev->arena.p) + at, src, len);
+        dev->arena_used = at + len;
+        return cudaMemcpyAsync(dst, static_cast<char*>(dev->arena.p) + at, len, cudaMemcpyHostToDevice, st);
+    }
+    return upload_host(dev, dst, src, len, st);
+}
+
 cudaError_t download_host(asnn_dev* dev, void* dst, const void* src, size_t len, cudaStream_t st) {
     if (len < 2 * kStageChunk || page_locked(dst))  // stream-ordered, as the caller expects
         return len ? cudaMemcpyAsync(dst, src, len, cudaMemcpyDeviceToHost, st) : cudaSuccess;
@@ -704,7 +724,7 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
         if (e != cudaSuccess) return cleanup_fail(cuda_fail(dev, e, #expr)); \
     } while (0)
     CKL(d_meta.alloc(meta.size()));
-    CKL(cudaMemcpyAsync(d_meta.p, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, st));
+    CKL(h2d(dev, d_meta.p, meta.data(), meta.size() * 4, st));
     MetaPtrs m{d_meta.p, d_meta.p + (G + 1), d_meta.p + 2 * (G + 1), d_meta.p + 3 * (G + 1),
                d_meta.p + 4 * (G + 1), d_meta.p + 5 * (G + 1), G};
     CKL(bad.alloc(2));
@@ -742,6 +762,7 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
     // positions ordered by in-degree descending (longest rows first, LPT),
     // ties by position.  A stable radix sort of all positions by
     // (level, ~degree); level-0 sensors sort first and are skipped.
+    std::vector<uint32_t> le_host, lo_base_host;
     uint32_t n_levels = 0;
     for (const auto& n : nets) n_levels = std::max(n_levels, n.n_layers);
     L->n_levels = n_levels;
@@ -765,41 +786,13 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
         }
         if (n_levels) L->lvl_off[n_levels] = acc;
         const uint32_t P = L->total_pos;
-        DevBuf<uint32_t> d_lo, d_lob, keys, vals, hv;
+        DevBuf<uint32_t> d_lo, d_lob;
         CKL(d_lo.alloc(lo_cat.size()));
         CKL(d_lob.alloc(G + 1));
-        CKL(keys.alloc(P + 1));
-        CKL(vals.alloc(P + 1));
         if (!lo_cat.empty())
-            CKL(cudaMemcpyAsync(d_lo.p, lo_cat.data(), lo_cat.size() * 4, cudaMemcpyHostToDevice, st));
-        CKL(cudaMemcpyAsync(d_lob.p, lo_base.data(), (G + 1) * 4, cudaMemcpyHostToDevice, st));
-        if (P)
-            k_sched_keys<<<blocks_for(P), kThreads, 0, st>>>(m, d_lo.p, d_lob.p, flat.row_ptr.p, P, keys.p,
-                                                             vals.p);
-        CKL(cudaGetLastError());
-        SortBuffers sb;
-        uint32_t *ks = nullptr, *vs = nullptr;
-        int lb = 0;
-        while ((1u << lb) < n_levels) ++lb;
-        int rc = radix_sort_pairs(dev, keys.p, vals.p, P, std::max(1, lb) + 16, sb, &ks, &vs, st);
-        if (rc) return cleanup_fail(rc);
-        const uint32_t S = L->total_sensors;
-        CKL(L->sched.alloc(P - S + 1));
-        if (P > S)
-            CKL(cudaMemcpyAsync(L->sched.p, vs + S, (P - S) * 4ull, cudaMemcpyDeviceToDevice, st));
-        CKL(L->rtask.alloc(P - S + 1));
-        if (P > S)
-            k_row_tasks<<<blocks_for(P - S), kThreads, 0, st>>>(L->sched.p, flat.row_ptr.p, P - S, L->rtask.p);
-        // heavy-row counts per level for each threshold kHeavyThr[t]
-        const size_t nh = static_cast<size_t>(kNumHeavyThr) * (n_levels + 1);
-        CKL(hv.alloc(nh));
-        CKL(cudaMemsetAsync(hv.p, 0, nh * 4, st));
-        if (P > S)
-            k_heavy_counts<<<blocks_for(P - S), kThreads, 0, st>>>(ks + S, P - S, n_levels + 1, hv.p);
-        CKL(cudaGetLastError());
-        L->heavy_cnt.assign(nh, 0);
-        CKL(cudaMemcpyAsync(L->heavy_cnt.data(), hv.p, nh * 4, cudaMemcpyDeviceToHost, st));
-
+            CKL(h2d(dev, d_lo.p, lo_cat.data(), lo_cat.size() * 4, st));
+        CKL(h2d(dev, d_lob.p, lo_base.data(), (G + 1) * 4, st));
+        (void)P;
         // K-cta metadata: per-network records and layer boundaries as edge offsets
         std::vector<uint32_t> recs(static_cast<size_t>(G) * 12, 0);
         uint32_t sens = 0;
@@ -820,22 +813,19 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
             L->max_pos = std::max(L->max_pos, n.n_pos);
         }
         CKL(L->cta_nets.alloc(recs.size()));
-        CKL(cudaMemcpyAsync(L->cta_nets.p, recs.data(), recs.size() * 4, cudaMemcpyHostToDevice, st));
+        CKL(h2d(dev, L->cta_nets.p, recs.data(), recs.size() * 4, st));
         CKL(L->le_cat.alloc(lo_cat.size() + 1));
         if (!lo_cat.empty())
             k_layer_edges<<<blocks_for(lo_cat.size()), kThreads, 0, st>>>(
                 d_lo.p, d_lob.p, G, m.pos, flat.row_ptr.p, static_cast<uint32_t>(lo_cat.size()),
                 L->le_cat.p);
         CKL(cudaGetLastError());
-        std::vector<uint32_t> le(lo_cat.size());
-        if (!le.empty())
-            CKL(cudaMemcpyAsync(le.data(), L->le_cat.p, le.size() * 4, cudaMemcpyDeviceToHost, st));
-        CKL(cudaStreamSynchronize(st));
-        for (uint32_t g = 0; g < G; ++g)
-            for (uint32_t l = 0; l < nets[g].n_layers; ++l)
-                L->max_level_edges =
-                    std::max(L->max_level_edges, le[lo_base[g] + l + 1] - le[lo_base[g] + l]);
+        le_host.resize(lo_cat.size());
+        lo_base_host = lo_base;
+        if (!le_host.empty())
+            CKL(cudaMemcpyAsync(le_host.data(), L->le_cat.p, le_host.size() * 4, cudaMemcpyDeviceToHost, st));
         L->lo_cat = std::move(d_lo);
+        L->lo_base = std::move(d_lob);
     }
     CKL(L->idb_prefix.alloc(G + 1));
     CKL(cudaMemcpyAsync(L->idb_prefix.p, d_meta.p + (G + 1), (G + 1) * 4, cudaMemcpyDeviceToDevice,
@@ -843,7 +833,12 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
     uint32_t h_bad[2] = {0, 0};
     CKL(cudaMemcpyAsync(h_bad, bad.p, 8, cudaMemcpyDeviceToHost, st));
     CKL(cudaMemcpyAsync(&L->max_deg, maxdeg.p, 4, cudaMemcpyDeviceToHost, st));
-    CKL(cudaStreamSynchronize(st));
+    CKL(cudaStreamSynchronize(st));  // the one synchronisation of a layout build
+    arena_reset(dev);
+    for (uint32_t g = 0; g < G; ++g)
+        for (uint32_t l = 0; l < nets[g].n_layers; ++l)
+            L->max_level_edges =
+                std::max(L->max_level_edges, le_host[lo_base_host[g] + l + 1] - le_host[lo_base_host[g] + l]);
 #undef CKL
     if (h_bad[0] & 7u) {
         delete L;
@@ -851,6 +846,7 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
                     "layout references an id >= id_bound (code " + std::to_string(h_bad[0]) + ")");
     }
     L->zero_refs = (h_bad[0] & 8u) != 0;
+    L->d_meta = std::move(d_meta);
     L->row_ptr = std::move(flat.row_ptr);
     L->node_ids = std::move(flat.node_ids);
     L->nets = std::move(nets);
@@ -865,6 +861,53 @@ namespace {
 
 template <typename Mark>
 int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark);
+
+// The per-level launch schedule (built on first use: K-cta sweeps -- small,
+// deep and population layouts, the per-call drop-in -- never need it).
+// Level-major: global level l runs layer l of every network, its positions
+// ordered by in-degree descending (longest rows first, LPT), ties by
+// position -- a stable radix sort of all positions by (level, ~degree);
+// level-0 sensors sort first and are skipped.  Plus the heavy-row counts
+// per level for every threshold heavy_thr(t).
+int ensure_schedule(asnn_dev_layout* L) {
+    if (L->sched_ready) return ASNN_OK;
+    asnn_dev* dev = L->dev;
+    cudaStream_t st = dev->stream;
+    const uint32_t G = static_cast<uint32_t>(L->nets.size());
+    const uint32_t n_levels = L->n_levels;
+    const uint32_t P = L->total_pos;
+    MetaPtrs m{L->d_meta.p, L->d_meta.p + (G + 1), L->d_meta.p + 2 * (G + 1), L->d_meta.p + 3 * (G + 1),
+               L->d_meta.p + 4 * (G + 1), L->d_meta.p + 5 * (G + 1), G};
+    DevBuf<uint32_t> keys, vals, hv;
+    CK(keys.alloc(P + 1));
+    CK(vals.alloc(P + 1));
+    if (P)
+        k_sched_keys<<<blocks_for(P), kThreads, 0, st>>>(m, L->lo_cat.p, L->lo_base.p, L->row_ptr.p, P, keys.p,
+                                                         vals.p);
+    CK(cudaGetLastError());
+    SortBuffers sb;
+    uint32_t *ks = nullptr, *vs = nullptr;
+    int lb = 0;
+    while ((1u << lb) < n_levels) ++lb;
+    int rc = radix_sort_pairs(dev, keys.p, vals.p, P, std::max(1, lb) + 16, sb, &ks, &vs, st);
+    if (rc) return rc;
+    const uint32_t S = L->total_sensors;
+    CK(L->sched.alloc(P - S + 1));
+    if (P > S) CK(cudaMemcpyAsync(L->sched.p, vs + S, (P - S) * 4ull, cudaMemcpyDeviceToDevice, st));
+    CK(L->rtask.alloc(P - S + 1));
+    if (P > S) k_row_tasks<<<blocks_for(P - S), kThreads, 0, st>>>(L->sched.p, L->row_ptr.p, P - S, L->rtask.p);
+    const size_t nh = static_cast<size_t>(kNumHeavyThr) * (n_levels + 1);
+    CK(hv.alloc(nh));
+    CK(cudaMemsetAsync(hv.p, 0, nh * 4, st));
+    if (P > S) k_heavy_counts<<<blocks_for(P - S), kThreads, 0, st>>>(ks + S, P - S, n_levels + 1, hv.p);
+    CK(cudaGetLastError());
+    L->heavy_cnt.assign(nh, 0);
+    CK(cudaMemcpyAsync(L->heavy_cnt.data(), hv.p, nh * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    L->sched_ready = true;
+    return ASNN_OK;
+}
+
 
 // ---- heavy-row segments (segments.cuh) --------------------------------------
 // Shortest interrupted segment and longest segment k_rows takes (longer ones
@@ -895,6 +938,10 @@ uint64_t seg_key_for(const asnn_dev_layout* L) {
 int ensure_segments(asnn_dev_layout* L) {
     asnn_dev* dev = L->dev;
     cudaStream_t st = dev->stream;
+    {
+        const int rc = ensure_schedule(L);
+        if (rc) return rc;
+    }
     const NetMeta& n = L->nets[0];
     const int thr = heavy_index_for(dev->heavy_threshold);
     const uint32_t NL = L->n_levels;
@@ -1139,6 +1186,10 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
 int ensure_workspace(asnn_dev_layout* L, uint32_t n_vec) {
     asnn_dev* dev = L->dev;
     const uint32_t ldA = padded_batch(n_vec);
+    if (!cta_plan(L, ldA).use) {
+        const int rc = ensure_schedule(L);
+        if (rc) return rc;
+    }
     if (cta_plan(L, ldA).pipe && !L->split.p) {
         L->graph.reset();
         CK(L->split.alloc(L->total_pos + 8));  // slack: K-cta bulk copies round up to 16 bytes
@@ -1475,6 +1526,14 @@ int asnn_dev_upload_layout(asnn_dev* dev, const asnn_layout_desc* d, asnn_dev_la
         if (bad) return fail(dev, ASNN_E_INVALID, "row_ptr decreases");
     }
     cudaStream_t st = dev->stream;
+    // small layouts (the per-call drop-in): every host array through the
+    // pinned arena, one asynchronous DMA each
+    {
+        const uint64_t bytes = 12ull * d->node_count + 8 * E + 4ull * (d->n_inputs + d->n_outputs) +
+                               64ull * (d->total_layers + 64);
+        arena_reset(dev);
+        if (bytes <= (64ull << 20)) CK(dev->arena.ensure(std::max<uint64_t>(bytes + (1 << 16), 1 << 20)));
+    }
     CK(cudaEventRecord(dev->ev0, st));
     NetMeta n;
     n.n_pos = d->node_count;
@@ -1497,21 +1556,21 @@ int asnn_dev_upload_layout(asnn_dev* dev, const asnn_layout_desc* d, asnn_dev_la
     CK(f.inputs.alloc(d->n_inputs));
     CK(f.outputs.alloc(d->n_outputs));
     if (d->node_count) {
-        CK(cudaMemcpyAsync(f.node_ids.p, d->node_ids, d->node_count * 4ull, cudaMemcpyHostToDevice, st));
-        CK(upload_host(dev, row64.p, d->row_ptr, (d->node_count + 1) * 8ull, st));
+        CK(h2d(dev, f.node_ids.p, d->node_ids, d->node_count * 4ull, st));
+        CK(h2d(dev, row64.p, d->row_ptr, (d->node_count + 1) * 8ull, st));
         k_row64_to_32<<<blocks_for(d->node_count + 1), kThreads, 0, st>>>(row64.p, d->node_count + 1,
                                                                            f.row_ptr.p);
     } else {
         CK(cudaMemsetAsync(f.row_ptr.p, 0, 4, st));
     }
     if (E) {
-        CK(upload_host(dev, f.in_ids.p, d->in_nodes, E * 4, st));
-        CK(upload_host(dev, f.w.p, d->in_weights, E * 4, st));
+        CK(h2d(dev, f.in_ids.p, d->in_nodes, E * 4, st));
+        CK(h2d(dev, f.w.p, d->in_weights, E * 4, st));
     }
     if (d->n_inputs)
-        CK(cudaMemcpyAsync(f.inputs.p, d->input_order, d->n_inputs * 4ull, cudaMemcpyHostToDevice, st));
+        CK(h2d(dev, f.inputs.p, d->input_order, d->n_inputs * 4ull, st));
     if (d->n_outputs)
-        CK(cudaMemcpyAsync(f.outputs.p, d->outputs, d->n_outputs * 4ull, cudaMemcpyHostToDevice, st));
+        CK(h2d(dev, f.outputs.p, d->outputs, d->n_outputs * 4ull, st));
     std::vector<NetMeta> nets;
     nets.push_back(std::move(n));
     int rc = assemble_layout(dev, std::move(nets), std::move(f), out);
@@ -1629,6 +1688,7 @@ static uint32_t sweep_launches(asnn_dev_layout* L, uint32_t n_vec, bool stages, 
         // unless it is the global-memory variant
         return 1u + (with_out && cp.global && L->total_out ? 1u : 0u);
     } else {
+        if (ensure_schedule(L)) return 0;
         const int thr = heavy_index_for(L->dev->heavy_threshold);
         const bool heavy = heavy_launch_for(ldA).fn && thr >= 0;
         const bool segs = seg_eligible(L, ldA);

@@ -136,6 +136,8 @@ struct asnn_dev {
     asnn_timings timings{};
     asnn_b200::PinnedBuf pin_x, pin_out;  // pinned staging of pageable host buffers (all layouts)
     asnn_b200::PinnedBuf stage[2];        // double-buffered staging of large pageable transfers
+    asnn_b200::PinnedBuf arena;           // small uploads of one layout build, bump-allocated (h2d)
+    size_t arena_used = 0;
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     // NCCL communicator this device belongs to (group.cu): one rank of a
     // multi-process job (asnn_dev_comm_init) or a member of an asnn_group
@@ -153,6 +155,13 @@ namespace asnn_b200 {
 // filled); the direct ones are ordinary stream-ordered copies.
 cudaError_t upload_host(asnn_dev* dev, void* dst, const void* src, size_t len, cudaStream_t st);
 cudaError_t download_host(asnn_dev* dev, void* dst, const void* src, size_t len, cudaStream_t st);
+// A host -> device copy inside a layout build: pageable sources are packed
+// into the handle's pinned arena (one host memcpy, then an asynchronous DMA
+// instead of the driver's synchronous pageable path); the build synchronises
+// before it returns, after which arena_reset() recycles it.  Large or
+// non-fitting copies take upload_host.
+cudaError_t h2d(asnn_dev* dev, void* dst, const void* src, size_t len, cudaStream_t st);
+inline void arena_reset(asnn_dev* dev) { dev->arena_used = 0; }
 
 // In-degree thresholds above which a row goes to the streamed heavy kernel.
 constexpr int kNumHeavyThr = 9;
@@ -217,6 +226,9 @@ struct asnn_dev_layout {
     asnn_b200::DevBuf<uint32_t> state_map;  // [total_idb] id -> pos
     asnn_b200::DevBuf<uint32_t> idb_prefix; // [n_nets + 1]
     asnn_b200::DevBuf<uint32_t> node_ids;   // [total_pos]
+    asnn_b200::DevBuf<uint32_t> d_meta;     // per-network prefix tables (MetaPtrs)
+    asnn_b200::DevBuf<uint32_t> lo_base;    // [n_nets + 1] offsets into lo_cat
+    bool sched_ready = false;               // sched / rtask / heavy_cnt built (ensure_schedule)
 
     // activation workspace
     asnn_b200::DevBuf<float> A;

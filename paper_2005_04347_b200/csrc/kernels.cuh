@@ -222,6 +222,94 @@ k_rows(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ldA,
 }
 
 // ---------------------------------------------------------------------------
+// K-rows-cp: k_rows with the source-row gathers staged through shared memory
+// by cp.async instead of registers (L2-bound levels: config 2's 2 MB level
+// slabs).  Every lane keeps D gathers of its 16-byte column quad in flight
+// in its own ring slot column (it reads back only what it copied itself, so
+// no synchronisation beyond cp.async.wait_group), the edge records
+// prefetched into L1 two rounds ahead; the data registers k_rows spends on the U
+// in-flight gathers are freed, so more warps per SM keep more bytes in
+// flight.  Same items, same in-order __fmul_rn / __fadd_rn chain, bitwise
+// identical to k_rows.
+__device__ __forceinline__ void rows_cp16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+template <int LANES, int D, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+k_rows_cp(const uint2* __restrict__ edges, float* __restrict__ A, uint32_t ldA,
+          const uint4* __restrict__ rows, uint32_t n_rows, uint32_t tiles, const uint4* __restrict__ seg,
+          uint32_t n_seg, float* __restrict__ accbuf) {
+    __shared__ __align__(16) float4 ring[D][256];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t item = gt / LANES;
+    const uint32_t ni = item / tiles;
+    if (ni >= n_seg + n_rows) return;  // uniform across the LANES group
+    const uint32_t lane = threadIdx.x % LANES;
+    const uint32_t tile = item - ni * tiles;
+    const uint4 t = ni < n_seg ? __ldg(&seg[ni]) : __ldg(&rows[ni - n_seg]);
+    const uint32_t node = t.x, beg = t.y, end = t.z, aux = t.w;
+    const uint32_t col = tile * (LANES * 4) + lane * 4;
+    const uint32_t stride = ldA * 4u;
+    const char* __restrict__ Acol = reinterpret_cast<const char*>(A + col);
+    float4* my = &ring[0][threadIdx.x];
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(edges + beg));
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    float w[D];
+    // prologue: the first D gathers in flight
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+        if (beg + u < end) {
+            const uint2 e = __ldg(&edges[beg + u]);
+            w[u] = __uint_as_float(e.y);
+            rows_cp16(my + u * 256, Acol + static_cast<uint64_t>(e.x) * stride);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    if (aux & kAccLoad) {
+        const float4 p = *reinterpret_cast<const float4*>(accbuf + static_cast<uint64_t>(aux & kSlotMask) * ldA + col);
+        a0 = p.x, a1 = p.y, a2 = p.z, a3 = p.w;
+    }
+    for (uint32_t base = beg; base < end; base += D) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(edges + base + 2 * D));
+#pragma unroll
+        for (int u = 0; u < D; ++u) {
+            const uint32_t k = base + u;
+            asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");  // edge k's row landed
+            if (k < end) {
+                const float4 v = my[u * 256];
+                a0 = mac(a0, w[u], v.x);
+                a1 = mac(a1, w[u], v.y);
+                a2 = mac(a2, w[u], v.z);
+                a3 = mac(a3, w[u], v.w);
+            }
+            // refill slot u with edge k + D
+            if (k + D < end) {
+                const uint2 e = __ldg(&edges[k + D]);
+                w[u] = __uint_as_float(e.y);
+                rows_cp16(my + u * 256, Acol + static_cast<uint64_t>(e.x) * stride);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (aux & kAccStore) {
+        *reinterpret_cast<float4*>(accbuf + static_cast<uint64_t>(aux & kSlotMask) * ldA + col) =
+            make_float4(a0, a1, a2, a3);
+    } else {
+        float o[4] = {a0, a1, a2, a3};
+        sigmoid32_v<4>(o);
+        *reinterpret_cast<float4*>(A + static_cast<uint64_t>(node) * ldA + col) = make_float4(o[0], o[1], o[2], o[3]);
+        wc_note(node, col, 4);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K-warp-rows: one warp per row for a single input vector (batch 1, the
 // reference's eval_parallel call).  The 32 lanes load 32 consecutive edges
 // and their source activations at once (32 gathers in flight per row instead

@@ -38,23 +38,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(heavy::smem_u32(bar))
         : "memory");
 }
-// The producer's waits for ring space: it runs ahead of the consumers, so
-// back off between polls instead of spinning -- a spinning producer warp
-// takes issue slots from the consumer warp sharing its SM sub-partition
-// (two CTAs per SM in the windowed variant).
+// The producer's waits for ring space: it runs ahead of the consumers, so it
+// waits suspended in the hardware (try_wait with a suspend-time hint, woken
+// when the phase completes) instead of spinning -- a spinning producer warp
+// takes issue slots from the consumer warp sharing its SM sub-partition.  (A
+// __nanosleep back-off oversleeps: on config 3 under K-chain it held the
+// staging rate to one layer per ~1250 cycles.)
 __device__ __forceinline__ void producer_wait(uint64_t* b, uint32_t parity) {
-    for (;;) {
-        uint32_t ok;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n}"
-            : "=r"(ok)
-            : "r"(heavy::smem_u32(b)), "r"(parity)
-            : "memory");
-        if (ok) return;
-        __nanosleep(200);
-    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "PWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra PWAIT_%=;\n}" ::"r"(heavy::smem_u32(b)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
 }
 __device__ __forceinline__ void consumer_barrier(uint32_t n_threads) {
     asm volatile("bar.sync 1, %0;" ::"r"(n_threads) : "memory");
@@ -218,6 +215,183 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
 }
 }  // namespace cta
 
+#ifdef ASNN_CHAIN_PROF
+static __device__ long long g_issue_clk[4096];
+static __device__ long long g_trace[5][4096];  // issue, P full ready, P done, F done, producer space-wait start
+#endif
+namespace cta {
+constexpr uint32_t kSlots = 32;
+constexpr uint32_t kMetaBytes = kSlots * (8 + 8 + 32);
+
+// The producer (one warp; lane 0 issues the copies): stages layers
+// 1..n_layers-1 in order into the ring.  The layer bounds (lo, le) are read
+// 32 layers at a time by the warp's lanes and broadcast with __shfl, the next
+// window loaded one window ahead: a dependent L2 round trip per layer capped
+// the staging rate at ~1 layer / 1000 cycles (config 3 under K-chain).  meta[m] = {a, b, e0, staged, row index, edge index, extent, split
+// index} of the layer using slot m; the extent (its bytes plus the wasted tail
+// when it wrapped) is what its release frees, so the live bytes are always
+// [w - used, w) modulo the ring.  SPLIT: the layer's split[] slice is staged
+// too.  keep: the newest layers whose release the producer never waits for
+// (the consumers need them staged before they release the older ones) --
+// such a layer is read from global memory instead.
+template <bool SPLIT>
+__device__ __forceinline__ void produce(const CtaNet& n, const uint32_t* __restrict__ lo_cat,
+                                        const uint32_t* __restrict__ le_cat, const uint32_t* __restrict__ row_ptr,
+                                        const uint32_t* __restrict__ split, const uint2* __restrict__ edges,
+                                        unsigned char* ring, uint32_t ring_bytes, uint64_t* full, uint64_t* empty,
+                                        uint32_t* meta, int write_all, uint32_t keep, uint32_t lane) {
+#ifdef ASNN_CHAIN_PROF
+#define PROD_T0(v) const long long v = clock64()
+#define PROD_T1(v, acc) acc += clock64() - v
+    long long w_slot = 0, w_space = 0, w_issue = 0, w_total = 0;
+    const long long t_start = clock64();
+#else
+#define PROD_T0(v)
+#define PROD_T1(v, acc)
+#endif
+    uint32_t n_space = 0, n_global = 0;
+    (void)n_space, (void)n_global;
+    const uint32_t* lo = lo_cat + n.lo_base;
+    const uint32_t* le = le_cat + n.lo_base;
+    uint32_t w = 0;       // next write offset in the ring
+    uint32_t used = 0;    // bytes of layers in flight (incl. wrap gaps)
+    uint32_t oldest = 1;  // oldest layer whose release the producer has not seen
+    auto release_to = [&](uint32_t upto) {  // layers < upto are released
+        for (; oldest < upto; ++oldest) used -= meta[8 * ((oldest - 1) % kSlots) + 6];
+    };
+    // window [base, base + 32) of layer bounds in lanes (lo_c, le_c), the next
+    // one (base + 31: windows overlap by one so l and l + 1 share one) in flight
+    uint32_t base = 1, lo_c, le_c, lo_n, le_n;
+    {
+        const uint32_t i0 = min(base + lane, n.n_layers), i1 = min(base + 31 + lane, n.n_layers);
+        lo_c = lo[i0], le_c = le[i0], lo_n = lo[i1], le_n = le[i1];
+    }
+    const bool leader = lane == 0;
+    for (uint32_t l = 1; l < n.n_layers; ++l) {
+        if (l - base == 31) {
+            base += 31;
+            lo_c = lo_n, le_c = le_n;
+            const uint32_t i1 = min(base + 31 + lane, n.n_layers);
+            lo_n = lo[i1], le_n = le[i1];
+        }
+        const uint32_t m = (l - 1) % kSlots, u = (l - 1) / kSlots;
+        const uint32_t a = __shfl_sync(0xFFFFFFFFu, lo_c, l - base), b = __shfl_sync(0xFFFFFFFFu, lo_c, l - base + 1);
+        const uint32_t e0 = __shfl_sync(0xFFFFFFFFu, le_c, l - base), e1 = __shfl_sync(0xFFFFFFFFu, le_c, l - base + 1);
+        const uint32_t r0 = n.pos_base + a, r0a = r0 & ~3u;
+        const uint32_t rbytes = ((b - a + 1 + (r0 - r0a)) * 4 + 15) & ~15u;
+        // the layer's split[] slice too (same alignment as row_ptr)
+        const uint32_t sbytes = SPLIT ? ((b - a + (r0 - r0a)) * 4 + 15) & ~15u : 0u;
+        const uint32_t e0a = e0 & ~1u;
+        const uint32_t ebytes = ((e1 - e0 + (e0 - e0a)) * 8 + 15) & ~15u;
+        const uint32_t size = rbytes + sbytes + ebytes;
+        if (u > 0) {  // slot m's previous layer (l - kSlots) and all before it are released
+            PROD_T0(t0);
+            producer_wait(&empty[m], (u - 1) & 1);
+            PROD_T1(t0, w_slot);
+            release_to(l - kSlots + 1);
+        }
+        bool staged = size <= ring_bytes && !(write_all & 2);
+        uint32_t at = 0, extent = 0;
+        if (staged) {
+            for (;;) {
+                if (used == 0) w = 0;
+                const bool wrap = w + size > ring_bytes;
+                const uint32_t need = wrap ? ring_bytes - w + size : size;
+                if (need <= ring_bytes - used) {
+                    at = wrap ? 0u : w;
+                    extent = need;
+                    w = at + size;
+                    used += need;
+                    break;
+                }
+                // pipelined consumers: layer l-1 is released only after the
+                // step that also needs layer l (its prefix): never wait for
+                // it -- layer l is then read from global memory instead
+                if (keep && oldest + keep >= l) {
+                    staged = false;
+                    break;
+                }
+                PROD_T0(t1);
+#ifdef ASNN_CHAIN_PROF
+                if (blockIdx.x == 0 && blockIdx.y == 0 && l < 4096 && leader) g_trace[4][l] = oldest;
+#endif
+                producer_wait(&empty[(oldest - 1) % kSlots], ((oldest - 1) / kSlots) & 1);
+                PROD_T1(t1, w_space);
+                ++n_space;
+                release_to(oldest + 1);
+            }
+        }
+        if (leader) {
+            uint32_t* mm = meta + 8 * m;
+            mm[0] = a;
+            mm[1] = b;
+            mm[2] = e0;
+            mm[3] = staged ? 1u : 0u;
+            mm[4] = at / 4 + (r0 - r0a);
+            mm[5] = (at + rbytes + sbytes) / 8 + (e0 - e0a);
+            mm[6] = extent;
+            mm[7] = (at + rbytes) / 4 + (r0 - r0a);
+#ifdef ASNN_CHAIN_PROF
+            if (blockIdx.x == 0 && blockIdx.y == 0 && l < 4096) g_issue_clk[l] = clock64();
+#endif
+            if (staged) {
+                PROD_T0(t2);
+                expect_tx(&full[m], size);
+                bulk_g2s(ring + at, row_ptr + r0a, rbytes, &full[m]);
+                if (sbytes) bulk_g2s(ring + at + rbytes, split + r0a, sbytes, &full[m]);
+                if (ebytes) bulk_g2s(ring + at + rbytes + sbytes, edges + e0a, ebytes, &full[m]);
+                PROD_T1(t2, w_issue);
+            } else {
+                heavy::mbar_arrive(&full[m]);
+                ++n_global;
+            }
+        }
+        __syncwarp();  // the extent in meta is read by every lane's release_to
+    }
+#ifdef ASNN_CHAIN_PROF
+    if (blockIdx.x == 0 && blockIdx.y == 0 && leader)
+        printf("producer: total %lld, slot waits %lld cycles, space waits %lld cycles (%u), issue %lld, unstaged layers %u, ring %u\n",
+               clock64() - t_start, w_slot, w_space, n_space, w_issue, n_global, ring_bytes);
+#endif
+}
+}  // namespace cta
+
+namespace cta {
+// Write back after the sweep: every row (state requested) or only the
+// declared outputs, from the CTA's shared-memory rows As ([n_pos][C]).
+__device__ __forceinline__ void write_back(const CtaNet& n, const float* As, uint32_t C, float* __restrict__ A,
+                                           uint32_t ldA, uint32_t c0, uint32_t n_vec,
+                                           const uint4* __restrict__ oinfo, float* __restrict__ out,
+                                           int write_all, uint32_t tid, uint32_t T) {
+    const uint32_t ncols = min(C, ldA - c0);
+    if (write_all & 1) {
+        for (uint32_t i = tid; i < n.n_pos * ncols; i += T) {
+            const uint32_t p = i / ncols, c = i - p * ncols;
+            A[static_cast<uint64_t>(n.pos_base + p) * ldA + c0 + c] = As[p * C + c];
+        }
+    } else if (out) {
+        // read_outputs (eval.cpp:82-87) straight from shared memory into the
+        // caller's [net][vector][output] buffer (device or mapped host memory):
+        // no output gather launch, and the writes of finished CTAs overlap the
+        // sweeps of the others
+        const uint32_t vcols = c0 < n_vec ? min(C, n_vec - c0) : 0u;
+        for (uint32_t i = tid; i < n.n_out * vcols; i += T) {
+            const uint32_t c = i / n.n_out, j = i - c * n.n_out;
+            const uint32_t pos = oinfo[n.out_prefix + j].x;
+            out[static_cast<uint64_t>(n_vec) * n.out_prefix + static_cast<uint64_t>(c0 + c) * n.n_out + j] =
+                pos != kUnassigned ? As[(pos - n.pos_base) * C + c] : 0.0f;
+        }
+    } else {
+        for (uint32_t i = tid; i < n.n_out * ncols; i += T) {
+            const uint32_t j = i / ncols, c = i - j * ncols;
+            const uint32_t pos = oinfo[n.out_prefix + j].x;
+            if (pos != kUnassigned)
+                A[static_cast<uint64_t>(pos) * ldA + c0 + c] = As[(pos - n.pos_base) * C + c];
+        }
+    }
+}
+}  // namespace cta
+
 // Block = consumer warps + 1 producer warp (the last).  Shared memory:
 // [As[(max_pos+1)*C, 16-B rounded; row max_pos is zeros] unless GLOBAL] |
 // ring[ring_bytes] | full[kSlots], empty[kSlots] u64 | meta[kSlots][8] u32.
@@ -228,10 +402,6 @@ __device__ __forceinline__ void layer_items(float* As, const uint32_t* Rp, const
 // sized by the largest one.  Layers larger than the ring (or every layer in
 // debug mode 2) are read from global memory.  Layer l uses mbarrier pair
 // (l-1) % kSlots for its ((l-1) / kSlots)-th time.
-namespace cta {
-constexpr uint32_t kSlots = 32;
-constexpr uint32_t kMetaBytes = kSlots * (8 + 8 + 32);
-}  // namespace cta
 
 //
 // PIPE (latency-bound layers: at most two warps of items): the consumers form
@@ -288,78 +458,8 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     __syncthreads();
 
     if (tid >= Tc) {
-        if (tid == Tc) {
-            // producer.  meta[m] = {a, b, e0, staged, row index, edge index,
-            // extent} of the layer using slot m; the extent (its bytes plus
-            // the wasted tail when it wrapped) is what its release frees, so
-            // the live bytes are always [w - used, w) modulo the ring.
-            const uint32_t* lo = lo_cat + n.lo_base;
-            const uint32_t* le = le_cat + n.lo_base;
-            uint32_t w = 0;       // next write offset in the ring
-            uint32_t used = 0;    // bytes of layers in flight (incl. wrap gaps)
-            uint32_t oldest = 1;  // oldest layer whose release the producer has not seen
-            auto release_to = [&](uint32_t upto) {  // layers < upto are released
-                for (; oldest < upto; ++oldest) used -= meta[8 * ((oldest - 1) % kSlots) + 6];
-            };
-            for (uint32_t l = 1; l < n.n_layers; ++l) {
-                const uint32_t m = (l - 1) % kSlots, u = (l - 1) / kSlots;
-                const uint32_t a = lo[l], b = lo[l + 1];
-                const uint32_t e0 = le[l], e1 = le[l + 1];
-                const uint32_t r0 = n.pos_base + a, r0a = r0 & ~3u;
-                const uint32_t rbytes = ((b - a + 1 + (r0 - r0a)) * 4 + 15) & ~15u;
-                // PIPE: the layer's split[] slice too (same alignment as row_ptr)
-                const uint32_t sbytes = PIPE ? ((b - a + (r0 - r0a)) * 4 + 15) & ~15u : 0u;
-                const uint32_t e0a = e0 & ~1u;
-                const uint32_t ebytes = ((e1 - e0 + (e0 - e0a)) * 8 + 15) & ~15u;
-                const uint32_t size = rbytes + sbytes + ebytes;
-                if (u > 0) {  // slot m's previous layer (l - kSlots) and all before it are released
-                    producer_wait(&empty[m], (u - 1) & 1);
-                    release_to(l - kSlots + 1);
-                }
-                bool staged = size <= ring_bytes && !(write_all & 2);
-                uint32_t at = 0, extent = 0;
-                if (staged) {
-                    for (;;) {
-                        if (used == 0) w = 0;
-                        const bool wrap = w + size > ring_bytes;
-                        const uint32_t need = wrap ? ring_bytes - w + size : size;
-                        if (need <= ring_bytes - used) {
-                            at = wrap ? 0u : w;
-                            extent = need;
-                            w = at + size;
-                            used += need;
-                            break;
-                        }
-                        // PIPE: layer l-1 is released only after the step that
-                        // also needs layer l (its prefix): never wait for it --
-                        // layer l is then read from global memory instead
-                        if (PIPE && oldest + (WIN && stg_edges ? 2u : 1u) >= l) {
-                            staged = false;
-                            break;
-                        }
-                        producer_wait(&empty[(oldest - 1) % kSlots], ((oldest - 1) / kSlots) & 1);
-                        release_to(oldest + 1);
-                    }
-                }
-                uint32_t* mm = meta + 8 * m;
-                mm[0] = a;
-                mm[1] = b;
-                mm[2] = e0;
-                mm[3] = staged ? 1u : 0u;
-                mm[4] = at / 4 + (r0 - r0a);
-                mm[5] = (at + rbytes + sbytes) / 8 + (e0 - e0a);
-                mm[6] = extent;
-                mm[7] = (at + rbytes) / 4 + (r0 - r0a);
-                if (staged) {
-                    expect_tx(&full[m], size);
-                    bulk_g2s(ring + at, row_ptr + r0a, rbytes, &full[m]);
-                    if (sbytes) bulk_g2s(ring + at + rbytes, split + r0a, sbytes, &full[m]);
-                    if (ebytes) bulk_g2s(ring + at + rbytes + sbytes, edges + e0a, ebytes, &full[m]);
-                } else {
-                    heavy::mbar_arrive(&full[m]);
-                }
-            }
-        }
+        cta::produce<PIPE>(n, lo_cat, le_cat, row_ptr, split, edges, ring, ring_bytes, full, empty, meta,
+                           write_all, PIPE ? (WIN && stg_edges ? 2u : 1u) : 0u, tid - Tc);
     } else {
         if constexpr (!GLOBAL)
             for (uint32_t c = tid; c < C; c += Tc) As[zero_slot * C + c] = 0.0f;
@@ -466,44 +566,18 @@ k_cta(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
     if constexpr (GLOBAL || WIN) return;  // the activations are already in A
     __syncthreads();
 
-    // write back: every row (state requested) or only the declared outputs
-    const uint32_t T = blockDim.x;
-    const uint32_t ncols = min(C, ldA - c0);
-    if (write_all & 1) {
-        for (uint32_t i = tid; i < n.n_pos * ncols; i += T) {
-            const uint32_t p = i / ncols, c = i - p * ncols;
-            A[static_cast<uint64_t>(n.pos_base + p) * ldA + c0 + c] = As[p * C + c];
-        }
-    } else if (out) {
-        // read_outputs (eval.cpp:82-87) straight from shared memory into the
-        // caller's [net][vector][output] buffer (device or mapped host memory):
-        // no output gather launch, and the writes of finished CTAs overlap the
-        // sweeps of the others
-        const uint32_t vcols = c0 < n_vec ? min(C, n_vec - c0) : 0u;
-        for (uint32_t i = tid; i < n.n_out * vcols; i += T) {
-            const uint32_t c = i / n.n_out, j = i - c * n.n_out;
-            const uint32_t pos = oinfo[n.out_prefix + j].x;
-            out[static_cast<uint64_t>(n_vec) * n.out_prefix + static_cast<uint64_t>(c0 + c) * n.n_out + j] =
-                pos != kUnassigned ? As[(pos - n.pos_base) * C + c] : 0.0f;
-        }
-    } else {
-        for (uint32_t i = tid; i < n.n_out * ncols; i += T) {
-            const uint32_t j = i / ncols, c = i - j * ncols;
-            const uint32_t pos = oinfo[n.out_prefix + j].x;
-            if (pos != kUnassigned)
-                A[static_cast<uint64_t>(pos) * ldA + c0 + c] = As[(pos - n.pos_base) * C + c];
-        }
-    }
+    cta::write_back(n, As, C, A, ldA, c0, n_vec, oinfo, out, write_all, tid, blockDim.x);
 }
 
 // split[p] for every non-sensor position p of network blockIdx.y: the first
-// stored edge (ascending source id) whose source is on layer level(p) - 1,
-// as an absolute edge index; the edges before it have all their sources on
-// layers <= level(p) - 2.  Sources outside the network (the zero row) count
-// as layer 0.
+// stored edge (ascending source id) whose source is on a layer >= level(p) -
+// D, as an absolute edge index; the edges before it have all their sources on
+// layers <= level(p) - D - 1 (K-cta's pipelined consumers use D = 1, K-chain
+// D = its prefix groups - 1).  Sources outside the network (the zero row)
+// count as layer 0.
 __global__ void k_splits(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat,
                          const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges,
-                         uint32_t* __restrict__ split) {
+                         uint32_t* __restrict__ split, uint32_t D) {
     const CtaNet n = nets[blockIdx.y];
     const uint32_t lp = blockIdx.x * blockDim.x + threadIdx.x;
     if (lp >= n.n_pos || lp < n.n_sensors) return;
@@ -524,7 +598,7 @@ __global__ void k_splits(const CtaNet* __restrict__ nets, const uint32_t* __rest
     for (; k < e1; ++k) {
         const uint32_t src = edges[k].x;
         const uint32_t ls = src - n.pos_base < n.n_pos ? layer_of(src - n.pos_base) : 0u;
-        if (ls + 1 >= lv) break;
+        if (ls + D >= lv) break;
     }
     split[p] = k;
 }

@@ -381,9 +381,17 @@ struct CtaPlan {
     bool win = false;     // ring of the newest positions in shared memory + A (cta.cuh Win)
     uint32_t win_mask = 0;
     uint32_t stg_edges = 0;  // WIN + pipe: staged prefix sources per layer (0 = direct loads)
+    uint32_t chain_nf = 0;   // K-chain (chain.cuh): finish warps (0 = not used)
 };
 
+// K-chain's prefix groups for NF finish warps: four (prefix depth D = 3) while
+// NF x 5 warps + the producer fit the 544-thread bound, else three (D = 2).
+constexpr uint32_t chain_np(uint32_t nf) { return nf <= 3 ? 4u : 3u; }
+
 constexpr uint32_t kMaxDynSmem = 227 * 1024;
+
+// K-chain staging groups take about 1/6 of the ring each: a handful in flight.
+uint32_t chain_group_target(const CtaPlan& p) { return std::max<uint32_t>(256, p.ring_bytes / 6); }
 
 // ASNN_CTA_DEBUG (timing experiments only): 2 = no layer staging (read row
 // pointers and edges from global memory).
@@ -416,6 +424,12 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     // layers of <= 512 items; off with ASNN_CTA_PIPE=0.
     const char* pe = getenv("ASNN_CTA_PIPE");
     const bool want_pipe = !(pe && pe[0] == '0');
+    // K-chain (chain.cuh) for one-column-per-item slices of <= 4 warps of
+    // items per layer; off with ASNN_CTA_CHAIN=0 (the pipelined K-cta runs).
+    static const bool want_chain = [] {
+        const char* s = getenv("ASNN_CTA_CHAIN");
+        return !(s && s[0] == '0');
+    }();
     for (uint32_t C = cmax; C >= 1; C >>= 1) {
         if (ldA % C) continue;
         // activations (+ the zero row) | ring | mbarriers + metas | pipelined
@@ -423,7 +437,9 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         const uint64_t as_bytes = (static_cast<uint64_t>(L->max_pos + 1) * C + 3) / 4 * 16;
         const uint64_t vq = C >= 4 ? 4 : 1;
         const uint64_t items_c = static_cast<uint64_t>(L->max_width) * (C / vq);
-        const uint64_t pipe_c = want_pipe && items_c <= 512 ? 2 * items_c * (vq + 1) * 4 : 0;
+        const uint64_t nf = want_chain && want_pipe && vq == 1 && items_c <= 128 ? (items_c + 31) / 32 : 0;
+        const uint64_t pipe_c = nf ? chain::tail_bytes(static_cast<uint32_t>(nf)) - cta::kMetaBytes
+                                   : want_pipe && items_c <= 512 ? 2 * items_c * (vq + 1) * 4 : 0;
         const uint64_t fixed = as_bytes + cta::kMetaBytes + pipe_c;
         if (fixed + 1024 > kMaxDynSmem) {
             if (C == 1) break;
@@ -446,7 +462,8 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         p.C = C;
         p.ring_bytes = static_cast<uint32_t>(std::max<uint64_t>(ring, 16));
         p.smem = static_cast<uint32_t>(fixed + p.ring_bytes);
-        p.pipe = pipe_c > 0;
+        p.pipe = pipe_c > 0 && !nf;
+        p.chain_nf = static_cast<uint32_t>(nf);
         break;
     }
     // Global (L2-resident) variant for one network whose shared-memory slices
@@ -518,6 +535,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         if (force_win ||
             (ring >= 2 * max_layer && W >= 4 * static_cast<uint64_t>(L->max_width) && W < L->max_pos)) {
             p.C = C;
+            p.chain_nf = 0;
             p.win = true;
             p.win_mask = static_cast<uint32_t>(W - 1);
             p.stg_edges = pipe_c && stg_c ? L->max_level_edges : 0;
@@ -531,6 +549,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         uint32_t C = 1;
         while (ldA / C > sms && C < 128) C <<= 1;
         p.C = C;
+        p.chain_nf = 0;
         p.global = true;
         p.ring_bytes = static_cast<uint32_t>(
             std::min<uint64_t>(32 * max_layer, kMaxDynSmem - cta::kMetaBytes) / 16 * 16);
@@ -549,6 +568,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     }();
     p.T = static_cast<uint32_t>(std::min<uint64_t>(tmax, std::max<uint64_t>(32, (items + 31) / 32 * 32)));
     if (p.global) p.pipe = false;
+    if (p.chain_nf) p.T = 32 * p.chain_nf * (1 + chain_np(p.chain_nf));
     if (p.pipe) {  // finish group + prefix group of up to 8 warps each (one row per
                    // thread up to 256 items: config 1's ~200-row layers, ASNN_CTA_PIPE_MAX)
         static const uint64_t gmax = [] {
@@ -846,6 +866,8 @@ int assemble_layout(asnn_dev* dev, std::vector<NetMeta>&& nets, FlatDevice&& fla
                     "layout references an id >= id_bound (code " + std::to_string(h_bad[0]) + ")");
     }
     L->zero_refs = (h_bad[0] & 8u) != 0;
+    L->le_host = std::move(le_host);
+    L->lo_base_host = std::move(lo_base_host);
     L->d_meta = std::move(d_meta);
     L->row_ptr = std::move(flat.row_ptr);
     L->node_ids = std::move(flat.node_ids);
@@ -1045,7 +1067,22 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
     const CtaPlan cp = cta_plan(L, ldA);
     // K-cta writes the declared outputs itself (shared-memory variant, no state)
     const bool cta_out = cp.use && !cp.global && !cp.win && !state && out && L->total_out;
-    if (cp.use) {
+    if (cp.use && cp.chain_nf) {
+        using KC = void (*)(const CtaNet*, const uint32_t*, const uint4*, const uint32_t*, const uint32_t*,
+                            const uint32_t*, const uint2*, const uint4*, const uint4*, const float*, uint32_t, float*,
+                            uint32_t, uint32_t, uint32_t, uint32_t, int, float*, const uint32_t*);
+        static const KC kc[2][4] = {
+            {k_chain<1, chain_np(1), false>, k_chain<2, chain_np(2), false>, k_chain<3, chain_np(3), false>,
+             k_chain<4, chain_np(4), false>},
+            {k_chain<1, chain_np(1), true>, k_chain<2, chain_np(2), true>, k_chain<3, chain_np(3), true>,
+             k_chain<4, chain_np(4), true>}};
+        const KC fn = kc[L->zero_refs ? 1 : 0][cp.chain_nf - 1];
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cp.smem)));
+        fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T + 32, cp.smem, st>>>(
+            reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->grp.p, L->grp_off.p, L->lg_cat.p,
+            L->row_ptr.p, L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos,
+            cp.ring_bytes, (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr, L->split.p);
+    } else if (cp.use) {
         // the whole sweep (sensors + every layer) of each (network, slice) in one CTA
         auto fn = cp.win ? (cp.pipe ? (L->zero_refs ? k_cta<1, true, false, true, true> : k_cta<1, false, false, true, true>)
                                     : (L->zero_refs ? k_cta<1, true, false, false, true> : k_cta<1, false, false, false, true>))
@@ -1183,6 +1220,50 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
     return ASNN_OK;
 }
 
+// K-chain staging groups: consecutive layers packed greedily while their row
+// pointers, splits and edges stay within `target` bytes in the ring (a layer
+// larger than that is a group alone).  Built on the host from the layer
+// bounds once per target (the plan's ring / 6).
+int ensure_groups(asnn_dev_layout* L, uint32_t target) {
+    if (L->grp.p && L->grp_target == target) return ASNN_OK;
+    asnn_dev* dev = L->dev;
+    const uint32_t G = static_cast<uint32_t>(L->nets.size());
+    std::vector<uint4> g;
+    std::vector<uint32_t> off(G + 1, 0), lg(L->le_host.size() + 1, 0);
+    for (uint32_t gi = 0; gi < G; ++gi) {
+        const NetMeta& n = L->nets[gi];
+        const uint32_t* lo = n.layer_offsets.data();
+        const uint32_t* le = L->le_host.data() + L->lo_base_host[gi];
+        uint32_t* lgn = lg.data() + L->lo_base_host[gi];
+        off[gi] = static_cast<uint32_t>(g.size());
+        uint32_t l = 1;
+        while (l < n.n_layers) {
+            const uint32_t l0 = l, k = static_cast<uint32_t>(g.size()) - off[gi];
+            g.push_back(make_uint4(l0, lo[l0], le[l0], 0u));
+            lgn[l++] = k;
+            while (l < n.n_layers) {
+                uint32_t rb, sb, eb;
+                chain::group_bytes(n.pos_base + lo[l0], n.pos_base + lo[l + 1], le[l0], le[l + 1], rb, sb, eb);
+                if (static_cast<uint64_t>(rb) + sb + eb > target) break;
+                lgn[l++] = k;
+            }
+        }
+        g.push_back(make_uint4(n.n_layers, lo[n.n_layers], le[n.n_layers], 0u));  // sentinel
+    }
+    off[G] = static_cast<uint32_t>(g.size());
+    L->graph.reset();
+    cudaStream_t st = dev->stream;
+    CK(L->grp.alloc(g.size()));
+    CK(L->grp_off.alloc(G + 1));
+    CK(L->lg_cat.alloc(lg.size()));
+    CK(cudaMemcpyAsync(L->grp.p, g.data(), g.size() * sizeof(uint4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(L->grp_off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(L->lg_cat.p, lg.data(), lg.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // the host vectors go out of scope
+    L->grp_target = target;
+    return ASNN_OK;
+}
+
 int ensure_workspace(asnn_dev_layout* L, uint32_t n_vec) {
     asnn_dev* dev = L->dev;
     const uint32_t ldA = padded_batch(n_vec);
@@ -1190,13 +1271,22 @@ int ensure_workspace(asnn_dev_layout* L, uint32_t n_vec) {
         const int rc = ensure_schedule(L);
         if (rc) return rc;
     }
-    if (cta_plan(L, ldA).pipe && !L->split.p) {
+    // split[] at the prefix depth the plan needs (pipelined K-cta 1, K-chain NP - 1)
+    const CtaPlan cpl = cta_plan(L, ldA);
+    const uint32_t want_d = cpl.chain_nf ? chain_np(cpl.chain_nf) - 1 : cpl.pipe ? 1u : 0u;
+    if (want_d && (!L->split.p || L->split_d != want_d)) {
         L->graph.reset();
-        CK(L->split.alloc(L->total_pos + 8));  // slack: K-cta bulk copies round up to 16 bytes
+        if (!L->split.p) CK(L->split.alloc(L->total_pos + 8));  // slack: K-cta bulk copies round up to 16 bytes
         const uint32_t G = static_cast<uint32_t>(L->nets.size());
         k_splits<<<dim3((L->max_pos + 255) / 256, G), 256, 0, dev->stream>>>(
-            reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->row_ptr.p, L->edges.p, L->split.p);
+            reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->row_ptr.p, L->edges.p, L->split.p,
+            want_d);
         CK(cudaGetLastError());
+        L->split_d = want_d;
+    }
+    if (cpl.use && cpl.chain_nf) {
+        const int rc = ensure_groups(L, chain_group_target(cpl));
+        if (rc) return rc;
     }
     if (seg_eligible(L, ldA)) {
         if (L->seg_key != seg_key_for(L)) {

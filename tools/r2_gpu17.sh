@@ -1,0 +1,9 @@
+# K-chain with mbarrier signalling: parity + C3 timing + profile counters
+O=gpurun_out/r2_t17.txt
+timeout 900 python -m pytest tests/test_gpu_activate.py tests/test_gpu_segments.py tests/test_gpu_integration.py tests/test_gpu_writecount.py tests/test_gpu_fullsize.py tests/test_gpu_concurrency.py -x -q > gpurun_out/r2_t17_pytest.txt 2>&1; echo "pytest rc=$?" > $O
+for c in c3 c1; do
+  echo "cfg $c" >> $O
+  timeout 300 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline 2>>$O | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], d.get('e2e',{}).get('value'), d['value'])" >> $O 2>&1
+done
+echo "prof c3" >> $O
+ASNN_B200_LIB=$PWD/build/exp/libasnn_b200_prof.so timeout 300 python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline 2>&1 | grep 'chain prof' | tail -12 >> $O

@@ -1,0 +1,5 @@
+O=gpurun_out/r2_t18.txt
+echo "prof c3" > $O
+ASNN_B200_LIB=$PWD/build/exp/libasnn_b200_prof.so timeout 300 python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline 2>&1 | grep "chain prof\|producer" | tail -8 >> $O
+
+

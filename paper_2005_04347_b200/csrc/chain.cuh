@@ -8,15 +8,20 @@
 // prefix's sources all sit on layers <= l - D - 1, the tail starts at the
 // first source on layer l - D or later (on config 3 the tail is one edge for
 // 98% of rows, at most three).  Warp roles:
-//  * F (NF warps, one item = (row, column) per lane): per layer, one record
-//    load, the tail's source loads, two multiply-adds, sigmoid32, one store
-//    and a warp (NF = 1) or F-only named barrier -- nothing else on the chain.
-//    F arrives on layer l's done mbarrier (release) once layer l is final;
+//  * F (two groups of NF warps, one item = (row, column) per lane; group f
+//    finishes layers l = 1 + f (mod 2)): per layer, a named barrier with the
+//    other group (layer l-1 final), the tail's source loads, two
+//    multiply-adds, sigmoid32, one store and a barrier arrival for the other
+//    group -- the record prefetch, the mbarrier arrivals and the loop overhead
+//    of one group run in the shadow of the other group's chain (ncu, one
+//    group: ~680 cycles per layer of which ~300 are the data chain).  Each F
+//    warp arrives on layer l's done mbarrier (release) once its items are final;
 //  * P (NP groups of NF warps; group j owns layers m = 1 + j (mod NP)): waits
 //    (suspended) until layer m - D - 1 is final, sums the prefix of layer m's
 //    rows (8 source loads in flight per lane), and leaves per item a 32-byte
-//    record {partial sum, destination, first two tail edges as (shared-memory
-//    offset, weight), tail length + flags, index of the third} in a ring of
+//    record {partial sum, destination + staging slot + group-end flag, first
+//    two tail edges as (shared-memory offset, weight), tail length + flag,
+//    index of the third} in a ring of
 //    kRecBufs layer buffers, then arrives on the buffer's mbarrier.  D = NP - 1
 //    gives each prefix D - 1 whole F steps plus the current one of slack;
 //  * the producer warp stages GROUPS of consecutive layers (row pointers,
@@ -39,8 +44,11 @@ namespace chain {
 constexpr uint32_t kRecBufs = 4;           // >= D + 1 (D <= 3): F holds layers l, l+1
 constexpr uint32_t kNoTail = 0xFFFFFFFFu;  // record of an item past the layer's width
 constexpr uint32_t kUnstaged = 1u << 30;   // rb.z flag: the tail's edges are in global memory
-constexpr uint32_t kGroupEnd = 1u << 29;   // rb.z flag: the layer is its group's last
-constexpr uint32_t kTailMask = kGroupEnd - 1;
+constexpr uint32_t kTailMask = kUnstaged - 1;
+// ra.y = destination (shared-memory float index, < 2^20) | staging slot << 20
+// | the layer is its staging group's last << 25
+constexpr uint32_t kDstMask = (1u << 20) - 1;
+constexpr uint32_t kGroupEnd = 1u << 25;
 constexpr uint32_t kDoneBars = 8;          // >= D + 2: layer k's barrier is reused for k + kDoneBars
 
 // Waits for a phase of an mbarrier, suspending in the hardware between tests
@@ -54,8 +62,13 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
         "r"(parity), "r"(1000000u)
         : "memory");
 }
-__device__ __forceinline__ void f_barrier(uint32_t n_threads) {
-    asm volatile("bar.sync 2, %0;" ::"r"(n_threads) : "memory");
+// Named barriers 2 + f between the finish groups: group 1-f arrives when its
+// layer is final, group f syncs before the next.
+__device__ __forceinline__ void f_sync(uint32_t id, uint32_t n_threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n_threads) : "memory");
+}
+__device__ __forceinline__ void f_arrive(uint32_t id, uint32_t n_threads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n_threads) : "memory");
 }
 
 // Shared-memory bytes past the staging ring: mbarriers + group metas, then
@@ -163,7 +176,7 @@ __device__ __forceinline__ void produce_groups(const CtaNet& n, const uint4* __r
 }  // namespace chain
 
 template <int NF, int NP, bool GUARD>
-__global__ void __launch_bounds__(32 * (NF * (1 + NP) + 1))
+__global__ void __launch_bounds__(32 * (NF * (2 + NP) + 1))
 k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, const uint4* __restrict__ grp,
         const uint32_t* __restrict__ grp_off, const uint32_t* __restrict__ lg_cat,
         const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,
@@ -189,7 +202,7 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
     uint4* recA = reinterpret_cast<uint4*>(meta + 8 * kSlots);  // [kRecBufs][I]
     uint4* recB = recA + kRecBufs * I;                          // [kRecBufs][I]
     // rec_bar[b]: record buffer b filled (one arrival per P warp of the group);
-    // done_bar[(k - 1) % kDoneBars]: layer k final (F, after its barrier)
+    // done_bar[(k - 1) % kDoneBars]: layer k final (one arrival per F warp)
     uint64_t* rec_bar = reinterpret_cast<uint64_t*>(recB + kRecBufs * I);
     uint64_t* done_bar = rec_bar + kRecBufs;
     const uint4* ngrp = grp + grp_off[blockIdx.y];
@@ -197,17 +210,17 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
     const uint32_t* lo = lo_cat + n.lo_base;
     const uint32_t* lg = lg_cat + n.lo_base;
 
-    const uint32_t Tc = 32 * NF * (1 + NP);  // consumer threads
+    const uint32_t Tc = 32 * NF * (2 + NP);  // consumer threads
     const uint32_t tid = threadIdx.x;
     const uint32_t warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
         for (uint32_t s = 0; s < kSlots; ++s) {
             heavy::mbar_init(&full[s], 1);
-            heavy::mbar_init(&empty[s], 1);
+            heavy::mbar_init(&empty[s], NF);
         }
         for (uint32_t b = 0; b < kRecBufs; ++b) heavy::mbar_init(&rec_bar[b], NF);
-        for (uint32_t b = 0; b < chain::kDoneBars; ++b) heavy::mbar_init(&done_bar[b], 1);
+        for (uint32_t b = 0; b < chain::kDoneBars; ++b) heavy::mbar_init(&done_bar[b], NF);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -238,9 +251,9 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
         }
         consumer_barrier(Tc);
 
-        if (warp >= NF) {
+        if (warp >= 2 * NF) {
             // ---- P group j: prefixes of layers m = 1 + j, 1 + j + NP, ... ----
-            const uint32_t j = warp / NF - 1, w = warp % NF;
+            const uint32_t j = warp / NF - 2, w = warp % NF;
             const uint32_t it = w * 32 + lane;
             const uint32_t i = it / C, q = it - i * C;
             // layer m's bounds and group, loaded one layer of this group ahead
@@ -266,7 +279,9 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
                     chain::mbar_wait_sleep(&done_bar[k % chain::kDoneBars], (k / chain::kDoneBars) & 1);
                 }
                 const uint32_t zo = zero_slot * C + q;
-                uint4 ra = make_uint4(0u, 0u, zo, 0u), rb = make_uint4(zo, 0u, kNoTail, 0u);
+                // every item carries the staging slot and group end (F's lane 0 releases)
+                const uint32_t tag = (g % kSlots) << 20 | (m + 1 == l1 ? chain::kGroupEnd : 0u);
+                uint4 ra = make_uint4(0u, tag, zo, 0u), rb = make_uint4(zo, 0u, kNoTail, 0u);
                 if (i < b - a) {
                     const uint32_t r = n.pos_base + a + i;
                     uint32_t k, ks, ke;
@@ -295,7 +310,7 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
                         acc = mac(acc, __uint_as_float(ed.y), As[off(ed.x, q)]);
                     }
                     ra.x = __float_as_uint(acc);
-                    ra.y = (a + i) * C + q;
+                    ra.y |= (a + i) * C + q;
                     if (ke > ks) {
                         const uint2 e0 = Ep[ks];
                         ra.z = off(e0.x, q);
@@ -308,7 +323,7 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
                     }
                     // F reads edges beyond the second from ring_u2 (staged,
                     // index relative to the ring) or edges (absolute)
-                    rb.z = (ke - ks) | (st ? 0u : chain::kUnstaged) | (m + 1 == l1 ? chain::kGroupEnd : 0u);
+                    rb.z = (ke - ks) | (st ? 0u : chain::kUnstaged);
                     rb.w = st ? edges_at + ks + 2 - e0a : ks + 2;
                 }
                 recA[((m - 1) % kRecBufs) * I + it] = ra;
@@ -317,9 +332,10 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
                 if (lane == 0) heavy::mbar_arrive(&rec_bar[(m - 1) % kRecBufs]);
             }
         } else {
-            // ---- F: finish every layer ----
-            const uint32_t w = warp, it = w * 32 + lane;
+            // ---- F group f: finish layers l = 1 + f, 3 + f, ... ----
+            const uint32_t f = warp / NF, it = (warp % NF) * 32 + lane;
             const uint32_t q = it % C;
+            constexpr uint32_t kPair = 2 * 32 * NF;  // both finish groups
             // record buffer (m - 1) % kRecBufs, its ((m - 1) / kRecBufs)-th fill
             auto wait_rec = [&](uint32_t m, uint4& ra, uint4& rb) {
                 heavy::mbar_wait(&rec_bar[(m - 1) % kRecBufs], ((m - 1) / kRecBufs) & 1);
@@ -327,17 +343,15 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
                 rb = recB[((m - 1) % kRecBufs) * I + it];
             };
             uint4 ra = make_uint4(0u, 0u, 0u, 0u), rb = make_uint4(0u, 0u, kNoTail, 0u);
-            if (n.n_layers > 1) wait_rec(1, ra, rb);
-            uint32_t gf = 0;  // (item 0) the group of layer l, released after its last layer
-            for (uint32_t l = 1; l < n.n_layers; ++l) {
-                // layer l-1's values are final (the barrier below); the tail's
-                // first two sources, then layer l+1's record while they load
+            uint32_t l = 1 + f;
+            if (l < n.n_layers) wait_rec(l, ra, rb);
+            for (; l < n.n_layers; l += 2) {
+                // layer l-1 final (the other group; layer 0: the sensor barrier)
+                if (l > 1) chain::f_sync(2 + f, kPair);
                 const float v0 = As[ra.z], v1 = As[rb.x];
-                uint4 na = ra, nb = make_uint4(0u, 0u, kNoTail, 0u);
-                if (l + 1 < n.n_layers) wait_rec(l + 1, na, nb);
                 const uint32_t flags = rb.z;
-                const uint32_t nt = flags & chain::kTailMask;
                 if (flags != kNoTail) {
+                    const uint32_t nt = flags & chain::kTailMask;
                     float acc = __uint_as_float(ra.x);
                     acc = mac(acc, __uint_as_float(ra.w), v0);
                     acc = mac(acc, __uint_as_float(rb.y), v1);
@@ -349,18 +363,16 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
                             acc = mac(acc, __uint_as_float(ed.y), As[off(ed.x, q)]);
                         }
                     }
-                    As[ra.y] = sigmoid32(acc);
-                    wc_note(n.pos_base + ra.y / C, c0 + q, 1);
+                    As[ra.y & chain::kDstMask] = sigmoid32(acc);
+                    wc_note(n.pos_base + (ra.y & chain::kDstMask) / C, c0 + q, 1);
                 }
-                ra = na;
-                rb = nb;
-                if constexpr (NF == 1) __syncwarp();
-                else chain::f_barrier(32 * NF);
-                // item 0 exists in every layer, so its record carries the group end
-                if (it == 0) {
+                __syncwarp();
+                if (l + 1 < n.n_layers) chain::f_arrive(2 + (1 - f), kPair);  // layer l final
+                if (lane == 0) {
                     heavy::mbar_arrive(&done_bar[(l - 1) % chain::kDoneBars]);
-                    if (flags & chain::kGroupEnd) heavy::mbar_arrive(&empty[gf++ % kSlots]);
+                    if (ra.y & chain::kGroupEnd) heavy::mbar_arrive(&empty[(ra.y >> 20) & (kSlots - 1)]);
                 }
+                if (l + 2 < n.n_layers) wait_rec(l + 2, ra, rb);
             }
         }
     }

@@ -384,9 +384,10 @@ struct CtaPlan {
     uint32_t chain_nf = 0;   // K-chain (chain.cuh): finish warps (0 = not used)
 };
 
-// K-chain's prefix groups for NF finish warps: four (prefix depth D = 3) while
-// NF x 5 warps + the producer fit the 544-thread bound, else three (D = 2).
-constexpr uint32_t chain_np(uint32_t nf) { return nf <= 3 ? 4u : 3u; }
+// K-chain's prefix groups for NF-warp finish groups: two finish groups + NP
+// prefix groups + the producer warp within the 544-thread bound, at most four
+// (prefix depth D = NP - 1 <= 3).
+constexpr uint32_t chain_np(uint32_t nf) { return nf <= 2 ? 4u : nf == 3 ? 3u : 2u; }
 
 constexpr uint32_t kMaxDynSmem = 227 * 1024;
 
@@ -568,7 +569,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     }();
     p.T = static_cast<uint32_t>(std::min<uint64_t>(tmax, std::max<uint64_t>(32, (items + 31) / 32 * 32)));
     if (p.global) p.pipe = false;
-    if (p.chain_nf) p.T = 32 * p.chain_nf * (1 + chain_np(p.chain_nf));
+    if (p.chain_nf) p.T = 32 * p.chain_nf * (2 + chain_np(p.chain_nf));
     if (p.pipe) {  // finish group + prefix group of up to 8 warps each (one row per
                    // thread up to 256 items: config 1's ~200-row layers, ASNN_CTA_PIPE_MAX)
         static const uint64_t gmax = [] {

@@ -19,9 +19,9 @@
 //  * P (NP groups of NF warps; group j owns layers m = 1 + j (mod NP)): waits
 //    (suspended) until layer m - D - 1 is final, sums the prefix of layer m's
 //    rows (8 source loads in flight per lane), and leaves per item a 32-byte
-//    record {partial sum, destination + staging slot + group-end flag, first
-//    two tail edges as (shared-memory offset, weight), tail length + flag,
-//    index of the third} in a ring of
+//    record {partial sum, destination, first two tail edges as (shared-memory
+//    address, weight), tail length + staging slot + flags, index of the
+//    third} in a ring of
 //    kRecBufs layer buffers, then arrives on the buffer's mbarrier.  D = NP - 1
 //    gives each prefix D - 1 whole F steps plus the current one of slack;
 //  * the producer warp stages GROUPS of consecutive layers (row pointers,
@@ -41,15 +41,20 @@
 #pragma once
 
 namespace chain {
-constexpr uint32_t kRecBufs = 4;           // >= D + 1 (D <= 3): F holds layers l, l+1
-constexpr uint32_t kNoTail = 0xFFFFFFFFu;  // record of an item past the layer's width
-constexpr uint32_t kUnstaged = 1u << 30;   // rb.z flag: the tail's edges are in global memory
-constexpr uint32_t kTailMask = kUnstaged - 1;
-// ra.y = destination (shared-memory float index, < 2^20) | staging slot << 20
-// | the layer is its staging group's last << 25
-constexpr uint32_t kDstMask = (1u << 20) - 1;
-constexpr uint32_t kGroupEnd = 1u << 25;
-constexpr uint32_t kDoneBars = 8;          // >= D + 2: layer k's barrier is reused for k + kDoneBars
+// record ring of a prefix depth D: a power of two >= D + 1 (P writes layer m's
+// buffer only after layer m - D - 1 is final; F holds at most layers m-D..m-1)
+__host__ __device__ constexpr uint32_t rec_bufs(uint32_t d) { return d < 4 ? 4u : d < 8 ? 8u : 16u; }
+// Record tail word rb.z: tail length (< 2^16: a row's in-degree is below the
+// network's positions) | staging slot << 16 | group end | unstaged tail.
+constexpr uint32_t kTailMask = 0xFFFFu;
+constexpr uint32_t kGroupEnd = 1u << 21;  // the layer is its staging group's last
+constexpr uint32_t kUnstaged = 1u << 22;  // the tail's edges beyond the second are in global memory
+// Staging plan records (ensure_groups): per group {r0a, e0a, ebytes, wait+1},
+// {at | kPlanStaged, rbytes, sbytes, 0}; per layer {a, b, group | kPlanGroupEnd,
+// edges_at}, {r0a, e0a, rows_at | kPlanStaged, split_at}.
+constexpr uint32_t kPlanStaged = 1u << 31;
+constexpr uint32_t kPlanGroupEnd = 1u << 31;
+constexpr uint32_t kDoneBars = 16;         // >= D + 2: layer k's barrier is reused for k + kDoneBars
 
 // Waits for a phase of an mbarrier, suspending in the hardware between tests
 // (woken when the phase completes).
@@ -64,18 +69,36 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
 }
 // Named barriers 2 + f between the finish groups: group 1-f arrives when its
 // layer is final, group f syncs before the next.
+// (non-.aligned forms: no warp-convergence fence is emitted around them)
 __device__ __forceinline__ void f_sync(uint32_t id, uint32_t n_threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n_threads) : "memory");
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n_threads) : "memory");
 }
 __device__ __forceinline__ void f_arrive(uint32_t id, uint32_t n_threads) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n_threads) : "memory");
+    asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(n_threads) : "memory");
 }
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+// sigmoid32's 2^(i/32) table from a shared-memory copy (16-byte entries)
+struct ExpTabShared {
+    uint32_t base;
+    __device__ __forceinline__ ulonglong2 operator()(uint32_t i) const {
+        ulonglong2 v;
+        asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(base + i * 16));
+        return v;
+    }
+};
 
 // Shared-memory bytes past the staging ring: mbarriers + group metas, then
 // the record ring (2 x uint4 per item per buffer) and its mbarriers, then the
 // layer-done mbarriers.
-__host__ __device__ constexpr uint32_t tail_bytes(uint32_t nf) {
-    return cta::kMetaBytes + kRecBufs * nf * 32 * 32 + kRecBufs * 8 + kDoneBars * 8;
+__host__ __device__ constexpr uint32_t tail_bytes(uint32_t nf, uint32_t np) {
+    return cta::kMetaBytes + rec_bufs(np - 1) * (nf * 32 * 32 + 8) + kDoneBars * 8;
 }
 
 // Bytes one group of layers takes in the ring: 16-byte aligned bulk copies
@@ -89,104 +112,50 @@ __host__ __device__ inline void group_bytes(uint32_t r0, uint32_t r1, uint32_t e
     ebytes = ((e1 - e0a) * 8 + 15) & ~15u;
 }
 
-// The producer warp: stages groups 0..K-1 of network n in order.  meta[slot]
-// = {l1, r0a, e0a, staged, rows_at, split_at, extent, edges_at} (ring indices
-// in u32 / u32 / uint2 units).  A group whose bytes would need the release of
-// the group just before it is read from global memory instead: F finishes
-// that group's last layer only with the next group's first prefix, which
-// needs that group staged.
-__device__ __forceinline__ void produce_groups(const CtaNet& n, const uint4* __restrict__ grp, uint32_t K,
-                                               const uint32_t* __restrict__ row_ptr,
-                                               const uint32_t* __restrict__ split, const uint2* __restrict__ edges,
-                                               unsigned char* ring, uint32_t ring_bytes, uint64_t* full,
-                                               uint64_t* empty, uint32_t* meta, int write_all, uint32_t lane) {
+// The producer (lane 0 of the last warp) executes the host-built plan of
+// network n's K groups: wait for the release of the group the plan names
+// (the bytes it overwrites, or its mbarrier slot's previous group), then
+// three bulk copies (or a plain arrival: the group is read from global
+// memory).  ~40 instructions per group instead of the ~200 of the dynamic
+// ring bookkeeping.
+__device__ __forceinline__ void produce_plan(const uint4* __restrict__ plan, uint32_t K,
+                                             const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ split,
+                                             const uint2* __restrict__ edges, unsigned char* ring, uint64_t* full,
+                                             uint64_t* empty) {
     using namespace cta;
-    uint32_t w = 0, used = 0, oldest = 0;  // oldest: first group whose release is not yet seen
-    auto release_to = [&](uint32_t upto) {
-        for (; oldest < upto; ++oldest) used -= meta[8 * (oldest % kSlots) + 6];
-    };
-    // window of group records: lane j holds grp[base + j] (records 0..K, K = sentinel)
-    uint32_t base = 0;
-    uint4 rc = grp[min(base + lane, K)], rn = grp[min(base + 31 + lane, K)];
-    const bool leader = lane == 0;
+    uint4 p0 = K ? plan[0] : make_uint4(0u, 0u, 0u, 0u), p1 = K ? plan[1] : p0;
     for (uint32_t k = 0; k < K; ++k) {
-        if (k - base == 31) {
-            base += 31;
-            rc = rn;
-            rn = grp[min(base + 31 + lane, K)];
+        const uint4 c0 = p0, c1 = p1;
+        if (k + 1 < K) p0 = plan[2 * k + 2], p1 = plan[2 * k + 3];  // next group's plan in flight
+        if (c0.w) {
+            const uint32_t x = c0.w - 1;
+            producer_wait(&empty[x % kSlots], (x / kSlots) & 1);
         }
-        const uint32_t i0 = k - base;
-        const uint32_t l1 = __shfl_sync(0xFFFFFFFFu, rc.x, i0 + 1);
-        const uint32_t r0 = n.pos_base + __shfl_sync(0xFFFFFFFFu, rc.y, i0);
-        const uint32_t r1 = n.pos_base + __shfl_sync(0xFFFFFFFFu, rc.y, i0 + 1);
-        const uint32_t e0 = __shfl_sync(0xFFFFFFFFu, rc.z, i0), e1 = __shfl_sync(0xFFFFFFFFu, rc.z, i0 + 1);
-        const uint32_t m = k % kSlots, u = k / kSlots;
-        uint32_t rbytes, sbytes, ebytes;
-        group_bytes(r0, r1, e0, e1, rbytes, sbytes, ebytes);
-        const uint32_t r0a = r0 & ~3u, e0a = e0 & ~1u;
-        const uint32_t size = rbytes + sbytes + ebytes;
-        if (u > 0) {  // slot m's previous group (k - kSlots) and all before it are released
-            producer_wait(&empty[m], (u - 1) & 1);
-            release_to(k - kSlots + 1);
+        uint64_t* fb = &full[k % kSlots];
+        if (c1.x & kPlanStaged) {
+            const uint32_t at = c1.x & ~kPlanStaged, rbytes = c1.y, sbytes = c1.z, ebytes = c0.z;
+            expect_tx(fb, rbytes + sbytes + ebytes);
+            bulk_g2s(ring + at, row_ptr + c0.x, rbytes, fb);
+            bulk_g2s(ring + at + rbytes, split + c0.x, sbytes, fb);
+            if (ebytes) bulk_g2s(ring + at + rbytes + sbytes, edges + c0.y, ebytes, fb);
+        } else {
+            heavy::mbar_arrive(fb);
         }
-        bool staged = size <= ring_bytes && !(write_all & 2);
-        uint32_t at = 0, extent = 0;
-        if (staged) {
-            for (;;) {
-                if (used == 0) w = 0;
-                const bool wrap = w + size > ring_bytes;
-                const uint32_t need = wrap ? ring_bytes - w + size : size;
-                if (need <= ring_bytes - used) {
-                    at = wrap ? 0u : w;
-                    extent = need;
-                    w = at + size;
-                    used += need;
-                    break;
-                }
-                if (oldest + 1 >= k) {  // only the previous group holds the space
-                    staged = false;
-                    break;
-                }
-                producer_wait(&empty[oldest % kSlots], (oldest / kSlots) & 1);
-                release_to(oldest + 1);
-            }
-        }
-        if (leader) {
-            uint32_t* mm = meta + 8 * m;
-            mm[0] = l1;
-            mm[1] = r0a;
-            mm[2] = e0a;
-            mm[3] = staged ? 1u : 0u;
-            mm[4] = at / 4;
-            mm[5] = (at + rbytes) / 4;
-            mm[6] = extent;
-            mm[7] = (at + rbytes + sbytes) / 8;
-            if (staged) {
-                expect_tx(&full[m], size);
-                bulk_g2s(ring + at, row_ptr + r0a, rbytes, &full[m]);
-                bulk_g2s(ring + at + rbytes, split + r0a, sbytes, &full[m]);
-                if (ebytes) bulk_g2s(ring + at + rbytes + sbytes, edges + e0a, ebytes, &full[m]);
-            } else {
-                heavy::mbar_arrive(&full[m]);
-            }
-        }
-        __syncwarp();  // the extent in meta is read by every lane's release_to
     }
 }
 }  // namespace chain
 
 template <int NF, int NP, bool GUARD>
 __global__ void __launch_bounds__(32 * (NF * (2 + NP) + 1))
-k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, const uint4* __restrict__ grp,
-        const uint32_t* __restrict__ grp_off, const uint32_t* __restrict__ lg_cat,
+k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ unused, const uint4* __restrict__ grp,
+        const uint32_t* __restrict__ grp_off, const uint4* __restrict__ lplan,
         const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,
         const uint4* __restrict__ oinfo, const float* __restrict__ x, uint32_t n_vec, float* __restrict__ A,
         uint32_t ldA, uint32_t C, uint32_t max_pos, uint32_t ring_bytes, int write_all, float* __restrict__ out,
         const uint32_t* __restrict__ split) {
     using namespace cta;
-    using chain::kRecBufs;
-    using chain::kNoTail;
     constexpr uint32_t D = NP - 1;
+    constexpr uint32_t kRecBufs = chain::rec_bufs(D);
     constexpr uint32_t I = NF * 32;  // items of one layer
     static_assert(NP >= 2 && D + 1 <= kRecBufs, "record ring too small for the prefix depth");
     extern __shared__ __align__(128) unsigned char cta_smem[];
@@ -198,17 +167,17 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
     unsigned char* ring = reinterpret_cast<unsigned char*>(As + as_floats);
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + ring_bytes);
     uint64_t* empty = full + kSlots;
-    uint32_t* meta = reinterpret_cast<uint32_t*>(empty + kSlots);
+    uint32_t* meta = reinterpret_cast<uint32_t*>(empty + kSlots);  // unused (plan in global memory)
     uint4* recA = reinterpret_cast<uint4*>(meta + 8 * kSlots);  // [kRecBufs][I]
     uint4* recB = recA + kRecBufs * I;                          // [kRecBufs][I]
     // rec_bar[b]: record buffer b filled (one arrival per P warp of the group);
     // done_bar[(k - 1) % kDoneBars]: layer k final (one arrival per F warp)
     uint64_t* rec_bar = reinterpret_cast<uint64_t*>(recB + kRecBufs * I);
     uint64_t* done_bar = rec_bar + kRecBufs;
-    const uint4* ngrp = grp + grp_off[blockIdx.y];
-    const uint32_t n_groups = grp_off[blockIdx.y + 1] - grp_off[blockIdx.y] - 1;  // + the sentinel
-    const uint32_t* lo = lo_cat + n.lo_base;
-    const uint32_t* lg = lg_cat + n.lo_base;
+    (void)unused;
+    const uint4* gplan = grp + 2 * static_cast<size_t>(grp_off[blockIdx.y]);
+    const uint32_t n_groups = grp_off[blockIdx.y + 1] - grp_off[blockIdx.y];
+    const uint4* lp = lplan + 2 * static_cast<size_t>(n.lo_base);  // layer l: lp[2l], lp[2l + 1]
 
     const uint32_t Tc = 32 * NF * (2 + NP);  // consumer threads
     const uint32_t tid = threadIdx.x;
@@ -232,12 +201,19 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
         const uint32_t p = pos - n.pos_base;
         return (GUARD && p >= n.n_pos ? zero_slot : p) * C + q;
     };
+    // records carry 32-bit shared-memory addresses (F's loads and stores need
+    // no address arithmetic); the meta area (unused by the plan-driven
+    // producer) holds the sigmoid table copy and a scratch word for the
+    // stores of items past a layer's width
+    const uint32_t as_sh = heavy::smem_u32(As);
+    const uint32_t tab_sh = heavy::smem_u32(meta), scratch_sh = tab_sh + 512;
+    auto addr = [&](uint32_t pos, uint32_t q) -> uint32_t { return as_sh + 4 * off(pos, q); };
 
     if (tid >= Tc) {
-        chain::produce_groups(n, ngrp, n_groups, row_ptr, split, edges, ring, ring_bytes, full, empty, meta,
-                              write_all, lane);
+        if (tid == Tc) chain::produce_plan(gplan, n_groups, row_ptr, split, edges, ring, full, empty);
     } else {
         for (uint32_t c = tid; c < C; c += Tc) As[zero_slot * C + c] = 0.0f;
+        for (uint32_t i = tid; i < 64; i += Tc) reinterpret_cast<uint64_t*>(meta)[i] = kExp32Tab[i];
         // sensors (eval.cpp:17), as K-cta
         for (uint32_t i = tid; i < n.n_sensors * C; i += Tc) {
             const uint32_t c = i / n.n_sensors, s = i - c * n.n_sensors;
@@ -256,19 +232,20 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
             const uint32_t j = warp / NF - 2, w = warp % NF;
             const uint32_t it = w * 32 + lane;
             const uint32_t i = it / C, q = it - i * C;
-            // layer m's bounds and group, loaded one layer of this group ahead
+            // layer m's plan, loaded one layer of this group ahead
             uint32_t m = 1 + j;
-            uint32_t a_n = 0, b_n = 0, g_n = 0;
-            if (m < n.n_layers) a_n = lo[m], b_n = lo[m + 1], g_n = lg[m];
+            uint4 pa_n = make_uint4(0u, 0u, 0u, 0u), pb_n = pa_n;
+            if (m < n.n_layers) pa_n = lp[2 * m], pb_n = lp[2 * m + 1];
             for (; m < n.n_layers; m += NP) {
-                const uint32_t a = a_n, b = b_n, g = g_n;
-                if (m + NP < n.n_layers) a_n = lo[m + NP], b_n = lo[m + NP + 1], g_n = lg[m + NP];
+                const uint4 pa = pa_n, pb = pb_n;
+                if (m + NP < n.n_layers) pa_n = lp[2 * (m + NP)], pb_n = lp[2 * (m + NP) + 1];
+                const uint32_t a = pa.x, b = pa.y, g = pa.z & ~chain::kPlanGroupEnd;
+                const bool gend = (pa.z & chain::kPlanGroupEnd) != 0;
+                const uint32_t edges_at = pa.w, r0a = pb.x, e0a = pb.y, split_at = pb.w;
+                const bool st = (pb.z & chain::kPlanStaged) != 0;
+                const uint32_t rows_at = pb.z & ~chain::kPlanStaged;
                 // group g's staging (F releases it only after finishing layer m)
                 chain::mbar_wait_sleep(&full[g % kSlots], (g / kSlots) & 1);
-                const uint32_t* mm = meta + 8 * (g % kSlots);
-                const uint32_t l1 = mm[0], r0a = mm[1], e0a = mm[2];
-                const bool st = mm[3] != 0;
-                const uint32_t rows_at = mm[4], split_at = mm[5], edges_at = mm[7];
                 // sources on layers <= m - D - 1 are final (layer 0: the
                 // sensor barrier); the record buffer (m - 1) % kRecBufs was
                 // last read by F at layer m - kRecBufs <= m - D - 1.  Layer k's
@@ -278,10 +255,11 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
                     const uint32_t k = m - D - 2;  // layer k + 1 (>= 1) done: phase k / kDoneBars
                     chain::mbar_wait_sleep(&done_bar[k % chain::kDoneBars], (k / chain::kDoneBars) & 1);
                 }
-                const uint32_t zo = zero_slot * C + q;
-                // every item carries the staging slot and group end (F's lane 0 releases)
-                const uint32_t tag = (g % kSlots) << 20 | (m + 1 == l1 ? chain::kGroupEnd : 0u);
-                uint4 ra = make_uint4(0u, tag, zo, 0u), rb = make_uint4(zo, 0u, kNoTail, 0u);
+                const uint32_t zo = as_sh + 4 * (zero_slot * C + q);
+                // every item carries the staging slot and group end (F's lane 0
+                // releases); an item past the width: sigmoid of +0 into scratch
+                const uint32_t tag = (g % kSlots) << 16 | (gend ? chain::kGroupEnd : 0u);
+                uint4 ra = make_uint4(0u, scratch_sh, zo, 0u), rb = make_uint4(zo, 0u, tag, 0u);
                 if (i < b - a) {
                     const uint32_t r = n.pos_base + a + i;
                     uint32_t k, ks, ke;
@@ -310,20 +288,20 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
                         acc = mac(acc, __uint_as_float(ed.y), As[off(ed.x, q)]);
                     }
                     ra.x = __float_as_uint(acc);
-                    ra.y |= (a + i) * C + q;
+                    ra.y = as_sh + 4 * ((a + i) * C + q);
                     if (ke > ks) {
                         const uint2 e0 = Ep[ks];
-                        ra.z = off(e0.x, q);
+                        ra.z = addr(e0.x, q);
                         ra.w = e0.y;
                     }
                     if (ke > ks + 1) {
                         const uint2 e1 = Ep[ks + 1];
-                        rb.x = off(e1.x, q);
+                        rb.x = addr(e1.x, q);
                         rb.y = e1.y;
                     }
                     // F reads edges beyond the second from ring_u2 (staged,
                     // index relative to the ring) or edges (absolute)
-                    rb.z = (ke - ks) | (st ? 0u : chain::kUnstaged);
+                    rb.z = tag | (ke - ks) | (st ? 0u : chain::kUnstaged);
                     rb.w = st ? edges_at + ks + 2 - e0a : ks + 2;
                 }
                 recA[((m - 1) % kRecBufs) * I + it] = ra;
@@ -342,35 +320,34 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
                 ra = recA[((m - 1) % kRecBufs) * I + it];
                 rb = recB[((m - 1) % kRecBufs) * I + it];
             };
-            uint4 ra = make_uint4(0u, 0u, 0u, 0u), rb = make_uint4(0u, 0u, kNoTail, 0u);
+            uint4 ra = make_uint4(0u, 0u, 0u, 0u), rb = ra;
             uint32_t l = 1 + f;
             if (l < n.n_layers) wait_rec(l, ra, rb);
             for (; l < n.n_layers; l += 2) {
                 // layer l-1 final (the other group; layer 0: the sensor barrier)
                 if (l > 1) chain::f_sync(2 + f, kPair);
-                const float v0 = As[ra.z], v1 = As[rb.x];
-                const uint32_t flags = rb.z;
-                if (flags != kNoTail) {
-                    const uint32_t nt = flags & chain::kTailMask;
-                    float acc = __uint_as_float(ra.x);
-                    acc = mac(acc, __uint_as_float(ra.w), v0);
-                    acc = mac(acc, __uint_as_float(rb.y), v1);
-                    if (nt > 2) {  // longer tails (and whole rows of layers <= D)
-                        const uint2* Eb = (flags & chain::kUnstaged) ? edges : ring_u2;
-                        const uint32_t ke = rb.w - 2 + nt;
-                        for (uint32_t k = rb.w; k < ke; ++k) {
-                            const uint2 ed = Eb[k];
-                            acc = mac(acc, __uint_as_float(ed.y), As[off(ed.x, q)]);
-                        }
+                const float v0 = chain::lds_f32(ra.z), v1 = chain::lds_f32(rb.x);
+                const uint32_t flags = rb.z, nt = flags & chain::kTailMask;
+                float acc = __uint_as_float(ra.x);
+                acc = mac(acc, __uint_as_float(ra.w), v0);
+                acc = mac(acc, __uint_as_float(rb.y), v1);
+                if (nt > 2) {  // longer tails (and whole rows of layers <= D)
+                    const uint2* Eb = (flags & chain::kUnstaged) ? edges : ring_u2;
+                    const uint32_t ke = rb.w - 2 + nt;
+                    for (uint32_t k = rb.w; k < ke; ++k) {
+                        const uint2 ed = Eb[k];
+                        acc = mac(acc, __uint_as_float(ed.y), chain::lds_f32(addr(ed.x, q)));
                     }
-                    As[ra.y & chain::kDstMask] = sigmoid32(acc);
-                    wc_note(n.pos_base + (ra.y & chain::kDstMask) / C, c0 + q, 1);
                 }
-                __syncwarp();
+                chain::sts_f32(ra.y, sigmoid32(acc, chain::ExpTabShared{tab_sh}));
                 if (l + 1 < n.n_layers) chain::f_arrive(2 + (1 - f), kPair);  // layer l final
+#ifdef ASNN_WRITE_COUNT
+                if (ra.y != scratch_sh) wc_note(n.pos_base + (ra.y - as_sh) / 4 / C, c0 + q, 1);
+#endif
+                __syncwarp();
                 if (lane == 0) {
                     heavy::mbar_arrive(&done_bar[(l - 1) % chain::kDoneBars]);
-                    if (ra.y & chain::kGroupEnd) heavy::mbar_arrive(&empty[(ra.y >> 20) & (kSlots - 1)]);
+                    if (flags & chain::kGroupEnd) heavy::mbar_arrive(&empty[(flags >> 16) & (kSlots - 1)]);
                 }
                 if (l + 2 < n.n_layers) wait_rec(l + 2, ra, rb);
             }

@@ -52,8 +52,10 @@ __device__ __forceinline__ float sigmoid32_exact(float x) {
 // sigmoid32 with a short double-precision fast path and an exact rounding
 // test (Ziv): the fast path evaluates 1/(1+exp(-4.97 x)) to a relative error
 // below 2^-47 (exp(t) = 2^(k/32) exp(r), |r| <= ln2/64, degree-5 Taylor
-// polynomial; reciprocal by MUFU.RCP64H + two Newton steps) -- about half the
-// FP64 operations of the correctly rounded exp + division.  Whenever that value lies within 2^12
+// polynomial; reciprocal by MUFU.RCP64H refined by one third-order step
+// y (1 + e + e^2), e = 1 - d y, which triples the bits where two Newton steps
+// chain four dependent DFMAs) -- about half the FP64 operations of the
+// correctly rounded exp + division.  Whenever that value lies within 2^12
 // double ulps (2^-40 relative) of a float rounding boundary, or the result
 // leaves the normal float range, the exact restatement above decides.  Both
 // results then round to the same float: the reference's double is within
@@ -64,22 +66,33 @@ __device__ __forceinline__ float sigmoid32_exact(float x) {
 // The fast path is straight-line code (selects, no branches) so that the V
 // evaluations of a column group interleave their FP64 dependency chains;
 // sigmoid32_v takes the exact restatement in one rarely-taken branch after
-// all of them.
-__device__ __forceinline__ float sigmoid32_fast(float x, bool& exact) {
-    const double t0 = __dmul_rn(-4.97, static_cast<double>(x));
+// all of them.  Saturated (t < -40) and out-of-range (t >= 86, NaN) inputs
+// run the same straight line on their unclamped t -- whatever it computes is
+// replaced by the clamp constant or sent to the exact path, so no clamp sits
+// on the latency chain of the latency-bound sweeps (K-chain).
+//
+// TabLoad: how the {tail, scale} pair of 2^(i/32) is read -- global memory
+// through L1 (default) or a shared-memory copy (K-chain's finish warps).
+struct ExpTabGlobal {
+    __device__ __forceinline__ ulonglong2 operator()(uint32_t i) const {
+        return __ldg(reinterpret_cast<const ulonglong2*>(kExp32Tab) + i);
+    }
+};
+template <class TabLoad = ExpTabGlobal>
+__device__ __forceinline__ float sigmoid32_fast(float x, bool& exact, TabLoad tab = TabLoad()) {
+    const double t = __dmul_rn(-4.97, static_cast<double>(x));
     // exp(t) <= 2^-54: 1 + exp(t) == 1 in both, v clamps below 1 and the
     // float rounds to 1 and clamps to 1 - FLT_EPSILON/2
-    const bool sat = t0 < -40.0;
-    const bool out = !(t0 < 86.0);  // float subnormal / clamped results, NaN
-    const double t = (sat || out) ? 0.0 : t0;
+    const bool sat = t < -40.0;
+    const bool out = !(t < 86.0);  // float subnormal / clamped results, NaN
     // k = round(t 32/ln2) in the low bits of zs; r = t - k ln2/32 with the hi
-    // part of ln2/32 exact against k (|k| < 2^12)
+    // part of ln2/32 exact against k (|k| < 2^12 on the accepted range)
     const double zs = __fma_rn(t, 0x1.71547652b82fep5, XG_SHIFT);
     const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(zs));
     const double kd = __dsub_rn(zs, XG_SHIFT);
     double r = __fma_rn(kd, -0x1.62e42fefa0000p-6, t);
     r = __fma_rn(kd, -0x1.cf79abc9e3b3ap-45, r);
-    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(kExp32Tab) + (ki & 31u));
+    const ulonglong2 e = tab(static_cast<uint32_t>(ki & 31u));
     const double tail = __longlong_as_double(static_cast<long long>(e.x));
     const uint64_t sbits = e.y + (ki << 47);
     double p = __fma_rn(r, 0x1.1111111111111p-7, 0x1.5555555555555p-5);
@@ -92,10 +105,9 @@ __device__ __forceinline__ float sigmoid32_fast(float x, bool& exact) {
     const double d = __dadd_rn(1.0, __fma_rn(scale, tmp, scale));
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-    // two Newton steps: one leaves too few bits for the rounding test (a
-    // one-step / one-constant-reduction variant failed the exhaustive check)
-    y = __fma_rn(y, __fma_rn(-d, y, 1.0), y);
-    y = __fma_rn(y, __fma_rn(-d, y, 1.0), y);
+    // third-order refinement: e = 1 - d y; y (1 + e + e^2) has error e^3
+    const double er = __fma_rn(-d, y, 1.0);
+    y = __fma_rn(y, __fma_rn(er, er, er), y);
     // y in (2^-125, 1]: distance of its low 29 mantissa bits from the float
     // rounding midpoint 2^28 (in double ulps of y)
     const uint64_t yb = static_cast<uint64_t>(__double_as_longlong(y));
@@ -118,9 +130,10 @@ __device__ __forceinline__ float sigmoid32_path(float x, bool& exact) {
 // (config 5 measured 4% slower out of line, profiles/r1_light_variants.txt).
 __device__ __noinline__ float sigmoid32_exact_call(float x) { return sigmoid32_exact(x); }
 
-__device__ __forceinline__ float sigmoid32(float x) {
+template <class TabLoad = ExpTabGlobal>
+__device__ __forceinline__ float sigmoid32(float x, TabLoad tab = TabLoad()) {
     bool exact;
-    const float f = sigmoid32_fast(x, exact);
+    const float f = sigmoid32_fast(x, exact, tab);
     return exact ? sigmoid32_exact_call(x) : f;
 }
 

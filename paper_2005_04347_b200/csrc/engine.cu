@@ -2,6 +2,7 @@
 // the C-ABI entry points of include/asnn_dev.h (except preprocessing, which
 // lives in preprocess.cu and corpora in netgen.cpp).
 #include <algorithm>
+#include <deque>
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -387,12 +388,18 @@ struct CtaPlan {
 // K-chain's prefix groups for NF-warp finish groups: two finish groups + NP
 // prefix groups + the producer warp within the 544-thread bound, at most four
 // (prefix depth D = NP - 1 <= 3).
-constexpr uint32_t chain_np(uint32_t nf) { return nf <= 2 ? 4u : nf == 3 ? 3u : 2u; }
+constexpr uint32_t chain_np(uint32_t nf) { return nf == 1 ? 8u : nf == 2 ? 4u : nf == 3 ? 3u : 2u; }
 
 constexpr uint32_t kMaxDynSmem = 227 * 1024;
 
 // K-chain staging groups take about 1/6 of the ring each: a handful in flight.
-uint32_t chain_group_target(const CtaPlan& p) { return std::max<uint32_t>(256, p.ring_bytes / 6); }
+uint32_t chain_group_target(const CtaPlan& p) {
+    static const uint32_t div = [] {  // experiments: ASNN_CHAIN_GROUP_DIV (ring / div per group)
+        const char* s = getenv("ASNN_CHAIN_GROUP_DIV");
+        return s ? std::max(1, atoi(s)) : 6;
+    }();
+    return std::max<uint32_t>(256, p.ring_bytes / div);
+}
 
 // ASNN_CTA_DEBUG (timing experiments only): 2 = no layer staging (read row
 // pointers and edges from global memory).
@@ -439,7 +446,8 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
         const uint64_t vq = C >= 4 ? 4 : 1;
         const uint64_t items_c = static_cast<uint64_t>(L->max_width) * (C / vq);
         const uint64_t nf = want_chain && want_pipe && vq == 1 && items_c <= 128 ? (items_c + 31) / 32 : 0;
-        const uint64_t pipe_c = nf ? chain::tail_bytes(static_cast<uint32_t>(nf)) - cta::kMetaBytes
+        const uint64_t pipe_c = nf ? chain::tail_bytes(static_cast<uint32_t>(nf), chain_np(static_cast<uint32_t>(nf))) -
+                                         cta::kMetaBytes
                                    : want_pipe && items_c <= 512 ? 2 * items_c * (vq + 1) * 4 : 0;
         const uint64_t fixed = as_bytes + cta::kMetaBytes + pipe_c;
         if (fixed + 1024 > kMaxDynSmem) {
@@ -1069,7 +1077,7 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
     // K-cta writes the declared outputs itself (shared-memory variant, no state)
     const bool cta_out = cp.use && !cp.global && !cp.win && !state && out && L->total_out;
     if (cp.use && cp.chain_nf) {
-        using KC = void (*)(const CtaNet*, const uint32_t*, const uint4*, const uint32_t*, const uint32_t*,
+        using KC = void (*)(const CtaNet*, const uint32_t*, const uint4*, const uint32_t*, const uint4*,
                             const uint32_t*, const uint2*, const uint4*, const uint4*, const float*, uint32_t, float*,
                             uint32_t, uint32_t, uint32_t, uint32_t, int, float*, const uint32_t*);
         static const KC kc[2][4] = {
@@ -1080,7 +1088,7 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
         const KC fn = kc[L->zero_refs ? 1 : 0][cp.chain_nf - 1];
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cp.smem)));
         fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T + 32, cp.smem, st>>>(
-            reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->grp.p, L->grp_off.p, L->lg_cat.p,
+            reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_base.p, L->grp.p, L->grp_off.p, L->lplan.p,
             L->row_ptr.p, L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos,
             cp.ring_bytes, (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr, L->split.p);
     } else if (cp.use) {
@@ -1221,47 +1229,103 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
     return ASNN_OK;
 }
 
-// K-chain staging groups: consecutive layers packed greedily while their row
-// pointers, splits and edges stay within `target` bytes in the ring (a layer
-// larger than that is a group alone).  Built on the host from the layer
-// bounds once per target (the plan's ring / 6).
-int ensure_groups(asnn_dev_layout* L, uint32_t target) {
-    if (L->grp.p && L->grp_target == target) return ASNN_OK;
+// K-chain staging plan (chain.cuh).  Groups: consecutive layers packed
+// greedily while their row pointers, splits and edges stay within `target`
+// bytes (a larger layer is a group alone).  The ring is then simulated on the
+// host exactly as a dynamic producer would run it -- byte-granular packing
+// with wrap, releases in group order, 32 mbarrier slots, and a group that
+// would need the release of the group just before it read from global memory
+// (F finishes a group's last layer only with the next group's first prefix)
+// -- so the device producer only executes the plan: per group {wait for the
+// release of group X, 3 bulk copies}.  Built once per (target, ring).
+int ensure_groups(asnn_dev_layout* L, uint32_t target, uint32_t ring) {
+    if (L->grp.p && L->grp_target == target && L->grp_ring == ring) return ASNN_OK;
     asnn_dev* dev = L->dev;
     const uint32_t G = static_cast<uint32_t>(L->nets.size());
-    std::vector<uint4> g;
-    std::vector<uint32_t> off(G + 1, 0), lg(L->le_host.size() + 1, 0);
+    std::vector<uint4> gp;                  // per group: 2 x uint4 (chain::GroupPlan)
+    std::vector<uint4> lp(2 * (L->le_host.size() + 1), make_uint4(0u, 0u, 0u, 0u));  // per layer
+    std::vector<uint32_t> off(G + 1, 0);
     for (uint32_t gi = 0; gi < G; ++gi) {
         const NetMeta& n = L->nets[gi];
         const uint32_t* lo = n.layer_offsets.data();
         const uint32_t* le = L->le_host.data() + L->lo_base_host[gi];
-        uint32_t* lgn = lg.data() + L->lo_base_host[gi];
-        off[gi] = static_cast<uint32_t>(g.size());
-        uint32_t l = 1;
-        while (l < n.n_layers) {
-            const uint32_t l0 = l, k = static_cast<uint32_t>(g.size()) - off[gi];
-            g.push_back(make_uint4(l0, lo[l0], le[l0], 0u));
-            lgn[l++] = k;
+        const uint32_t lb = L->lo_base_host[gi];
+        off[gi] = static_cast<uint32_t>(gp.size() / 2);
+        // groups of this network
+        std::vector<uint32_t> l0s;
+        for (uint32_t l = 1; l < n.n_layers;) {
+            const uint32_t l0 = l++;
+            l0s.push_back(l0);
             while (l < n.n_layers) {
                 uint32_t rb, sb, eb;
                 chain::group_bytes(n.pos_base + lo[l0], n.pos_base + lo[l + 1], le[l0], le[l + 1], rb, sb, eb);
                 if (static_cast<uint64_t>(rb) + sb + eb > target) break;
-                lgn[l++] = k;
+                ++l;
             }
         }
-        g.push_back(make_uint4(n.n_layers, lo[n.n_layers], le[n.n_layers], 0u));  // sentinel
+        l0s.push_back(n.n_layers);
+        const uint32_t K = static_cast<uint32_t>(l0s.size()) - 1;
+        // ring simulation
+        uint32_t w = 0, used = 0;
+        std::deque<std::pair<uint32_t, uint32_t>> live;  // (group, extent)
+        for (uint32_t k = 0; k < K; ++k) {
+            const uint32_t l0 = l0s[k], l1 = l0s[k + 1];
+            const uint32_t r0 = n.pos_base + lo[l0], r1 = n.pos_base + lo[l1];
+            uint32_t rb, sb, eb;
+            chain::group_bytes(r0, r1, le[l0], le[l1], rb, sb, eb);
+            const uint32_t size = rb + sb + eb;
+            int64_t wait = k >= cta::kSlots ? static_cast<int64_t>(k) - cta::kSlots : -1;  // slot reuse
+            while (!live.empty() && static_cast<int64_t>(live.front().first) <= wait) {
+                used -= live.front().second;
+                live.pop_front();
+            }
+            bool staged = size <= ring;
+            uint32_t at = 0;
+            if (staged) {
+                for (;;) {
+                    if (used == 0) w = 0;
+                    const bool wrap = w + size > ring;
+                    const uint32_t need = wrap ? ring - w + size : size;
+                    if (need <= ring - used) {
+                        at = wrap ? 0u : w;
+                        w = at + size;
+                        used += need;
+                        live.emplace_back(k, need);
+                        break;
+                    }
+                    if (live.front().first + 1 >= k) {  // only the previous group holds the space
+                        staged = false;
+                        break;
+                    }
+                    wait = std::max<int64_t>(wait, live.front().first);
+                    used -= live.front().second;
+                    live.pop_front();
+                }
+            }
+            const uint32_t r0a = r0 & ~3u, e0a = le[l0] & ~1u;
+            const uint32_t rows_at = at / 4, split_at = (at + rb) / 4, edges_at = (at + rb + sb) / 8;
+            gp.push_back(make_uint4(r0a, e0a, eb, static_cast<uint32_t>(wait + 1)));
+            gp.push_back(make_uint4(at | (staged ? chain::kPlanStaged : 0u), rb, sb, 0u));
+            for (uint32_t l = l0; l < l1; ++l) {
+                lp[2 * (lb + l)] = make_uint4(lo[l], lo[l + 1], k | (l + 1 == l1 ? chain::kPlanGroupEnd : 0u),
+                                              edges_at);
+                lp[2 * (lb + l) + 1] = make_uint4(r0a, e0a, rows_at | (staged ? chain::kPlanStaged : 0u), split_at);
+            }
+        }
     }
-    off[G] = static_cast<uint32_t>(g.size());
+    off[G] = static_cast<uint32_t>(gp.size() / 2);
+    if (gp.empty()) gp.push_back(make_uint4(0u, 0u, 0u, 0u));
     L->graph.reset();
     cudaStream_t st = dev->stream;
-    CK(L->grp.alloc(g.size()));
+    CK(L->grp.alloc(gp.size()));
     CK(L->grp_off.alloc(G + 1));
-    CK(L->lg_cat.alloc(lg.size()));
-    CK(cudaMemcpyAsync(L->grp.p, g.data(), g.size() * sizeof(uint4), cudaMemcpyHostToDevice, st));
+    CK(L->lplan.alloc(lp.size()));
+    CK(cudaMemcpyAsync(L->grp.p, gp.data(), gp.size() * sizeof(uint4), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(L->grp_off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(L->lg_cat.p, lg.data(), lg.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(L->lplan.p, lp.data(), lp.size() * sizeof(uint4), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));  // the host vectors go out of scope
     L->grp_target = target;
+    L->grp_ring = ring;
     return ASNN_OK;
 }
 
@@ -1286,7 +1350,7 @@ int ensure_workspace(asnn_dev_layout* L, uint32_t n_vec) {
         L->split_d = want_d;
     }
     if (cpl.use && cpl.chain_nf) {
-        const int rc = ensure_groups(L, chain_group_target(cpl));
+        const int rc = ensure_groups(L, chain_group_target(cpl), cpl.ring_bytes);
         if (rc) return rc;
     }
     if (seg_eligible(L, ldA)) {

@@ -256,12 +256,13 @@ struct asnn_dev_layout {
     // source is on the layer just below (k_splits)
     asnn_b200::DevBuf<uint32_t> split;     // [total_pos] absolute edge index
     uint32_t split_d = 0;                  // the prefix depth split[] was computed for
-    // K-chain staging groups (chain.cuh, ensure_groups): per network {first
-    // layer, lo, le, 0} records + a sentinel, their offsets, and layer -> group
+    // K-chain staging plan (chain.cuh, ensure_groups): per group 2 x uint4
+    // (chain::GroupPlan), per-network group offsets, per layer 2 x uint4
+    // (chain::LayerPlan, lo_cat indexing)
     asnn_b200::DevBuf<uint4> grp;
     asnn_b200::DevBuf<uint32_t> grp_off;   // [n_nets + 1]
-    asnn_b200::DevBuf<uint32_t> lg_cat;    // lo_cat indexing
-    uint32_t grp_target = 0;               // group byte target they were built for
+    asnn_b200::DevBuf<uint4> lplan;
+    uint32_t grp_target = 0, grp_ring = 0;  // group byte target and ring the plan was built for
     std::vector<uint32_t> le_host, lo_base_host;  // host copies of le_cat / lo_base
 
     ~asnn_dev_layout() { graph.reset(); }

@@ -194,6 +194,30 @@ int asnn_dev_layout_download(asnn_dev_layout* layout, uint32_t net_index, uint32
 int asnn_dev_activate(asnn_dev_layout* layout, const float* x, uint32_t n_vec, uint64_t n_x,
                       float* out, float* state);
 
+/* Batch-1 latency path (serve.cuh): a persistent one-CTA kernel that keeps
+ * a single-network layout resident in shared memory and polls a doorbell in
+ * page-locked host memory, so an activation costs no launch, copy call or
+ * stream synchronisation -- the drop-in per-vector eval_parallel of a small
+ * network (eval.cpp:49-80) at the latency of a PCIe round trip plus the
+ * sweep.  max_vec (1..64) bounds the vectors per request.
+ * ASNN_E_UNAVAILABLE when the layout holds several networks, does not fit
+ * one SM's shared memory, or max_vec * n_inputs exceeds 511.  The server
+ * is a persistent kernel on its own stream: it occupies one SM until
+ * stopped, and a device-wide synchronisation (cudaDeviceSynchronize) waits
+ * for it to exit -- synchronise streams instead.  asnn_dev_free_layout stops
+ * a live server. */
+typedef struct asnn_dev_server asnn_dev_server;
+int asnn_dev_server_start(asnn_dev_layout* layout, uint32_t max_vec, asnn_dev_server** out);
+/* Same contract as asnn_dev_activate with out != NULL, state == NULL:
+ * x[n_vec][n_inputs] (n_x == n_inputs * n_vec, else ASNN_E_ARITY),
+ * out[n_vec][n_outputs]; blocks until the outputs are in `out`. */
+int asnn_dev_server_activate(asnn_dev_server* server, const float* x, uint32_t n_vec, uint64_t n_x, float* out);
+void asnn_dev_server_stop(asnn_dev_server* server);
+/* The last activation's host round trip (inputs posted -> outputs seen, ns)
+ * and the device's phase times in SM cycles: [0] sensors, [1] layers,
+ * [2] outputs issued, [3] waiting for the request (polling). */
+int asnn_dev_server_timings(asnn_dev_server* server, double* host_ns, int64_t* device_cycles);
+
 /* Same, with device pointers, stream-ordered on the handle's stream (no
  * synchronisation).  x_dev [n_vec][n_inputs], out_dev [n_vec][n_outputs]. */
 int asnn_dev_activate_device(asnn_dev_layout* layout, const float* x_dev, uint32_t n_vec,
@@ -215,7 +239,8 @@ int asnn_dev_activate_plan(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* ke
  * launches of whole rows (k_rows / k_level, heavy rows on k_heavy), 1 =
  * per-level launches with heavy rows split into segments across the levels of
  * their sources (k_rows, long segments on k_heavy), 2 = one CTA per (network,
- * batch slice) for the whole sweep (k_cta). */
+ * batch slice) for the whole sweep (k_cta), 3 = the same with decoupled
+ * finish / prefix warps for deep, narrow layers (k_chain, chain.cuh). */
 int asnn_dev_sweep_kind(asnn_dev_layout* layout, uint32_t n_vec, uint32_t* kind);
 
 /* Debug: one sweep of n_vec (zero) vectors counting how often each op slot

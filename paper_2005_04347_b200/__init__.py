@@ -6,7 +6,7 @@ include/asnn_dev.h); this package is the host-side mirror of the reference
 API (see api.py) plus ctypes plumbing.
 """
 from .api import (  # noqa: F401
-    ActivationState, Backend, BackendUnavailable, Device, DeviceError, DeviceGroup, DeviceLayout,
+    ActivationState, Backend, BackendUnavailable, Device, DeviceError, DeviceGroup, DeviceLayout, Server,
     GenSpec, GroupLayout, comm_unique_id, device_generate_mlp, device_generate_powerlaw,
     InfeasibleSpec, InputArityMismatch, IoError, LayerAssignment, LayeredLayout, LayerOutOfRange,
     Network, OutputUnreachable, ParallelConfig, ParseError, RequiredSet, SplitMix64, UnassignedOutput,

@@ -95,6 +95,10 @@ PROTOTYPES = {
     "asnn_dev_layout_download": (C.c_int, [C.c_void_p, C.c_uint32, u32p, u32p, u64p, u32p, f32p, u32p]),
     "asnn_dev_activate": (C.c_int, [C.c_void_p, f32p, C.c_uint32, C.c_uint64, f32p, f32p]),
     "asnn_dev_activate_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p]),
+    "asnn_dev_server_start": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "asnn_dev_server_activate": (C.c_int, [C.c_void_p, f32p, C.c_uint32, C.c_uint64, f32p]),
+    "asnn_dev_server_stop": (None, [C.c_void_p]),
+    "asnn_dev_server_timings": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "asnn_dev_activate_plan": (C.c_int, [C.c_void_p, C.c_uint32, u32p, u64p, u64p]),
     "asnn_dev_profile_sweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, f32p, u32p]),
     "asnn_dev_sweep_kind": (C.c_int, [C.c_void_p, C.c_uint32, u32p]),
@@ -166,6 +170,8 @@ def load() -> C.CDLL:
         # by the caller as integers): no per-call ctypes casts
         lib.activate_addr = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64,
                                         C.c_void_p, C.c_void_p)(("asnn_dev_activate", lib))
+        lib.server_activate_addr = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64,
+                                               C.c_void_p)(("asnn_dev_server_activate", lib))
         _lib = lib
     return _lib
 

@@ -434,6 +434,9 @@ class DeviceLayout:
 
     def free(self):
         if self.h:
+            srv = getattr(self, "_server", None)
+            if srv is not None and srv.h:
+                srv.h = None  # asnn_dev_free_layout stops it
             self.dev.lib.asnn_dev_free_layout(self.h)
             self.h = None
 
@@ -481,7 +484,7 @@ class DeviceLayout:
         kind = C.c_uint32()
         self.dev.check(self.dev.lib.asnn_dev_sweep_kind(self.h, n_vec, C.byref(kind)))
         return {"kernels": k.value, "alg_bytes": b.value, "conn_evals": ce.value,
-                "strategy": ("rows", "segments", "k_cta")[kind.value]}
+                "strategy": ("rows", "segments", "k_cta", "k_chain")[kind.value]}
 
     def profile(self, x_ptr: int, n_vec: int, out_ptr: int) -> np.ndarray:
         """Per-stage device ms of one sweep (sensors, each level, gather)."""
@@ -526,6 +529,62 @@ class DeviceLayout:
         """Device pointers, stream-ordered on the device handle's stream."""
         self.dev.check(self.dev.lib.asnn_dev_activate_device(
             self.h, C.c_void_p(x_ptr), n_vec, C.c_void_p(out_ptr)))
+
+    def serve(self, max_vec: int = 1) -> "Server":
+        """Start the resident batch-1 server for this (single-network) layout
+        (asnn_dev_server_start, csrc/serve.cuh)."""
+        h = C.c_void_p()
+        self.dev.check(self.dev.lib.asnn_dev_server_start(self.h, max_vec, C.byref(h)))
+        self._server = Server(self, h, max_vec)
+        return self._server
+
+
+class Server:
+    """A persistent one-CTA kernel holding one layout in shared memory and
+    answering activations through a doorbell in page-locked host memory: no
+    launch or stream synchronisation per call.  Use as a context manager or
+    call close(); freeing the layout stops it too."""
+
+    def __init__(self, layout: "DeviceLayout", h, max_vec: int):
+        self.layout, self.h, self.max_vec = layout, h, max_vec
+        inf = layout.info() if layout._info is None else layout._info
+        layout._info = inf
+        self.n_in, self.n_out = inf["n_inputs"], inf["n_outputs"]
+
+    def activate(self, X: np.ndarray) -> np.ndarray:
+        """X: [n_vec][n_inputs] float32 -> outputs [n_vec][n_outputs]."""
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        if X.ndim == 1:
+            X = X[None, :]
+        out = np.empty((X.shape[0], self.n_out), np.float32)
+        self.layout.dev.check(self.layout.dev.lib.asnn_dev_server_activate(
+            self.h, _lib.ptr(X, C.c_float), X.shape[0], X.size, _lib.ptr(out, C.c_float)))
+        return out
+
+    def activate_ptr(self, x_ptr: int, n_vec: int, n_x: int, out_ptr: int):
+        """Raw host pointers (no per-call ctypes casts)."""
+        rc = self.layout.dev.lib.server_activate_addr(self.h, x_ptr, n_vec, n_x, out_ptr)
+        if rc:
+            self.layout.dev.check(rc)
+
+    def timings(self) -> dict:
+        """The last activation: host round trip (us) and device phases (cycles)."""
+        ns = C.c_double()
+        cyc = (C.c_int64 * 8)()
+        self.layout.dev.check(self.layout.dev.lib.asnn_dev_server_timings(self.h, C.byref(ns), cyc))
+        return {"round_trip_us": ns.value / 1e3, "sensors_cyc": cyc[0], "layers_cyc": cyc[1],
+                "outputs_cyc": cyc[2], "wait_cyc": cyc[3], "dbg": list(cyc[4:8])}
+
+    def close(self):
+        if self.h:
+            self.layout.dev.lib.asnn_dev_server_stop(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 class DeviceGroup:

@@ -3,6 +3,7 @@
 // lives in preprocess.cu and corpora in netgen.cpp).
 #include <algorithm>
 #include <deque>
+#include <mutex>
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -1739,6 +1740,7 @@ int asnn_dev_upload_layout(asnn_dev* dev, const asnn_layout_desc* d, asnn_dev_la
 
 void asnn_dev_free_layout(asnn_dev_layout* L) {
     if (!L) return;
+    if (L->server) asnn_dev_server_stop(L->server);
     std::lock_guard<std::recursive_mutex> lk(L->dev->mu);
     cudaSetDevice(L->dev->device);
     cudaStreamSynchronize(L->dev->stream);
@@ -1901,7 +1903,8 @@ int asnn_dev_activate_plan(asnn_dev_layout* L, uint32_t n_vec, uint32_t* kernels
 int asnn_dev_sweep_kind(asnn_dev_layout* L, uint32_t n_vec, uint32_t* kind) {
     if (!L || !kind) return ASNN_E_INVALID;
     const uint32_t ldA = padded_batch(n_vec);
-    *kind = cta_plan(L, ldA).use ? 2u : seg_eligible(L, ldA) ? 1u : 0u;
+    const CtaPlan cp = cta_plan(L, ldA);
+    *kind = cp.use ? (cp.chain_nf ? 3u : 2u) : seg_eligible(L, ldA) ? 1u : 0u;
     return ASNN_OK;
 }
 
@@ -2037,6 +2040,172 @@ int asnn_dev_activate(asnn_dev_layout* L, const float* x, uint32_t n_vec, uint64
     if (stage_out) std::memcpy(out, dev->pin_out.p, ob);
     cudaEventElapsedTime(&dev->timings.activate_ms, dev->ev0, dev->ev1);
     return ASNN_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Resident server (serve.cuh): the batch-1 latency path.
+struct asnn_dev_server {
+    asnn_dev_layout* L = nullptr;
+    cudaStream_t st = nullptr;
+    ServeCtl* ctl = nullptr;    // phase stamps (page-locked, mapped)
+    uint64_t* in_h = nullptr;   // [1 + max_vec * n_in] flagged records (page-locked, mapped)
+    uint64_t* out_h = nullptr;  // [max_vec * n_out]
+    uint32_t max_vec = 1, n_in = 0, n_out = 0, seq = 0;
+    double last_ns = 0;  // host round trip of the last activation (records out -> records back)
+    std::mutex mu;
+};
+
+namespace {
+void server_release(asnn_dev_server* s) {
+    if (s->st) cudaStreamDestroy(s->st);
+    if (s->ctl) cudaFreeHost(s->ctl);
+    if (s->in_h) cudaFreeHost(s->in_h);
+    if (s->out_h) cudaFreeHost(s->out_h);
+    delete s;
+}
+inline void put_rec(uint64_t* p, uint32_t v, uint32_t seq) {
+    *reinterpret_cast<volatile uint64_t*>(p) = static_cast<uint64_t>(seq) << 32 | v;
+}
+// host side of a request: every input slot (unused ones zero) and the header
+// carry seq, so each device thread's poll of its own record completes
+void server_post(asnn_dev_server* s, const float* x, uint32_t n_vec, uint32_t hdr) {
+    const uint32_t q = ++s->seq;
+    const uint32_t used = n_vec * s->n_in, slots = s->max_vec * s->n_in;
+    for (uint32_t k = 0; k < slots; ++k) {
+        uint32_t v = 0;
+        if (k < used) std::memcpy(&v, x + k, 4);
+        put_rec(s->in_h + 1 + k, v, q);
+    }
+    put_rec(s->in_h, hdr, q);
+}
+}  // namespace
+
+int asnn_dev_server_start(asnn_dev_layout* L, uint32_t max_vec, asnn_dev_server** out) {
+    if (!L || !out || max_vec == 0 || max_vec > 64) return ASNN_E_INVALID;
+    *out = nullptr;
+    asnn_dev* dev = L->dev;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    if (L->server) return fail(dev, ASNN_E_INVALID, "layout already has a live server");
+    if (L->nets.size() != 1) return fail(dev, ASNN_E_UNAVAILABLE, "the resident server takes one network");
+    const NetMeta& n = L->nets[0];
+    const uint32_t bytes = serve::smem_bytes(n.n_pos, L->total_edges, n.n_sensors, n.n_out, n.n_layers, max_vec);
+    if (bytes > kMaxDynSmem - 4096)
+        return fail(dev, ASNN_E_UNAVAILABLE,
+                    "network too large for one SM's shared memory (" + std::to_string(bytes) + " bytes)");
+    if (static_cast<uint64_t>(max_vec) * L->total_in > 511)
+        return fail(dev, ASNN_E_UNAVAILABLE, "more than 511 input values per request");
+    CK(cudaSetDevice(dev->device));
+    auto* s = new asnn_dev_server;
+    s->L = L;
+    s->max_vec = max_vec;
+    s->n_in = L->total_in;
+    s->n_out = L->total_out;
+    cudaError_t e;
+    auto bail = [&](cudaError_t err, const char* what) {
+        server_release(s);
+        return cuda_fail(dev, err, what);
+    };
+    const size_t in_n = 1 + static_cast<size_t>(max_vec) * s->n_in, out_n = std::max<size_t>(1, max_vec * s->n_out);
+    if ((e = cudaHostAlloc(&s->ctl, sizeof(ServeCtl), cudaHostAllocMapped)) != cudaSuccess) return bail(e, "ctl");
+    if ((e = cudaHostAlloc(&s->in_h, 8 * in_n, cudaHostAllocMapped)) != cudaSuccess) return bail(e, "in");
+    if ((e = cudaHostAlloc(&s->out_h, 8 * out_n, cudaHostAllocMapped)) != cudaSuccess) return bail(e, "out");
+    std::memset(s->ctl, 0, sizeof(ServeCtl));
+    std::memset(s->in_h, 0, 8 * in_n);
+    std::memset(s->out_h, 0, 8 * out_n);
+    void *ctl_d, *in_d, *out_d;
+    if ((e = cudaHostGetDevicePointer(&ctl_d, s->ctl, 0)) != cudaSuccess) return bail(e, "ctl map");
+    if ((e = cudaHostGetDevicePointer(&in_d, s->in_h, 0)) != cudaSuccess) return bail(e, "in map");
+    if ((e = cudaHostGetDevicePointer(&out_d, s->out_h, 0)) != cudaSuccess) return bail(e, "out map");
+    if ((e = cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking)) != cudaSuccess) return bail(e, "stream");
+    // the layout's arrays are complete on the handle's stream before the server starts
+    if ((e = cudaStreamSynchronize(dev->stream)) != cudaSuccess) return bail(e, "sync");
+    auto fn = L->zero_refs ? k_serve<true> : k_serve<false>;
+    if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes))) !=
+        cudaSuccess)
+        return bail(e, "smem attribute");
+    const uint32_t T = std::min<uint32_t>(
+        512, std::max<uint32_t>({64, (L->max_width * max_vec + 31) / 32 * 32,
+                                 static_cast<uint32_t>((in_n + 31) / 32 * 32)}));
+    fn<<<1, T, bytes, s->st>>>(reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->row_ptr.p,
+                               L->edges.p, L->sinfo.p, L->oinfo.p, static_cast<ServeCtl*>(ctl_d),
+                               static_cast<const uint2*>(in_d), static_cast<uint2*>(out_d), max_vec);
+    if ((e = cudaGetLastError()) != cudaSuccess) return bail(e, "k_serve launch");
+    L->server = s;
+    *out = s;
+    return ASNN_OK;
+}
+
+int asnn_dev_server_activate(asnn_dev_server* s, const float* x, uint32_t n_vec, uint64_t n_x, float* out) {
+    if (!s) return ASNN_E_INVALID;
+    asnn_dev* dev = s->L->dev;
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (n_x != static_cast<uint64_t>(s->n_in) * n_vec) {
+        std::lock_guard<std::recursive_mutex> lk2(dev->mu);
+        return fail(dev, ASNN_E_ARITY,
+                    "expected " + std::to_string(static_cast<uint64_t>(s->n_in) * n_vec) + " input values, got " +
+                        std::to_string(n_x));
+    }
+    if (n_vec == 0) return ASNN_OK;
+    if (n_vec > s->max_vec || (!x && n_x) || (!out && s->n_out)) {
+        std::lock_guard<std::recursive_mutex> lk2(dev->mu);
+        return fail(dev, ASNN_E_INVALID, "batch larger than the server's max_vec, or null buffer");
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    server_post(s, x, n_vec, n_vec);
+    const uint32_t q = s->seq;
+    const uint32_t m = n_vec * s->n_out;
+    const volatile uint64_t* rec = s->out_h;
+    // spin on the device's flagged outputs; every 64k polls check the kernel is alive
+    uint64_t spins = 0;
+    for (uint32_t j = 0; j < m; ++j) {
+        uint64_t r;
+        while (((r = rec[j]) >> 32) != q) {
+            if ((++spins & 0xFFFF) == 0) {
+                const cudaError_t e = cudaStreamQuery(s->st);
+                if (e != cudaErrorNotReady) {
+                    std::lock_guard<std::recursive_mutex> lk2(dev->mu);
+                    return cuda_fail(dev, e == cudaSuccess ? cudaErrorLaunchFailure : e, "resident server stopped");
+                }
+            }
+#if defined(__x86_64__)
+            __builtin_ia32_pause();
+#endif
+        }
+        const uint32_t v = static_cast<uint32_t>(r);
+        std::memcpy(out + j, &v, 4);
+    }
+    s->last_ns = std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
+    return ASNN_OK;
+}
+
+int asnn_dev_server_timings(asnn_dev_server* s, double* host_ns, int64_t* device_cycles) {
+    if (!s) return ASNN_E_INVALID;
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (host_ns) *host_ns = s->last_ns;
+    if (device_cycles) {
+        volatile ServeCtl* c = s->ctl;
+        device_cycles[0] = c->t_sens;
+        device_cycles[1] = c->t_layers;
+        device_cycles[2] = c->t_out;
+        device_cycles[3] = c->t_wait;
+        device_cycles[4] = c->t_dbg0;
+        device_cycles[5] = c->t_dbg1;
+        device_cycles[6] = c->t_dbg2;
+        device_cycles[7] = c->t_dbg3;
+    }
+    return ASNN_OK;
+}
+
+void asnn_dev_server_stop(asnn_dev_server* s) {
+    if (!s) return;
+    {
+        std::lock_guard<std::mutex> lk(s->mu);
+        server_post(s, nullptr, 0, kServeStop);
+        cudaStreamSynchronize(s->st);
+    }
+    if (s->L) s->L->server = nullptr;
+    server_release(s);
 }
 
 }  // extern "C"

@@ -265,6 +265,7 @@ struct asnn_dev_layout {
     uint32_t grp_target = 0, grp_ring = 0;  // group byte target and ring the plan was built for
     std::vector<uint32_t> le_host, lo_base_host;  // host copies of le_cat / lo_base
 
+    asnn_dev_server* server = nullptr;     // live resident server (asnn_dev_server_start)
     ~asnn_dev_layout() { graph.reset(); }
 };
 

@@ -204,3 +204,55 @@ extern "C" int ref_dev_resident_timed(const asnn::LayeredLayout* layout, const f
     stats_us(s, mean_us, sd_us);
     return 0;
 }
+
+// Resident server row (tools/bench_csv.py "device_server"): the layout uploaded
+// once and held by the persistent server kernel (asnn_dev_server_*), one
+// vector per request, the declared outputs back (read_outputs, eval.cpp:82-87).
+extern "C" int ref_dev_server_timed(const asnn::LayeredLayout* layout, const std::uint32_t* outputs,
+                                    std::uint32_t n_out, const float* x, std::uint32_t n_x, std::uint32_t warmup,
+                                    std::uint32_t reps, double* mean_us, double* sd_us) {
+    asnn_dev* dev = asnn::device();
+    std::vector<std::uint32_t> ids(layout->nodes.size()), in;
+    std::vector<std::uint64_t> rp(layout->nodes.size() + 1, 0);
+    std::vector<float> w;
+    for (std::size_t k = 0; k < layout->nodes.size(); ++k) {
+        ids[k] = layout->nodes[k].id;
+        in.insert(in.end(), layout->nodes[k].in_nodes.begin(), layout->nodes[k].in_nodes.end());
+        w.insert(w.end(), layout->nodes[k].in_weights.begin(), layout->nodes[k].in_weights.end());
+        rp[k + 1] = in.size();
+    }
+    asnn_layout_desc d{};
+    d.total_layers = layout->total_layers;
+    d.layer_offsets = layout->layer_offsets.data();
+    d.node_count = static_cast<std::uint32_t>(layout->nodes.size());
+    d.node_ids = ids.data();
+    d.row_ptr = rp.data();
+    d.in_nodes = in.data();
+    d.in_weights = w.data();
+    d.n_inputs = static_cast<std::uint32_t>(layout->input_order.size());
+    d.input_order = layout->input_order.data();
+    d.n_outputs = n_out;
+    d.outputs = outputs;
+    d.id_bound = layout->id_bound;
+    asnn_dev_layout* dl = nullptr;
+    if (asnn_dev_upload_layout(dev, &d, &dl)) return 6;
+    asnn_dev_server* srv = nullptr;
+    int rc = asnn_dev_server_start(dl, 1, &srv);
+    if (rc) {
+        asnn_dev_free_layout(dl);
+        return rc == ASNN_E_UNAVAILABLE ? 1 : 6;
+    }
+    std::vector<float> out(std::max<std::uint32_t>(1, n_out));
+    for (std::uint32_t i = 0; i < warmup + 2 && !rc; ++i) rc = asnn_dev_server_activate(srv, x, 1, n_x, out.data());
+    std::vector<double> s;
+    for (std::uint32_t i = 0; i < reps && !rc; ++i) {
+        const auto t0 = std::chrono::steady_clock::now();
+        rc = asnn_dev_server_activate(srv, x, 1, n_x, out.data());
+        s.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+    }
+    asnn_dev_server_stop(srv);
+    asnn_dev_free_layout(dl);
+    if (rc) return 6;
+    stats_us(s, mean_us, sd_us);
+    return 0;
+}

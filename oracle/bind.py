@@ -415,6 +415,25 @@ class RefDev(Ref):
             raise RuntimeError(f"device timing failed ({rc})")
         return m.value, sd.value
 
+    def server_timed(self, rn: "RefNet", x, warmup: int, reps: int):
+        """(mean_us, stddev_us) of one vector through the resident server
+        (asnn_dev_server_activate, declared outputs back), timed inside C++;
+        None when the network does not fit one SM's shared memory."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        outs = np.ascontiguousarray(rn.arrays()["outputs"], dtype=np.uint32)
+        m, sd = C.c_double(), C.c_double()
+        fn = self.L.ref_dev_server_timed
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_void_p, u32p, C.c_uint32, f32p, C.c_uint32, C.c_uint32, C.c_uint32,
+                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        rc = fn(self.L.ref_layout_ptr(rn.h), _p(outs, C.c_uint32), len(outs), _p(x, C.c_float), len(x), warmup,
+                reps, C.byref(m), C.byref(sd))
+        if rc == 1:
+            return None
+        if rc:
+            raise RuntimeError(f"server timing failed ({rc})")
+        return m.value, sd.value
+
     def eval_device(self, rn: "RefNet", x):
         """eval_parallel(..., DeviceCompute) on the reference's own LayeredLayout."""
         x = np.ascontiguousarray(x, dtype=np.float32)

@@ -2,7 +2,8 @@
 (tools/bench_csv.py) -- file set, headers, row order and number format of
 the reference's write_csv / write_meta (proj/src/bench.cpp:103-146), and the
 speedup files computed from the timing rows they claim (sequential over
-parallel, over device per call, over device resident)."""
+parallel, over device per call, over device resident, over the resident
+server)."""
 from __future__ import annotations
 
 import csv
@@ -13,7 +14,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-BACKENDS = ["sequential", "parallel", "device", "device_resident"]
+BACKENDS = ["sequential", "parallel", "device", "device_resident", "device_server"]
 
 
 def test_bench_csv_schema_and_speedups(tmp_path):
@@ -30,14 +31,16 @@ def test_bench_csv_schema_and_speedups(tmp_path):
                        "stddev_us"]
     body = rows[1:]
     ids = sorted({b[0] for b in body})
-    assert len(body) == 4 * len(ids) == 16
+    # the corpus networks all fit one SM's shared memory: every one has a server row
+    assert len(body) == 5 * len(ids) == 20
     # bench.cpp:105-110: by network_id (string order), then backend in enum order
     assert [b[0] for b in body] == [i for i in ids for _ in BACKENDS]
     assert [b[3] for b in body] == BACKENDS * len(ids)
-    assert [int(b[4]) for b in body] == [3, 4, 4, 4] * len(ids)
+    assert [int(b[4]) for b in body] == [3, 4, 4, 4, 4] * len(ids)
     t = {(b[0], b[3]): float(b[5]) for b in body}
     for name, den in (("speedup", "parallel"), ("device_speedup", "device"),
-                      ("device_resident_speedup", "device_resident")):
+                      ("device_resident_speedup", "device_resident"),
+                      ("device_server_speedup", "device_server")):
         s = list(csv.reader(open(f"{prefix}.{name}.csv")))
         assert s[0] == ["network_id", "connections", "layers", "speedup"]
         assert [x[0] for x in s[1:]] == ids

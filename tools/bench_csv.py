@@ -14,10 +14,14 @@ headers, row order and number format of bench.cpp:103-137):
                                             reference's LayeredLayout converted, uploaded,
                                             activated, state back, freed -- every call;
                           device_resident = asnn_dev_activate on a layout uploaded once
-                                            (state back)
+                                            (state back);
+                          device_server   = the resident server (asnn_dev_server_activate,
+                                            persistent kernel, declared outputs back) where
+                                            the network fits one SM's shared memory
   <prefix>.speedup.csv                  network_id,connections,layers,speedup  sequential / parallel
   <prefix>.device_speedup.csv           same columns, sequential / device (per call)
   <prefix>.device_resident_speedup.csv  same columns, sequential / device_resident
+  <prefix>.device_server_speedup.csv    same columns, sequential / device_server
   <prefix>.meta         key=value lines
 
 Usage: python tools/bench_csv.py --connections 1000,10000,100000 --depths 10,100 --csv out/bench
@@ -87,7 +91,7 @@ def main():
     depths = [int(x) for x in a.depths.split(",")]
     ref = RefDev()
     master = A.SplitMix64(a.seed)
-    records, speed, dspeed, rspeed, failures = [], [], [], [], []
+    records, speed, dspeed, rspeed, sspeed, failures = [], [], [], [], [], []
     for d in depths:
         for c in conns:
             nid = f"c{c}_d{d}"
@@ -113,28 +117,34 @@ def main():
                 # device rows through the reference-side binding, timed inside C++
                 dev = ref.timed(rn, x[0], resident=False, warmup=a.warmup, reps=a.reps_par)
                 res = ref.timed(rn, x[0], resident=True, warmup=a.warmup, reps=a.reps_par)
+                srv = ref.server_timed(rn, x[0], warmup=a.warmup, reps=a.reps_par)
                 records += [(nid, n_conn, layers, "sequential", a.reps_seq, *seq),
                             (nid, n_conn, layers, "parallel", a.reps_par, *par),
                             (nid, n_conn, layers, "device", a.reps_par, *dev),
                             (nid, n_conn, layers, "device_resident", a.reps_par, *res)]
+                if srv is not None:
+                    records.append((nid, n_conn, layers, "device_server", a.reps_par, *srv))
+                    sspeed.append((nid, n_conn, layers, seq[0] / srv[0]))
                 speed.append((nid, n_conn, layers, seq[0] / par[0]))
                 dspeed.append((nid, n_conn, layers, seq[0] / dev[0]))
                 rspeed.append((nid, n_conn, layers, seq[0] / res[0]))
                 print(f"{nid}: seq_us={format_double(seq[0])} par_us={format_double(par[0])} "
                       f"device_us={format_double(dev[0])} resident_us={format_double(res[0])} "
                       f"speedup={format_double(seq[0] / par[0])} device_speedup={format_double(seq[0] / dev[0])} "
-                      f"device_resident_speedup={format_double(seq[0] / res[0])}")
+                      f"device_resident_speedup={format_double(seq[0] / res[0])}"
+                      + (f" server_us={format_double(srv[0])}" if srv else ""))
             except Exception as e:  # bench.cpp:105-107: recorded and skipped
                 failures.append((nid, str(e)))
                 print(f"failed {nid}: {e}", file=sys.stderr)
-    order = {"sequential": 0, "parallel": 1, "device": 2, "device_resident": 3}
+    order = {"sequential": 0, "parallel": 1, "device": 2, "device_resident": 3, "device_server": 4}
     records.sort(key=lambda r: (r[0], order[r[3]]))
     with open(a.csv + ".timings.csv", "w") as f:
         f.write("network_id,connections,layers,backend,repetitions,mean_time_us,stddev_us\n")
         for r in records:
             f.write(f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]},{format_double(r[5])},{format_double(r[6])}\n")
     for path, rows in ((a.csv + ".speedup.csv", speed), (a.csv + ".device_speedup.csv", dspeed),
-                       (a.csv + ".device_resident_speedup.csv", rspeed)):
+                       (a.csv + ".device_resident_speedup.csv", rspeed),
+                       (a.csv + ".device_server_speedup.csv", sspeed)):
         with open(path, "w") as f:
             f.write("network_id,connections,layers,speedup\n")
             for r in sorted(rows):
@@ -148,7 +158,8 @@ def main():
                      ("corpus_inputs", 8), ("corpus_outputs", 2), ("input_value", a.input_value),
                      ("include_preprocessing", 0), ("device_backend", "B200 sm_100a (libasnn_b200.so)"),
                      ("device_path", "integration/asnn_device_backend.cpp eval_device (per call), "
-                                     "asnn_dev_activate (resident); timed in C++"),
+                                     "asnn_dev_activate (resident), asnn_dev_server_activate (server, "
+                                     "declared outputs); timed in C++"),
                      ("failures", len(failures))] + [(f"failure_{n}", r) for n, r in failures]:
             f.write(f"{k}={v}\n")
 

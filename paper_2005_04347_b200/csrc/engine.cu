@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "engine.hpp"
 #include "kernels.cuh"
 #include "sort.cuh"
@@ -1131,6 +1133,32 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
 }
 
 // Per-layer launches (k_level, plus k_heavy on the aux branch for heavy rows).
+// k_rows_tma (tma_rows.cuh): the TMA-gather level kernel for ldA a multiple
+// of 128; ASNN_LEVEL_VARIANT=13 selects it (experiments).
+bool tma_rows_enabled(uint32_t ldA) { return level_variant() == 13 && ldA >= 128 && ldA % 128 == 0; }
+
+int ensure_tmap_A(asnn_dev_layout* L, uint32_t ldA) {
+    if (L->tmA_base == L->A.p && L->tmA_ld == ldA) return ASNN_OK;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return fail(L->dev, ASNN_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {ldA, static_cast<cuuint64_t>(L->total_pos) + 1};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldA) * 4};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(tmarows::kTile), 1};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode(reinterpret_cast<CUtensorMap*>(L->tmA), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, L->A.p, dims,
+                              strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(L->dev, ASNN_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    L->tmA_base = L->A.p;
+    L->tmA_ld = ldA;
+    return ASNN_OK;
+}
+
 template <typename Mark>
 int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark) {
     asnn_dev* dev = L->dev;
@@ -1195,7 +1223,31 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
                 ll.warp_rows4<<<blocks_for(static_cast<uint64_t>(nrows + ns) * 32), kThreads, 0, st>>>(
                     L->edges.p, L->A.p, ldA, L->rtask.p + L->lvl_off[l] + nh, nrows,
                     segs ? L->seg.p + L->seg_short_off[l] : nullptr, ns, L->accbuf.p);
-            else if (ll.rows) {
+            else if (ll.rows && tma_rows_enabled(ldA)) {
+                RC_(ensure_tmap_A(L, ldA));
+                static bool attr_set = false;
+                if (!attr_set) {
+                    CK(cudaFuncSetAttribute(k_rows_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(tmarows::smem_bytes())));
+                    attr_set = true;
+                }
+                cudaLaunchConfig_t cfg{};
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.gridDim = dim3(static_cast<uint32_t>(std::min<uint64_t>(
+                    (items + tmarows::kWarps - 1) / tmarows::kWarps, 2ull * dev->sm_count)));
+                cfg.blockDim = dim3(32 * (tmarows::kWarps + 1));
+                cfg.dynamicSmemBytes = tmarows::smem_bytes();
+                cfg.stream = st;
+                cfg.attrs = attr;
+                cfg.numAttrs = pdl_enabled() && !fork && !prev_join && l > 1 ? 1 : 0;
+                CK(cudaLaunchKernelEx(&cfg, k_rows_tma, *reinterpret_cast<const CUtensorMap*>(L->tmA),
+                                      static_cast<const uint2*>(L->edges.p), L->A.p, ldA,
+                                      static_cast<const uint4*>(L->rtask.p + L->lvl_off[l] + nh), nrows, ll.tiles,
+                                      static_cast<const uint4*>(segs ? L->seg.p + L->seg_short_off[l] : nullptr), ns,
+                                      L->accbuf.p, L->total_pos));
+            } else if (ll.rows) {
                 cudaLaunchConfig_t cfg{};
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -266,6 +266,10 @@ struct asnn_dev_layout {
     std::vector<uint32_t> le_host, lo_base_host;  // host copies of le_cat / lo_base
 
     asnn_dev_server* server = nullptr;     // live resident server (asnn_dev_server_start)
+    // TMA descriptor of A for k_rows_tma (tma_rows.cuh), for (A, ldA) as built
+    alignas(64) unsigned char tmA[128] = {};
+    const float* tmA_base = nullptr;
+    uint32_t tmA_ld = 0;
     ~asnn_dev_layout() { graph.reset(); }
 };
 

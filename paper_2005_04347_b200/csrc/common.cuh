@@ -81,10 +81,14 @@ struct ExpTabGlobal {
 template <class TabLoad = ExpTabGlobal>
 __device__ __forceinline__ float sigmoid32_fast(float x, bool& exact, TabLoad tab = TabLoad()) {
     const double t = __dmul_rn(-4.97, static_cast<double>(x));
-    // exp(t) <= 2^-54: 1 + exp(t) == 1 in both, v clamps below 1 and the
-    // float rounds to 1 and clamps to 1 - FLT_EPSILON/2
-    const bool sat = t < -40.0;
-    const bool out = !(t < 86.0);  // float subnormal / clamped results, NaN
+    // decided on x with FP32 compares (the FP64 pipe binds populations):
+    // sat: x > 10 (t < -49.7): the true value is within 2^-71 of 1, the float
+    // rounds to 1 and clamps to 1 - FLT_EPSILON/2 -- and the fast path gives
+    // that same clamp on the band below (t in [-49.7, -40]) too;
+    // out: x <= -17 or NaN (t >= 84.49): float subnormal / clamped results
+    // go to the exact restatement (a superset of what needs it)
+    const bool sat = x > 10.0f;
+    const bool out = !(x > -17.0f);
     // k = round(t 32/ln2) in the low bits of zs; r = t - k ln2/32 with the hi
     // part of ln2/32 exact against k (|k| < 2^12 on the accepted range)
     const double zs = __fma_rn(t, 0x1.71547652b82fep5, XG_SHIFT);
@@ -109,10 +113,10 @@ __device__ __forceinline__ float sigmoid32_fast(float x, bool& exact, TabLoad ta
     const double er = __fma_rn(-d, y, 1.0);
     y = __fma_rn(y, __fma_rn(er, er, er), y);
     // y in (2^-125, 1]: distance of its low 29 mantissa bits from the float
-    // rounding midpoint 2^28 (in double ulps of y)
-    const uint64_t yb = static_cast<uint64_t>(__double_as_longlong(y));
-    const int64_t low = static_cast<int64_t>(yb & ((1ull << 29) - 1)) - (1ll << 28);
-    const bool near = low < (1ll << 12) && low > -(1ll << 12);
+    // rounding midpoint 2^28 (in double ulps of y), in 32-bit arithmetic:
+    // near <=> |low29 - 2^28| < 2^12 <=> low29 - (2^28 - 2^12 + 1) < 2^13 - 1
+    const uint32_t low29 = static_cast<uint32_t>(__double_as_longlong(y)) & ((1u << 29) - 1);
+    const bool near = low29 - ((1u << 28) - (1u << 12) + 1) < (1u << 13) - 1;
     float f = __double2float_rn(y);
     f = (sat || f >= 1.0f) ? 1.0f - 5.96046448e-08f : f;
     exact = out || (near && !sat);

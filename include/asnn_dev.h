@@ -136,9 +136,11 @@ int asnn_dev_set_heavy_threshold(asnn_dev* dev, uint32_t min_in_degree);
  * shared-memory-resident activations whenever they fit, 3 = one launch per
  * level with whole rows only, 4 = (one network) one CTA per batch column
  * keeping only a ring of the newest positions in shared memory and older
- * sources in HBM/L2, with the smallest legal ring (the windowed K-cta the
- * automatic choice uses for deep networks too large for one wave; forced
- * here to exercise it).  Also a scheduling knob: results are identical. */
+ * sources in HBM/L2, with the smallest legal ring (the windowed K-cta, an
+ * opt-in experiment: ASNN_CTA_WIN=1), 5 = (one network) the windowed K-chain
+ * (chain.cuh WIN: the automatic choice for deep, narrow networks whose
+ * one-column slices need more than one wave of CTAs; forced here to exercise
+ * it).  Also a scheduling knob: results are identical. */
 int asnn_dev_set_sweep_mode(asnn_dev* dev, uint32_t mode);
 int asnn_dev_last_timings(const asnn_dev* dev, asnn_timings* out);
 

@@ -49,6 +49,8 @@ __host__ __device__ constexpr uint32_t rec_bufs(uint32_t d) { return d < 4 ? 4u 
 constexpr uint32_t kTailMask = 0xFFFFu;
 constexpr uint32_t kGroupEnd = 1u << 21;  // the layer is its staging group's last
 constexpr uint32_t kUnstaged = 1u << 22;  // the tail's edges beyond the second are in global memory
+constexpr uint32_t kVal0 = 1u << 23;      // WIN: ra.z holds the first tail source's value (not an address)
+constexpr uint32_t kVal1 = 1u << 24;      // WIN: rb.x holds the second's
 // Staging plan records (ensure_groups): per group {r0a, e0a, ebytes, wait+1},
 // {at | kPlanStaged, rbytes, sbytes, 0}; per layer {a, b, group | kPlanGroupEnd,
 // edges_at}, {r0a, e0a, rows_at | kPlanStaged, split_at}.
@@ -145,14 +147,21 @@ __device__ __forceinline__ void produce_plan(const uint4* __restrict__ plan, uin
 }
 }  // namespace chain
 
-template <int NF, int NP, bool GUARD>
-__global__ void __launch_bounds__(32 * (NF * (2 + NP) + 1))
+// WIN (the full slice would need more than one wave of CTAs, config 3): the
+// CTA keeps only a ring of the newest W positions in shared memory (slot =
+// local position & win_mask) and every activation is written through to A.
+// The prefix warps read their sources -- all final, D steps old -- from A (L2;
+// they have D steps of slack), and resolve the inline tail edges whose
+// sources are already final into values; the finish warps read only sources
+// of the last D layers, from the ring.  Two CTAs per SM: one wave.
+template <int NF, int NP, bool GUARD, bool WIN>
+__global__ void __launch_bounds__(32 * (NF * (2 + NP) + 1), WIN ? 2 : 1)
 k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ unused, const uint4* __restrict__ grp,
         const uint32_t* __restrict__ grp_off, const uint4* __restrict__ lplan,
         const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, const uint4* __restrict__ sinfo,
         const uint4* __restrict__ oinfo, const float* __restrict__ x, uint32_t n_vec, float* __restrict__ A,
         uint32_t ldA, uint32_t C, uint32_t max_pos, uint32_t ring_bytes, int write_all, float* __restrict__ out,
-        const uint32_t* __restrict__ split) {
+        const uint32_t* __restrict__ split, uint32_t win_mask) {
     using namespace cta;
     constexpr uint32_t D = NP - 1;
     constexpr uint32_t kRecBufs = chain::rec_bufs(D);
@@ -161,9 +170,10 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ unused, co
     extern __shared__ __align__(128) unsigned char cta_smem[];
     const CtaNet n = nets[blockIdx.y];
     const uint32_t c0 = blockIdx.x * C;
-    float* As = reinterpret_cast<float*>(cta_smem);  // [max_pos + 1][C], row max_pos = zeros
-    const uint32_t zero_slot = max_pos;
-    const size_t as_floats = (static_cast<size_t>(zero_slot + 1) * C + 3) & ~size_t(3);
+    float* As = reinterpret_cast<float*>(cta_smem);  // [max_pos + 1][C], row max_pos = zeros (WIN: [W][C] ring)
+    const uint32_t zero_slot = WIN ? 0u : max_pos;
+    const size_t as_floats = ((static_cast<size_t>(WIN ? win_mask + 1 : zero_slot + 1)) * C + 3) & ~size_t(3);
+    float* Ag = A + c0;  // WIN: the written-through activations, row stride ldA
     unsigned char* ring = reinterpret_cast<unsigned char*>(As + as_floats);
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + ring_bytes);
     uint64_t* empty = full + kSlots;
@@ -207,12 +217,18 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ unused, co
     // stores of items past a layer's width
     const uint32_t as_sh = heavy::smem_u32(As);
     const uint32_t tab_sh = heavy::smem_u32(meta), scratch_sh = tab_sh + 512;
-    auto addr = [&](uint32_t pos, uint32_t q) -> uint32_t { return as_sh + 4 * off(pos, q); };
+    auto addr = [&](uint32_t pos, uint32_t q) -> uint32_t {
+        if constexpr (WIN) return as_sh + 4 * (((pos - n.pos_base) & win_mask) * C + q);
+        else return as_sh + 4 * off(pos, q);
+    };
+    // WIN: a final source's value from A (absolute position; the zero row is zero)
+    auto gval = [&](uint32_t pos, uint32_t q) -> float { return Ag[static_cast<size_t>(pos) * ldA + q]; };
 
     if (tid >= Tc) {
         if (tid == Tc) chain::produce_plan(gplan, n_groups, row_ptr, split, edges, ring, full, empty);
     } else {
-        for (uint32_t c = tid; c < C; c += Tc) As[zero_slot * C + c] = 0.0f;
+        if constexpr (!WIN)
+            for (uint32_t c = tid; c < C; c += Tc) As[zero_slot * C + c] = 0.0f;
         for (uint32_t i = tid; i < 64; i += Tc) reinterpret_cast<uint64_t*>(meta)[i] = kExp32Tab[i];
         // sensors (eval.cpp:17), as K-cta
         for (uint32_t i = tid; i < n.n_sensors * C; i += Tc) {
@@ -222,7 +238,13 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ unused, co
             float xv = 0.0f;
             if (col < n_vec && k != kUnassigned)
                 xv = x[static_cast<uint64_t>(n_vec) * n.in_prefix + static_cast<uint64_t>(col) * n.n_in + k];
-            As[static_cast<size_t>(s) * C + c] = sigmoid32(xv);
+            const float sv = sigmoid32(xv);
+            if constexpr (WIN) {
+                Ag[static_cast<size_t>(n.pos_base + s) * ldA + c] = sv;
+                As[static_cast<size_t>(s & win_mask) * C + c] = sv;
+            } else {
+                As[static_cast<size_t>(s) * C + c] = sv;
+            }
             wc_note(n.pos_base + s, col, 1);
         }
         consumer_barrier(Tc);
@@ -235,10 +257,20 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ unused, co
             // layer m's plan, loaded one layer of this group ahead
             uint32_t m = 1 + j;
             uint4 pa_n = make_uint4(0u, 0u, 0u, 0u), pb_n = pa_n;
-            if (m < n.n_layers) pa_n = lp[2 * m], pb_n = lp[2 * m + 1];
+            // WIN: lo[m - D], the first position whose value may not be final
+            // when this prefix runs (sources below it are read from A)
+            uint32_t rec_n = 0;
+            if (m < n.n_layers) {
+                pa_n = lp[2 * m], pb_n = lp[2 * m + 1];
+                if (WIN && m > D) rec_n = lp[2 * (m - D)].x;
+            }
             for (; m < n.n_layers; m += NP) {
                 const uint4 pa = pa_n, pb = pb_n;
-                if (m + NP < n.n_layers) pa_n = lp[2 * (m + NP)], pb_n = lp[2 * (m + NP) + 1];
+                const uint32_t recent = rec_n;
+                if (m + NP < n.n_layers) {
+                    pa_n = lp[2 * (m + NP)], pb_n = lp[2 * (m + NP) + 1];
+                    if (WIN && m + NP > D) rec_n = lp[2 * (m + NP - D)].x;
+                }
                 const uint32_t a = pa.x, b = pa.y, g = pa.z & ~chain::kPlanGroupEnd;
                 const bool gend = (pa.z & chain::kPlanGroupEnd) != 0;
                 const uint32_t edges_at = pa.w, r0a = pb.x, e0a = pb.y, split_at = pb.w;
@@ -255,10 +287,12 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ unused, co
                     const uint32_t k = m - D - 2;  // layer k + 1 (>= 1) done: phase k / kDoneBars
                     chain::mbar_wait_sleep(&done_bar[k % chain::kDoneBars], (k / chain::kDoneBars) & 1);
                 }
-                const uint32_t zo = as_sh + 4 * (zero_slot * C + q);
                 // every item carries the staging slot and group end (F's lane 0
-                // releases); an item past the width: sigmoid of +0 into scratch
-                const uint32_t tag = (g % kSlots) << 16 | (gend ? chain::kGroupEnd : 0u);
+                // releases); an item past the width: sigmoid of +0 into scratch;
+                // missing tail edges: the zero row (WIN: the value 0) with weight 0
+                const uint32_t tag = (g % kSlots) << 16 | (gend ? chain::kGroupEnd : 0u) |
+                                     (WIN ? chain::kVal0 | chain::kVal1 : 0u);
+                const uint32_t zo = WIN ? 0u : as_sh + 4 * (zero_slot * C + q);
                 uint4 ra = make_uint4(0u, scratch_sh, zo, 0u), rb = make_uint4(zo, 0u, tag, 0u);
                 if (i < b - a) {
                     const uint32_t r = n.pos_base + a + i;
@@ -272,36 +306,54 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ unused, co
                     }
                     // absolute edge index -> the staged copy (or global memory)
                     const uint2* Ep = st ? ring_u2 + edges_at - e0a : edges;
-                    float acc = 0.0f;
-                    for (; k + 8 <= ks; k += 8) {
-                        uint2 ed[8];
-                        float av[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) ed[u] = Ep[k + u];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) av[u] = As[off(ed[u].x, q)];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) acc = mac(acc, __uint_as_float(ed[u].y), av[u]);
-                    }
-                    for (; k < ks; ++k) {
-                        const uint2 ed = Ep[k];
-                        acc = mac(acc, __uint_as_float(ed.y), As[off(ed.x, q)]);
-                    }
-                    ra.x = __float_as_uint(acc);
-                    ra.y = as_sh + 4 * ((a + i) * C + q);
+                    // (the tail first: its final sources' loads overlap the prefix's)
+                    ra.y = WIN ? as_sh + 4 * (((a + i) & win_mask) * C + q) : as_sh + 4 * ((a + i) * C + q);
+                    uint32_t vflags = WIN ? chain::kVal0 | chain::kVal1 : 0u;
+                    // WIN: a tail source below `recent` is final now -- its value
+                    // goes into the record; the others are read from the ring
+                    auto tail_src = [&](uint32_t pos, uint32_t vbit) -> uint32_t {
+                        if constexpr (WIN) {
+                            if (pos - n.pos_base >= recent && pos - n.pos_base < n.n_pos) {
+                                vflags &= ~vbit;
+                                return addr(pos, q);
+                            }
+                            return __float_as_uint(gval(pos, q));
+                        } else {
+                            return addr(pos, q);
+                        }
+                    };
                     if (ke > ks) {
                         const uint2 e0 = Ep[ks];
-                        ra.z = addr(e0.x, q);
+                        ra.z = tail_src(e0.x, chain::kVal0);
                         ra.w = e0.y;
                     }
                     if (ke > ks + 1) {
                         const uint2 e1 = Ep[ks + 1];
-                        rb.x = addr(e1.x, q);
+                        rb.x = tail_src(e1.x, chain::kVal1);
                         rb.y = e1.y;
                     }
+                    // batches of 8 (the last one predicated): all of a batch's
+                    // source loads in flight together -- under WIN they are L2
+                    // round trips, which a one-edge remainder loop would serialise
+                    float acc = 0.0f;
+                    for (; k < ks; k += 8) {
+                        const uint32_t nb = min(8u, ks - k);
+                        uint2 ed[8];
+                        float av[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (u < nb) ed[u] = Ep[k + u];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (u < nb) av[u] = WIN ? gval(ed[u].x, q) : As[off(ed[u].x, q)];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (u < nb) acc = mac(acc, __uint_as_float(ed[u].y), av[u]);
+                    }
+                    ra.x = __float_as_uint(acc);
                     // F reads edges beyond the second from ring_u2 (staged,
                     // index relative to the ring) or edges (absolute)
-                    rb.z = tag | (ke - ks) | (st ? 0u : chain::kUnstaged);
+                    rb.z = ((tag & ~(chain::kVal0 | chain::kVal1)) | vflags) | (ke - ks) | (st ? 0u : chain::kUnstaged);
                     rb.w = st ? edges_at + ks + 2 - e0a : ks + 2;
                 }
                 recA[((m - 1) % kRecBufs) * I + it] = ra;
@@ -322,27 +374,51 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ unused, co
             };
             uint4 ra = make_uint4(0u, 0u, 0u, 0u), rb = ra;
             uint32_t l = 1 + f;
-            if (l < n.n_layers) wait_rec(l, ra, rb);
+            uint32_t lo_l = 0;  // WIN: lo[l], for the write-through position
+            if (l < n.n_layers) {
+                wait_rec(l, ra, rb);
+                if (WIN) lo_l = lp[2 * l].x;
+            }
             for (; l < n.n_layers; l += 2) {
+                const uint32_t lo_next = WIN && l + 2 < n.n_layers ? lp[2 * (l + 2)].x : 0u;
                 // layer l-1 final (the other group; layer 0: the sensor barrier)
                 if (l > 1) chain::f_sync(2 + f, kPair);
-                const float v0 = chain::lds_f32(ra.z), v1 = chain::lds_f32(rb.x);
                 const uint32_t flags = rb.z, nt = flags & chain::kTailMask;
+                float v0 = __uint_as_float(ra.z), v1 = __uint_as_float(rb.x);
+                if (!WIN || !(flags & chain::kVal0)) v0 = chain::lds_f32(ra.z);
+                if (!WIN || !(flags & chain::kVal1)) v1 = chain::lds_f32(rb.x);
                 float acc = __uint_as_float(ra.x);
                 acc = mac(acc, __uint_as_float(ra.w), v0);
                 acc = mac(acc, __uint_as_float(rb.y), v1);
                 if (nt > 2) {  // longer tails (and whole rows of layers <= D)
                     const uint2* Eb = (flags & chain::kUnstaged) ? edges : ring_u2;
                     const uint32_t ke = rb.w - 2 + nt;
+                    // WIN: sources below lo[l - D] are final and may have left the ring
+                    const uint32_t recent = WIN && l > D ? lp[2 * (l - D)].x : 0u;
                     for (uint32_t k = rb.w; k < ke; ++k) {
                         const uint2 ed = Eb[k];
-                        acc = mac(acc, __uint_as_float(ed.y), chain::lds_f32(addr(ed.x, q)));
+                        float v;
+                        if constexpr (WIN)
+                            v = ed.x - n.pos_base >= recent && ed.x - n.pos_base < n.n_pos
+                                    ? chain::lds_f32(addr(ed.x, q)) : gval(ed.x, q);
+                        else
+                            v = chain::lds_f32(addr(ed.x, q));
+                        acc = mac(acc, __uint_as_float(ed.y), v);
                     }
                 }
-                chain::sts_f32(ra.y, sigmoid32(acc, chain::ExpTabShared{tab_sh}));
+                const float y = sigmoid32(acc, chain::ExpTabShared{tab_sh});
+                chain::sts_f32(ra.y, y);
+                // WIN: the write-through precedes the handoff -- a prefix warp
+                // that saw layer l+1 done (done_bar, released after the other
+                // group's barrier.sync) must also see layer l in A
+                const uint32_t pos_w = n.pos_base + lo_l + it / C;  // WIN: this item's position
+                if constexpr (WIN)
+                    if (ra.y != scratch_sh) Ag[static_cast<size_t>(pos_w) * ldA + q] = y;
                 if (l + 1 < n.n_layers) chain::f_arrive(2 + (1 - f), kPair);  // layer l final
+                lo_l = lo_next;
 #ifdef ASNN_WRITE_COUNT
-                if (ra.y != scratch_sh) wc_note(n.pos_base + (ra.y - as_sh) / 4 / C, c0 + q, 1);
+                if (ra.y != scratch_sh)
+                    wc_note(WIN ? pos_w : n.pos_base + (ra.y - as_sh) / 4 / C, c0 + q, 1);
 #endif
                 __syncwarp();
                 if (lane == 0) {
@@ -354,5 +430,18 @@ k_chain(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ unused, co
         }
     }
     __syncthreads();
-    write_back(n, As, C, A, ldA, c0, n_vec, oinfo, out, write_all, tid, blockDim.x);
+    if constexpr (WIN) {
+        // every activation is already in A: only the declared outputs (eval.cpp:82-87)
+        if (out) {
+            const uint32_t vcols = c0 < n_vec ? min(C, n_vec - c0) : 0u;
+            for (uint32_t i = tid; i < n.n_out * vcols; i += blockDim.x) {
+                const uint32_t c = i / n.n_out, j = i - c * n.n_out;
+                const uint32_t pos = oinfo[n.out_prefix + j].x;
+                out[static_cast<uint64_t>(n_vec) * n.out_prefix + static_cast<uint64_t>(c0 + c) * n.n_out + j] =
+                    pos != kUnassigned ? Ag[static_cast<size_t>(pos) * ldA + c] : 0.0f;
+            }
+        }
+    } else {
+        write_back(n, As, C, A, ldA, c0, n_vec, oinfo, out, write_all, tid, blockDim.x);
+    }
 }

@@ -386,6 +386,7 @@ struct CtaPlan {
     uint32_t win_mask = 0;
     uint32_t stg_edges = 0;  // WIN + pipe: staged prefix sources per layer (0 = direct loads)
     uint32_t chain_nf = 0;   // K-chain (chain.cuh): finish warps (0 = not used)
+    bool chain_win = false;  // K-chain with a ring of the newest positions (WIN)
 };
 
 // K-chain's prefix groups for NF-warp finish groups: two finish groups + NP
@@ -556,7 +557,54 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
             p.pipe = pipe_c > 0;
         }
     }
-    if (want_global && L->nets.size() == 1 && smem_waves > 1 && a_bytes <= (96ull << 20) &&
+    // Windowed K-chain (chain.cuh WIN): a deep, narrow network whose
+    // one-column slices need more than one wave (config 3: 256 CTAs of
+    // 232 KB, two waves) runs one wave at two CTAs per SM, each keeping the
+    // newest W positions in shared memory and writing every activation
+    // through to A (which must sit in L2).  Opt-in (ASNN_CHAIN_WIN=1; sweep
+    // mode 5 forces it for the tests): on config 3 it measured 1.23 ms
+    // against 0.88 ms for the two full-slice waves -- the prefix warps' L2
+    // round trips and two CTAs' warps per SM stretch the per-layer chain from
+    // ~430 to ~1200 cycles (profiles/r2_c3_chain_window.txt).
+    static const bool want_chain_win = [] {
+        const char* s = getenv("ASNN_CHAIN_WIN");
+        return s && s[0] == '1';
+    }();
+    const bool force_cwin = mode == 5 && L->nets.size() == 1 && want_chain;
+    if ((force_cwin || (want_chain_win && p.chain_nf && smem_waves > 1)) && L->nets.size() == 1 &&
+        a_bytes <= (96ull << 20) && L->max_width <= 128) {
+        // the fewest columns per CTA that still fill a wave of two CTAs per SM
+        uint32_t C = 1;
+        while (ldA / C > 2 * sms && C < 2 && ldA % (2 * C) == 0) C <<= 1;
+        const uint64_t items_c = static_cast<uint64_t>(L->max_width) * C;
+        if (items_c <= 128) {
+            const uint32_t nf = static_cast<uint32_t>((items_c + 31) / 32), np = chain_np(nf);
+            const uint64_t D = np - 1;
+            uint64_t W = 64;
+            while (W < 2 * (D + 2) * static_cast<uint64_t>(L->max_width)) W *= 2;
+            const uint64_t wb = (W * C * 4 + 15) / 16 * 16;
+            const uint64_t tail = chain::tail_bytes(nf, np);
+            static const uint64_t cps = [] {  // experiments: CTAs per SM the ring is sized for
+                const char* s = getenv("ASNN_CHAIN_WIN_CTAS");
+                return static_cast<uint64_t>(s ? std::max(1, atoi(s)) : 2);
+            }();
+            const uint64_t budget = std::min<uint64_t>(kMaxDynSmem, per_sm / cps - 1024);
+            const uint64_t ring = budget > wb + tail ? std::min<uint64_t>(budget - wb - tail, 32 * max_layer) / 16 * 16
+                                                     : 0;
+            if (ring >= 2 * max_layer || (force_cwin && ring >= 1024)) {
+                p.C = C;
+                p.chain_nf = nf;
+                p.chain_win = true;
+                p.win = false;
+                p.pipe = false;
+                p.global = false;
+                p.win_mask = static_cast<uint32_t>(W - 1);
+                p.ring_bytes = static_cast<uint32_t>(ring);
+                p.smem = static_cast<uint32_t>(wb + tail + ring);
+            }
+        }
+    }
+    if (want_global && L->nets.size() == 1 && !p.chain_win && smem_waves > 1 && a_bytes <= (96ull << 20) &&
         !L->zero_refs) {
         uint32_t C = 1;
         while (ldA / C > sms && C < 128) C <<= 1;
@@ -603,7 +651,7 @@ CtaPlan cta_plan(const asnn_dev_layout* L, uint32_t ldA) {
     const double cta_us = (1.2 * L->n_levels + static_cast<double>(L->total_edges) / L->nets.size() * p.C / 1100.0) *
                           static_cast<double>((ctas + per_wave - 1) / per_wave);
     const double level_us = 7.0 * L->n_levels;
-    p.use = mode == 2 || force_win || (latency_bound && (L->nets.size() > 1 || cta_us <= level_us));
+    p.use = mode == 2 || force_win || (force_cwin && p.chain_win) || (latency_bound && (L->nets.size() > 1 || cta_us <= level_us));
     return p;
 }
 
@@ -1082,18 +1130,22 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
     if (cp.use && cp.chain_nf) {
         using KC = void (*)(const CtaNet*, const uint32_t*, const uint4*, const uint32_t*, const uint4*,
                             const uint32_t*, const uint2*, const uint4*, const uint4*, const float*, uint32_t, float*,
-                            uint32_t, uint32_t, uint32_t, uint32_t, int, float*, const uint32_t*);
-        static const KC kc[2][4] = {
-            {k_chain<1, chain_np(1), false>, k_chain<2, chain_np(2), false>, k_chain<3, chain_np(3), false>,
-             k_chain<4, chain_np(4), false>},
-            {k_chain<1, chain_np(1), true>, k_chain<2, chain_np(2), true>, k_chain<3, chain_np(3), true>,
-             k_chain<4, chain_np(4), true>}};
-        const KC fn = kc[L->zero_refs ? 1 : 0][cp.chain_nf - 1];
+                            uint32_t, uint32_t, uint32_t, uint32_t, int, float*, const uint32_t*, uint32_t);
+        static const KC kc[2][2][4] = {
+            {{k_chain<1, chain_np(1), false, false>, k_chain<2, chain_np(2), false, false>,
+              k_chain<3, chain_np(3), false, false>, k_chain<4, chain_np(4), false, false>},
+             {k_chain<1, chain_np(1), true, false>, k_chain<2, chain_np(2), true, false>,
+              k_chain<3, chain_np(3), true, false>, k_chain<4, chain_np(4), true, false>}},
+            {{k_chain<1, chain_np(1), false, true>, k_chain<2, chain_np(2), false, true>,
+              k_chain<3, chain_np(3), false, true>, k_chain<4, chain_np(4), false, true>},
+             {k_chain<1, chain_np(1), true, true>, k_chain<2, chain_np(2), true, true>,
+              k_chain<3, chain_np(3), true, true>, k_chain<4, chain_np(4), true, true>}}};
+        const KC fn = kc[cp.chain_win ? 1 : 0][L->zero_refs ? 1 : 0][cp.chain_nf - 1];
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cp.smem)));
         fn<<<dim3(ldA / cp.C, static_cast<uint32_t>(L->nets.size())), cp.T + 32, cp.smem, st>>>(
             reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_base.p, L->grp.p, L->grp_off.p, L->lplan.p,
             L->row_ptr.p, L->edges.p, L->sinfo.p, L->oinfo.p, x, n_vec, L->A.p, ldA, cp.C, L->max_pos,
-            cp.ring_bytes, (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr, L->split.p);
+            cp.ring_bytes, (state ? 1 : 0) | cta_debug_flags(), cta_out ? out : nullptr, L->split.p, cp.win_mask);
     } else if (cp.use) {
         // the whole sweep (sensors + every layer) of each (network, slice) in one CTA
         auto fn = cp.win ? (cp.pipe ? (L->zero_refs ? k_cta<1, true, false, true, true> : k_cta<1, false, false, true, true>)
@@ -1678,7 +1730,7 @@ int asnn_dev_set_stream(asnn_dev* dev, void* s) {
 void* asnn_dev_get_stream(asnn_dev* dev) { return dev ? dev->stream : nullptr; }
 
 int asnn_dev_set_sweep_mode(asnn_dev* dev, uint32_t mode) {
-    if (!dev || mode > 4) return ASNN_E_INVALID;
+    if (!dev || mode > 5) return ASNN_E_INVALID;
     std::lock_guard<std::recursive_mutex> lk(dev->mu);
     dev->sweep_mode = mode;
     ++dev->option_epoch;

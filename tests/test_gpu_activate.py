@@ -20,13 +20,15 @@ pytestmark = pytest.mark.gpu
 DEV = A.ParallelConfig(backend=A.Backend.DeviceCompute)
 
 
-@pytest.fixture(params=[1, 2, 3, 4], ids=["layer-launches", "k_cta", "whole-rows", "k_cta-window"])
+@pytest.fixture(params=[1, 2, 3, 4, 5], ids=["layer-launches", "k_cta", "whole-rows", "k_cta-window",
+                                              "k_chain-window"])
 def sweep_mode(request):
     """Run a test under every sweep strategy: one launch per dependency level
     (heavy rows split into segments where eligible), the one-CTA-per-slice
-    sweep (k_cta), per-level launches of whole rows (k_rows/k_level +
-    k_heavy), and the windowed k_cta (a ring of the newest positions in
-    shared memory, older sources from A) with its smallest ring."""
+    sweep (k_cta / k_chain), per-level launches of whole rows (k_rows/k_level +
+    k_heavy), the windowed k_cta (a ring of the newest positions in shared
+    memory, older sources from A) with its smallest ring, and the windowed
+    k_chain (chain.cuh WIN, forced on single networks)."""
     dev = A.Device.get(0)
     dev.set_sweep_mode(request.param)
     yield request.param

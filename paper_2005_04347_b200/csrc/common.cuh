@@ -66,7 +66,7 @@ __device__ __forceinline__ float sigmoid32_exact(float x) {
 // The fast path is straight-line code (selects, no branches) so that the V
 // evaluations of a column group interleave their FP64 dependency chains;
 // sigmoid32_v takes the exact restatement in one rarely-taken branch after
-// all of them.  Saturated (t < -40) and out-of-range (t >= 86, NaN) inputs
+// all of them.  Saturated (x > 10) and out-of-range (x <= -17, NaN) inputs
 // run the same straight line on their unclamped t -- whatever it computes is
 // replaced by the clamp constant or sent to the exact path, so no clamp sits
 // on the latency chain of the latency-bound sweeps (K-chain).
@@ -99,14 +99,19 @@ __device__ __forceinline__ float sigmoid32_fast(float x, bool& exact, TabLoad ta
     const ulonglong2 e = tab(static_cast<uint32_t>(ki & 31u));
     const double tail = __longlong_as_double(static_cast<long long>(e.x));
     const uint64_t sbits = e.y + (ki << 47);
-    double p = __fma_rn(r, 0x1.1111111111111p-7, 0x1.5555555555555p-5);
-    p = __fma_rn(r, p, 0x1.5555555555555p-3);
-    p = __fma_rn(r, p, 0.5);
-    // exp(r) - 1 = r + r^2 (1/2 + r (1/6 + r (1/24 + r/120))) + O(r^6/720),
-    // 2^-48.6 at |r| = ln2/64
-    const double tmp = __fma_rn(__dmul_rn(r, r), p, __dadd_rn(r, tail));
+    // exp(r) - 1 = r + r^2 (1/2 + r/6 + r^2 (1/24 + r/120)) + O(r^6/720),
+    // 2^-48.6 at |r| = ln2/64; the bracket by Estrin (two FMA levels where
+    // Horner chains three -- the sweeps of deep networks wait on this chain)
+    const double r2 = __dmul_rn(r, r);
+    const double q0 = __fma_rn(r, 0x1.5555555555555p-3, 0.5);
+    const double q1 = __fma_rn(r, 0x1.1111111111111p-7, 0x1.5555555555555p-5);
+    const double p = __fma_rn(r2, q1, q0);
+    const double tmp = __fma_rn(r2, p, __dadd_rn(r, tail));
     const double scale = __longlong_as_double(static_cast<long long>(sbits));
-    const double d = __dadd_rn(1.0, __fma_rn(scale, tmp, scale));
+    // 1 + scale (1 + tmp) as scale tmp + (1 + scale): the sum 1 + scale is
+    // formed while the polynomial runs (one rounding of ~2^-53 more, inside
+    // the fast path's 2^-47 budget)
+    const double d = __fma_rn(scale, tmp, __dadd_rn(1.0, scale));
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
     // third-order refinement: e = 1 - d y; y (1 + e + e^2) has error e^3

@@ -161,6 +161,7 @@ k_serve(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
                     const uint2 info = ri[r];
                     const uint4* q = reinterpret_cast<const uint4*>(e4 + info.x);
                     float acc = 0.0f;
+#pragma unroll 4
                     for (uint32_t bt = 0; bt < info.y; ++bt) {
                         const uint4 p0 = q[2 * bt], p1 = q[2 * bt + 1];  // 4 x {source address, weight}
                         const float v0 = chain::lds_f32(p0.x), v1 = chain::lds_f32(p0.z);

@@ -359,9 +359,9 @@ int asnn_dev_normalize(asnn_dev* dev, const asnn_network_desc* net, asnn_corpus*
 /* read_network (io.cpp:167-173): ASNN_E_IO when the file cannot be read. */
 int asnn_dev_read_network(asnn_dev* dev, const char* path, asnn_corpus** out, uint32_t* err_line);
 /* parse_weight's from_chars<float> on n tokens buf[off[i], off[i+1]) on the
- * device: status 0 = parsed, 1 = rejected, 2 / 3 = decided by the host's
- * from_chars (parsed / rejected) because the device flagged the token; the
- * parser's number kernel, exposed for parity tests. */
+ * device: status 0 = parsed, 1 = rejected (every token is decided on the
+ * device, the exact slow path included); the parser's number kernel, exposed
+ * for parity tests. */
 int asnn_dev_parse_weights(asnn_dev* dev, const char* buf, const uint64_t* off, uint64_t n, float* out,
                            uint8_t* status);
 

@@ -20,8 +20,8 @@
 //      declarations, input/output overlap, inputs with incoming connections,
 //      and a Kahn pass for cycles (the cycle's text, only needed for the error
 //      message, is recovered by the reference's DFS order on the host).
-// The host formats messages from the failing line's own text, and resolves
-// the rare weight tokens parse_tok.cuh marks kTokHost with std::from_chars.
+// The host formats messages from the failing line's own text; every weight
+// token is decided on the device (parse_tok.cuh, exact slow path included).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -75,7 +75,7 @@ enum : uint8_t {
     ERR_DUP,           // duplicate edge a->b
     ERR_BAD_ID,        // bad node id '<tok>' on the inputs / outputs line (token index in aux)
 };
-enum : uint8_t { ES_OK = 0, ES_NTOK, ES_SRC, ES_TGT, ES_W, ES_SELF, ES_HOST };
+enum : uint8_t { ES_OK = 0, ES_NTOK, ES_SRC, ES_TGT, ES_W, ES_SELF };
 
 __device__ __forceinline__ bool tok_eq(const char* p, uint32_t n, const char* lit, uint32_t ln) {
     if (n != ln) return false;
@@ -158,9 +158,8 @@ __global__ void k_parse_lines(const char* __restrict__ t, const uint64_t* __rest
                 es = ES_TGT;
             } else {
                 const uint8_t r = parse_f32(t + s + ts[3], t + s + ts[3] + tl[3], w);
-                if (r == kTokErr) es = ES_W;
-                else if (r == kTokHost) es = ES_HOST;  // the host decides weight, then self-loop
-                else if (a == b) es = ES_SELF;         // checked after the weight, as the reference does
+                if (r != kTokOk) es = ES_W;
+                else if (a == b) es = ES_SELF;  // checked after the weight, as the reference does
             }
         } else {
             kind = K_OTHER;
@@ -209,7 +208,7 @@ __global__ void k_line_errors(const uint8_t* __restrict__ kind, const uint8_t* _
             case ES_TGT: err = ERR_BAD_TGT; break;
             case ES_W: err = ERR_BAD_W; break;
             case ES_SELF: err = ERR_SELF; break;
-            default: keep[i] = 1; break;  // ES_OK, ES_HOST
+            default: keep[i] = 1; break;  // ES_OK
         }
     }
     if (err != ERR_NONE) atomicMin(first_err, (static_cast<unsigned long long>(i) << 8) | err);
@@ -219,7 +218,7 @@ __global__ void k_compact_edges(const uint32_t* __restrict__ keep, const uint32_
                                 const uint32_t* __restrict__ src, const uint32_t* __restrict__ tgt,
                                 const float* __restrict__ w, const uint8_t* __restrict__ estat,
                                 uint32_t* __restrict__ es, uint32_t* __restrict__ et, float* __restrict__ ew,
-                                uint32_t* __restrict__ eline, uint32_t* __restrict__ host_flag) {
+                                uint32_t* __restrict__ eline) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || !keep[i]) return;
     const uint32_t j = idx[i];
@@ -227,7 +226,6 @@ __global__ void k_compact_edges(const uint32_t* __restrict__ keep, const uint32_
     et[j] = tgt[i];
     ew[j] = w[i];
     eline[j] = i;
-    host_flag[j] = estat[i] == ES_HOST;
 }
 
 // Sorted by (source, target) with stable order: the later of two equal
@@ -428,49 +426,75 @@ std::string parse_message(uint8_t code, std::string_view line, uint32_t aux) {
     }
 }
 
-// find_cycle (network.cpp:107-149) on host copies -- only for the message of a
-// network the device already found cyclic.
-std::string cycle_message(const std::vector<uint32_t>& nodes, const std::vector<uint32_t>& src,
-                          const std::vector<uint32_t>& dst) {
-    const size_t n = nodes.size();
-    auto index = [&](uint32_t id) {
-        return static_cast<uint32_t>(std::lower_bound(nodes.begin(), nodes.end(), id) - nodes.begin());
-    };
-    std::vector<std::vector<uint32_t>> succ(n);
-    for (size_t k = 0; k < src.size(); ++k) succ[index(src[k])].push_back(index(dst[k]));
-    std::vector<uint8_t> color(n, 0);
-    for (size_t root = 0; root < n; ++root) {
+// find_cycle (network.cpp:107-149) on the device, for the message of a
+// network the device already found cyclic: the reference's iterative DFS,
+// roots in index order, successors in connection order, run by one thread
+// over a stable successor CSR (error path only).  path[0] = length, then the
+// cycle's node ids (first == last).
+__global__ void k_edge_index(const uint32_t* __restrict__ nodes, uint32_t N, const uint32_t* __restrict__ ids,
+                             uint64_t n, uint32_t* __restrict__ idx) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    uint32_t lo = 0, hi = N;  // lower_bound (network.cpp:57-61)
+    const uint32_t v = ids[k];
+    while (lo < hi) {
+        const uint32_t m = (lo + hi) / 2;
+        if (nodes[m] < v) lo = m + 1;
+        else hi = m;
+    }
+    idx[k] = lo;
+}
+__global__ void k_count_src(const uint32_t* __restrict__ si, uint64_t n, uint32_t* __restrict__ cnt) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k < n) atomicAdd(&cnt[si[k]], 1u);
+}
+__global__ void k_find_cycle(const uint32_t* __restrict__ nodes, uint32_t N, const uint32_t* __restrict__ off,
+                             const uint32_t* __restrict__ succ, uint8_t* __restrict__ color,
+                             uint32_t* __restrict__ st_node, uint32_t* __restrict__ st_pos,
+                             uint32_t* __restrict__ path) {
+    if (threadIdx.x || blockIdx.x) return;
+    path[0] = 0;
+    for (uint32_t root = 0; root < N; ++root) {
         if (color[root]) continue;
-        std::vector<std::pair<uint32_t, size_t>> stack;
-        stack.emplace_back(static_cast<uint32_t>(root), 0);
+        uint32_t top = 0;
+        st_node[0] = root;
+        st_pos[0] = off[root];
         color[root] = 1;
-        while (!stack.empty()) {
-            auto& [node, pos] = stack.back();
-            if (pos < succ[node].size()) {
-                const uint32_t next = succ[node][pos++];
-                if (color[next] == 1) {
-                    std::vector<uint32_t> path{nodes[next]};
-                    for (auto it = stack.rbegin(); it != stack.rend(); ++it) {
-                        path.push_back(nodes[it->first]);
-                        if (it->first == next) break;
+        while (true) {
+            const uint32_t node = st_node[top];
+            if (st_pos[top] < off[node + 1]) {
+                const uint32_t next = succ[st_pos[top]++];
+                if (color[next] == 1) {  // walk the stack back to `next`
+                    uint32_t len = 0, t = top;
+                    path[1 + len++] = nodes[next];
+                    while (true) {
+                        path[1 + len++] = nodes[st_node[t]];
+                        if (st_node[t] == next || t == 0) break;
+                        --t;
                     }
-                    std::reverse(path.begin(), path.end());
-                    path.push_back(nodes[next]);
-                    std::string msg = "cycle:";
-                    for (size_t i = 0; i < path.size(); ++i) msg += (i ? "->" : " ") + std::to_string(path[i]);
-                    return msg;
+                    // reverse path[2 .. len] into the reference's order, then close it
+                    for (uint32_t i = 1, j = len; i < j; ++i, --j) {
+                        const uint32_t x = path[i];
+                        path[i] = path[j];
+                        path[j] = x;
+                    }
+                    path[1 + len++] = nodes[next];
+                    path[0] = len;
+                    return;
                 }
                 if (color[next] == 0) {
                     color[next] = 1;
-                    stack.emplace_back(next, 0);
+                    ++top;
+                    st_node[top] = next;
+                    st_pos[top] = off[next];
                 }
             } else {
                 color[node] = 2;
-                stack.pop_back();
+                if (top == 0) break;
+                --top;
             }
         }
     }
-    return "cycle";
 }
 
 template <typename T>
@@ -634,13 +658,44 @@ int validate_device(asnn_dev* dev, const uint32_t* nodes, uint32_t N, const uint
     k_scatter_flagged<<<nb(E), kT, 0, st>>>(dst, valid.p, vidx.p, E, cd.p);
     bool cyclic = false;
     RCP(device_cycle_check(dev, nodes, N, cs.p, cd.p, nv, &cyclic));
-    if (cyclic) {  // the reference's DFS names the cycle (host copies, error path only)
-        std::vector<uint32_t> hn, h1, h2;
-        RCP(d2h(dev, hn, nodes, N));
-        RCP(d2h(dev, h1, cs.p, nv));
-        RCP(d2h(dev, h2, cd.p, nv));
+    if (cyclic) {  // the reference's DFS names the cycle (on the device, error path only)
+        DevBuf<uint32_t> si, di, cnt, off, t1, order, color_buf, stn, stp, path;
+        CKP(si.alloc(nv));
+        CKP(di.alloc(nv));
+        CKP(cnt.alloc(N + 1));
+        CKP(off.alloc(N + 1));
+        CKP(t1.alloc(1));
+        k_edge_index<<<nb(nv), kT, 0, st>>>(nodes, N, cs.p, nv, si.p);
+        k_edge_index<<<nb(nv), kT, 0, st>>>(nodes, N, cd.p, nv, di.p);
+        CKP(cudaMemsetAsync(cnt.p, 0, (N + 1) * 4ull, st));
+        k_count_src<<<nb(nv), kT, 0, st>>>(si.p, nv, cnt.p);
+        RCP(exclusive_scan(dev, cnt.p, off.p, N + 1, t1.p, st));
+        // successors grouped by source, connection order kept (stable sort)
+        SortBuffers sb;
+        uint32_t *keys_out = nullptr, *vals_out = nullptr;
+        int kb = 1;
+        while (kb < 32 && (1ull << kb) < N) ++kb;
+        RCP(radix_sort_pairs(dev, si.p, di.p, nv, kb, sb, &keys_out, &vals_out, st));
+        CKP(color_buf.alloc((N + 3) / 4));
+        CKP(cudaMemsetAsync(color_buf.p, 0, ((N + 3) / 4) * 4ull, st));
+        CKP(stn.alloc(N + 1));
+        CKP(stp.alloc(N + 1));
+        CKP(path.alloc(N + 3));
+        k_find_cycle<<<1, 32, 0, st>>>(nodes, N, off.p, vals_out, reinterpret_cast<uint8_t*>(color_buf.p), stn.p,
+                                       stp.p, path.p);
+        CKP(cudaGetLastError());
+        uint32_t len = 0;
+        CKP(cudaMemcpyAsync(&len, path.p, 4, cudaMemcpyDeviceToHost, st));
         CKP(cudaStreamSynchronize(st));
-        viol.push_back(cycle_message(hn, h1, h2));
+        std::vector<uint32_t> hp(len);
+        if (len) CKP(cudaMemcpyAsync(hp.data(), path.p + 1, len * 4ull, cudaMemcpyDeviceToHost, st));
+        CKP(cudaStreamSynchronize(st));
+        std::string msg = "cycle";
+        if (len) {
+            msg += ":";
+            for (uint32_t i = 0; i < len; ++i) msg += (i ? "->" : " ") + std::to_string(hp[i]);
+        }
+        viol.push_back(msg);
     }
     return ASNN_OK;
 }
@@ -718,15 +773,14 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, Parsed& res, uint32_
     CKP(cudaStreamSynchronize(st));
     const uint32_t n_sig = h_tot2[0];
     const uint64_t E = h_tot2[1];
-    DevBuf<uint32_t> es, et, eline, hflag;
+    DevBuf<uint32_t> es, et, eline;
     DevBuf<float> ew;
     CKP(es.alloc(E));
     CKP(et.alloc(E));
     CKP(ew.alloc(E));
     CKP(eline.alloc(E));
-    CKP(hflag.alloc(E));
     k_compact_edges<<<nb(n_lines), kT, 0, st>>>(keep.p, kidx.p, n_lines, lsrc.p, ltgt.p, lw.p, estat.p, es.p,
-                                                 et.p, ew.p, eline.p, hflag.p);
+                                                 et.p, ew.p, eline.p);
     CKP(cudaGetLastError());
     // duplicates: stable sort of edge indices by target, then by source
     if (E > 1) {
@@ -790,8 +844,7 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, Parsed& res, uint32_
     // ---- host side of the error decision
     unsigned long long h_ferr = 0;
     CKP(cudaMemcpyAsync(&h_ferr, ferr.p, 8, cudaMemcpyDeviceToHost, st));
-    std::vector<uint32_t> host_edges;
-    RCP(flagged_indices(dev, hflag.p, E, host_edges));
+    CKP(cudaStreamSynchronize(st));
     uint64_t best = h_ferr;  // (line << 8 | code), UINT64_MAX = none
     uint32_t best_aux = 0;
     for (int k = 0; k < 2; ++k)
@@ -802,33 +855,6 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, Parsed& res, uint32_
                 best_aux = static_cast<uint32_t>(h_bad_tok[k]);
             }
         }
-    std::vector<uint32_t> h_elines;
-    std::vector<std::pair<uint32_t, float>> patches;
-    if (!host_edges.empty()) {  // weights std::from_chars must decide
-        std::vector<uint32_t> all_lines;
-        RCP(d2h(dev, all_lines, eline.p, E));
-        std::vector<uint64_t> h_st(n_lines + 1);
-        CKP(cudaMemcpyAsync(h_st.data(), starts.p, (n_lines + 1) * 8ull, cudaMemcpyDeviceToHost, st));
-        CKP(cudaStreamSynchronize(st));
-        for (uint32_t j : host_edges) {
-            const uint32_t line = all_lines[j];
-            const auto tok = split_ws(line_text(text, len, h_st[line], h_st[line + 1]));
-            float v = 0.0f;
-            const auto r = std::from_chars(tok[3].data(), tok[3].data() + tok[3].size(), v);
-            uint32_t a = 0, b = 1;
-            std::from_chars(tok[1].data(), tok[1].data() + tok[1].size(), a);
-            std::from_chars(tok[2].data(), tok[2].data() + tok[2].size(), b);
-            uint8_t code = ERR_NONE;
-            if (r.ec != std::errc{} || r.ptr != tok[3].data() + tok[3].size()) code = ERR_BAD_W;
-            else if (a == b) code = ERR_SELF;
-            if (code != ERR_NONE) {
-                const uint64_t cand = (static_cast<uint64_t>(line) << 8) | code;
-                if (cand < best) best = cand;
-            } else {
-                patches.emplace_back(j, v);
-            }
-        }
-    }
     if (best == ~0ull && n_sig < 3) {  // io.cpp:149: no edges section reached
         std::string msg = "line " + std::to_string(n_lines) + ": truncated file";
         dev->err = msg;
@@ -846,7 +872,6 @@ int do_parse(asnn_dev* dev, const char* text, uint64_t len, Parsed& res, uint32_
         if (err_line) *err_line = line + 1;
         return ASNN_E_PARSE;
     }
-    for (const auto& pv : patches) CKP(cudaMemcpyAsync(ew.p + pv.first, &pv.second, 4, cudaMemcpyHostToDevice, st));
     clk.mark("errors");
     // ---- 6. make_network (network.cpp:39-55): nodes = sorted unique ids
     const uint64_t n_all = n_ids[0] + n_ids[1] + 2 * E;
@@ -1122,14 +1147,6 @@ int asnn_dev_parse_weights(asnn_dev* dev, const char* buf, const uint64_t* off, 
     CKP(cudaMemcpyAsync(out, d_out.p, n * 4, cudaMemcpyDeviceToHost, st));
     CKP(cudaMemcpyAsync(status, d_st.p, n, cudaMemcpyDeviceToHost, st));
     CKP(cudaStreamSynchronize(st));
-    for (uint64_t i = 0; i < n; ++i) {
-        if (status[i] != kTokHost) continue;
-        float v = 0.0f;
-        const auto r = std::from_chars(buf + off[i], buf + off[i + 1], v);
-        const bool ok = r.ec == std::errc{} && r.ptr == buf + off[i + 1];
-        out[i] = ok ? v : 0.0f;
-        status[i] = ok ? 2 : 3;
-    }
     return ASNN_OK;
 }
 

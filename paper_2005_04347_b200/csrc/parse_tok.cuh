@@ -13,10 +13,12 @@
 //     value with the neighbouring float midpoint in big-integer arithmetic
 //     (w * 5^q * 2^q against (2m +- 1) * 2^e, 320-bit);
 //   * tokens whose value needs more than 19 significant digits at a rounding
-//     boundary, or falls in the float subnormal range or next to the
-//     overflow threshold, are flagged kTokHost: the host resolves exactly
-//     those with std::from_chars itself (never the case for serialize_network
-//     output, whose shortest round-trip form has <= 9 digits).
+//     boundary, or falls in the float subnormal range, take the exact slow
+//     path (parse_f32_exact): the first 200 significant digits as a
+//     1152-bit integer plus a sticky bit for the rest, compared with the
+//     candidate's neighbouring midpoints -- a float midpoint has fewer than
+//     200 significant decimal digits, so the comparison is exact.  No token
+//     goes back to the host.
 // Checked against the reference's from_chars on random and adversarial
 // tokens (tests/test_gpu_parse.py).
 #pragma once
@@ -28,7 +30,7 @@ namespace parse {
 
 #include "pow_tables.inc"
 
-enum : uint8_t { kTokOk = 0, kTokErr = 1, kTokHost = 2 };
+enum : uint8_t { kTokOk = 0, kTokErr = 1 };
 
 __device__ __forceinline__ bool is_digit(char c) { return c >= '0' && c <= '9'; }
 __device__ __forceinline__ bool is_ws(char c) { return c == ' ' || c == '\t'; }
@@ -147,6 +149,146 @@ __device__ __forceinline__ bool round_exact(uint64_t w, int q, float c, bool sti
     return true;
 }
 
+// ---- exact slow path -------------------------------------------------------
+// 1152-bit unsigned integers (36 x 32-bit limbs), single thread, rare tokens.
+constexpr int kXL = 36;
+struct BigX {
+    uint32_t l[kXL];
+};
+__device__ __noinline__ void bx_set(BigX& b, uint32_t v) {
+    b.l[0] = v;
+    for (int i = 1; i < kXL; ++i) b.l[i] = 0;
+}
+// b = b * m + a (m, a < 2^32)
+__device__ __noinline__ void bx_muladd(BigX& b, uint32_t m, uint32_t a) {
+    uint64_t carry = a;
+    for (int i = 0; i < kXL; ++i) {
+        const uint64_t t = static_cast<uint64_t>(b.l[i]) * m + carry;
+        b.l[i] = static_cast<uint32_t>(t);
+        carry = t >> 32;
+    }
+}
+__device__ __noinline__ void bx_mul_pow5(BigX& b, int k) {
+    for (; k >= 13; k -= 13) bx_muladd(b, 1220703125u, 0);  // 5^13
+    uint32_t m = 1;
+    for (; k > 0; --k) m *= 5;
+    if (m != 1) bx_muladd(b, m, 0);
+}
+__device__ __noinline__ void bx_shl(BigX& b, int s) {
+    const int w = s >> 5, r = s & 31;
+    for (int i = kXL - 1; i >= 0; --i) {
+        const int j = i - w;
+        uint32_t v = j >= 0 ? b.l[j] : 0u;
+        if (r) {
+            v <<= r;
+            if (j - 1 >= 0) v |= b.l[j - 1] >> (32 - r);
+        }
+        b.l[i] = v;
+    }
+}
+__device__ __noinline__ int bx_cmp(const BigX& a, const BigX& b) {
+    for (int i = kXL - 1; i >= 0; --i)
+        if (a.l[i] != b.l[i]) return a.l[i] < b.l[i] ? -1 : 1;
+    return 0;
+}
+// sign of (D 10^q + sticky - M 2^F), D the digit integer, sticky a positive
+// amount below 10^q (truncated nonzero digits)
+__device__ __noinline__ int bx_cmp_dyadic(const BigX& D, int q, bool sticky, uint32_t M, int F) {
+    BigX L = D, R;
+    bx_set(R, M);
+    if (q >= 0) {  // D 5^q 2^q  vs  M 2^F
+        bx_mul_pow5(L, q);
+        if (q >= F) bx_shl(L, q - F);
+        else bx_shl(R, F - q);
+    } else {       // D  vs  M 5^-q 2^(F - q)
+        bx_mul_pow5(R, -q);
+        if (F - q >= 0) bx_shl(R, F - q);
+        else bx_shl(L, q - F);
+    }
+    const int c = bx_cmp(L, R);
+    return c == 0 && sticky ? 1 : c;
+}
+
+// std::from_chars<float> for the tokens the fast path cannot decide: the
+// decimal digits of [p, e) (a well-formed finite decimal, sign excluded)
+// rounded exactly, ties to even; kTokErr when the result is 0 or infinity
+// (result_out_of_range, as libstdc++ reports for parse_weight).  `approx` is
+// the fast path's double candidate (relative error < 2^-49).
+__device__ __noinline__ uint8_t parse_f32_exact(const char* p, const char* e, double approx, uint32_t sign,
+                                                float& out) {
+    constexpr int kDigits = 200;
+    BigX D;
+    bx_set(D, 0);
+    int nd = 0, q = 0;
+    bool sticky = false, point = false;
+    for (; p < e; ++p) {
+        const char ch = *p;
+        if (ch == '.') {
+            point = true;
+            continue;
+        }
+        if (!is_digit(ch)) break;
+        const uint32_t d = static_cast<uint32_t>(ch - '0');
+        if (nd == 0 && d == 0) {
+            if (point) --q;
+            continue;
+        }
+        if (nd < kDigits) {
+            bx_muladd(D, 10u, d);
+            ++nd;
+            if (point) --q;
+        } else {
+            sticky |= d != 0;
+            if (!point) ++q;
+        }
+    }
+    if (p < e && (*p | 0x20) == 'e') {
+        const char* t = p + 1;
+        bool eneg = false;
+        if (t < e && (*t == '+' || *t == '-')) {
+            eneg = *t == '-';
+            ++t;
+        }
+        int64_t x = 0;
+        for (; t < e && is_digit(*t); ++t)
+            if (x < 1000000) x = x * 10 + (*t - '0');
+        q += static_cast<int>(eneg ? -x : x);
+    }
+    // candidate: a float bit pattern within one step of the answer
+    uint32_t cb;
+    if (approx >= 0x1p-126) {
+        const float c = __double2float_rn(approx);
+        cb = __float_as_uint(c);
+        if ((cb & 0x7F800000u) == 0x7F800000u) cb = 0x7F7FFFFFu;  // FLT_MAX, decided below
+    } else {
+        cb = static_cast<uint32_t>(__double2uint_rn(__dmul_rn(approx, 0x1p149)));  // subnormal count
+    }
+    // value of a positive pattern b: m 2^E
+    auto mant = [](uint32_t b) -> uint32_t { return (b & 0x7FFFFFu) | ((b >> 23) ? 0x800000u : 0u); };
+    auto expo = [](uint32_t b) -> int { return static_cast<int>((b >> 23) ? (b >> 23) : 1u) - 150; };
+    // upper midpoint of cb: (2m + 1) 2^(E-1)
+    const uint32_t m = mant(cb);
+    const int E = expo(cb);
+    int cu = bx_cmp_dyadic(D, q, sticky, 2 * m + 1, E - 1);
+    uint32_t r = cb;
+    if (cu > 0 || (cu == 0 && (m & 1))) {
+        r = cb + 1;  // (a pattern past FLT_MAX is infinity)
+    } else if (cu < 0) {
+        // lower midpoint: below a power of two the neighbour is twice as close
+        if (cb == 0) {
+            r = 0;
+        } else {
+            const bool pow2 = (cb & 0x7FFFFFu) == 0 && (cb >> 23) > 1;
+            const int cl = pow2 ? bx_cmp_dyadic(D, q, sticky, 4 * m - 1, E - 2)
+                                : bx_cmp_dyadic(D, q, sticky, 2 * m - 1, E - 1);
+            if (cl < 0 || (cl == 0 && (m & 1))) r = cb - 1;
+        }
+    }
+    if (r == 0 || (r & 0x7F800000u) == 0x7F800000u) return kTokErr;  // rounds to 0 or infinity
+    out = __uint_as_float(r | sign);
+    return kTokOk;
+}
+
 // std::from_chars<float> (chars_format::general) over the whole token.
 __device__ __forceinline__ uint8_t parse_f32(const char* p, const char* e, float& out) {
     bool neg = false;
@@ -156,6 +298,7 @@ __device__ __forceinline__ uint8_t parse_f32(const char* p, const char* e, float
     }
     if (p == e) return kTokErr;
     const uint32_t sign = neg ? 0x80000000u : 0u;
+    const char* const digits0 = p;  // the decimal's first character (after the sign)
     const char c0 = static_cast<char>(*p | 0x20);
     if (c0 == 'i') {  // "inf" or "infinity", any case
         const char* kw = "infinity";
@@ -246,7 +389,7 @@ __device__ __forceinline__ uint8_t parse_f32(const char* p, const char* e, float
     // candidate: (double)w * 10^q, relative error < 2^-50
     const double d = __dmul_rn(static_cast<double>(w), kPow10[100 + q]);
     if (d < 0x1p-151) return kTokErr;                     // rounds to zero
-    if (d < 0x1.0000000001p-126) return kTokHost;         // float subnormals (and their edge)
+    if (d < 0x1.0000000001p-126) return parse_f32_exact(digits0, e, d, sign, out);  // subnormals (and their edge)
     float c = __double2float_rn(d);
     if ((__float_as_uint(c) & 0x7F800000u) == 0x7F800000u) {
         // candidate overflowed: the value rounds to infinity iff it reaches
@@ -256,22 +399,22 @@ __device__ __forceinline__ uint8_t parse_f32(const char* p, const char* e, float
         c = __uint_as_float(0x7F7FFFFFu);
     }
     float r;
-    if (!round_exact(w, q, c, trunc, r)) return kTokHost;
+    if (!round_exact(w, q, c, trunc, r)) return parse_f32_exact(digits0, e, d, sign, out);
     if (trunc) {  // the value lies in (w 10^q, (w+1) 10^q): both ends must agree
         float r2;
         const uint64_t w1 = w + 1;
         const double d1 = __dmul_rn(static_cast<double>(w1), kPow10[100 + q]);
         const float c1 = __double2float_rn(d1);
-        if ((__float_as_uint(c1) & 0x7F800000u) == 0x7F800000u) return kTokHost;
-        if (!round_exact(w1, q, c1, false, r2)) return kTokHost;
+        if ((__float_as_uint(c1) & 0x7F800000u) == 0x7F800000u) return parse_f32_exact(digits0, e, d, sign, out);
+        if (!round_exact(w1, q, c1, false, r2)) return parse_f32_exact(digits0, e, d, sign, out);
         // (w+1) 10^q exactly on a midpoint would round toward it from below
-        if (__float_as_uint(r2) != __float_as_uint(r)) return kTokHost;
+        if (__float_as_uint(r2) != __float_as_uint(r)) return parse_f32_exact(digits0, e, d, sign, out);
         const uint32_t rb = __float_as_uint(r2);
         const uint64_t m2 = (rb & 0x7FFFFFu) | 0x800000u;
         const int e2 = static_cast<int>(rb >> 23) - 150;
         if (cmp_decimal_dyadic(w1, q, 2 * m2 - 1, e2 - 1) == 0 ||
             cmp_decimal_dyadic(w1, q, 2 * m2 + 1, e2 - 1) == 0)
-            return kTokHost;
+            return parse_f32_exact(digits0, e, d, sign, out);
     }
     if ((__float_as_uint(r) & 0x7F800000u) == 0x7F800000u) return kTokErr;  // rounded to infinity
     out = __uint_as_float(__float_as_uint(r) | sign);

@@ -2228,8 +2228,9 @@ int asnn_dev_server_start(asnn_dev_layout* L, uint32_t max_vec, asnn_dev_server*
     if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes))) !=
         cudaSuccess)
         return bail(e, "smem attribute");
+    // batch 1: a finish half and a prefix half (serve.cuh)
     const uint32_t T = std::min<uint32_t>(
-        512, std::max<uint32_t>({64, (L->max_width * max_vec + 31) / 32 * 32,
+        512, std::max<uint32_t>({64, (max_vec == 1 ? 2 : 1) * ((L->max_width * max_vec + 31) / 32 * 32),
                                  static_cast<uint32_t>((in_n + 31) / 32 * 32)}));
     fn<<<1, T, bytes, s->st>>>(reinterpret_cast<const CtaNet*>(L->cta_nets.p), L->lo_cat.p, L->row_ptr.p,
                                L->edges.p, L->sinfo.p, L->oinfo.p, static_cast<ServeCtl*>(ctl_d),

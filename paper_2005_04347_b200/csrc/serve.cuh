@@ -44,7 +44,7 @@ __host__ __device__ inline uint32_t smem_bytes(uint32_t P, uint64_t E, uint32_t 
                  + 4ull * (P + 1) * ld                   // activations (+ zero row)
                  + 4ull * (P + 1) + 4ull * (L + 1)       // row pointers, layer offsets
                  + 4ull * (S + O) + 64;
-    if (ld == 1) b += 8 * (E + 3ull * P) + 8ull * P + 32;  // batch-1 rows: padded edges + row info
+    if (ld == 1) b += 8 * (E + 6ull * P) + 12ull * P + 32;  // batch-1 rows: padded edges, row info, partial sums
     return b > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(b);
 }
 }  // namespace serve
@@ -66,12 +66,16 @@ k_serve(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
     uint32_t* lo = rp + P + 1;                                    // [L + 1]
     uint32_t* sk = lo + L + 1;                                    // [S] input index of sensor s
     uint32_t* op = sk + S;                                        // [O] local position of output j
-    // batch-1 rows (ld == 1): each row's edges padded to a multiple of 4 with
-    // {zero row, 0.0} (appending +0.0f products leaves the sum's sigmoid32
-    // unchanged), as {shared address of the source, weight}; row info
-    // {first padded edge, batches of 4}
+    // batch-1 rows (ld == 1), split like K-chain (chain.cuh) at depth 1: the
+    // prefix (edges before the first source on layer l-1: sources final one
+    // step early) and the rest, each padded to a multiple of 4 with {zero
+    // row, 0.0} (+0.0f appended to a partial or final sum changes at most the
+    // sign of a zero, which sigmoid32 ignores), as {shared address of the
+    // source, weight}; row info {first padded edge, prefix batches | rest
+    // batches << 16}; pre[r] the parked prefix sum
     uint2* ri = reinterpret_cast<uint2*>((reinterpret_cast<uintptr_t>(op + O) + 15) & ~uintptr_t(15));
-    uint2* e4 = reinterpret_cast<uint2*>((reinterpret_cast<uintptr_t>(ri + (ld == 1 ? P : 0)) + 15) & ~uintptr_t(15));
+    float* pre = reinterpret_cast<float*>(ri + (ld == 1 ? P : 0));
+    uint2* e4 = reinterpret_cast<uint2*>((reinterpret_cast<uintptr_t>(pre + (ld == 1 ? P : 0)) + 15) & ~uintptr_t(15));
     __shared__ uint32_t sh_nvec;
     __shared__ uint32_t sh_scan[513];
     __shared__ float sh_x[512];                                   // this request's inputs
@@ -100,8 +104,24 @@ k_serve(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
         // padded offsets: thread t scans rows [t*chunk, (t+1)*chunk), then a
         // serial scan of the T partial sums
         const uint32_t chunk = (P + T - 1) / T, r0 = min(P, tid * chunk), r1 = min(P, r0 + chunk);
+        // split of row r: edges before the first source at or after lo[level(r) - 1]
+        auto split_of = [&](uint32_t r) -> uint32_t {
+            uint32_t a = 0, b = L;  // level: lo[a] <= r < lo[a + 1]
+            while (b - a > 1) {
+                const uint32_t m = (a + b) / 2;
+                if (lo[m] <= r) a = m;
+                else b = m;
+            }
+            const uint32_t thr = a >= 1 ? lo[a - 1] : 0u;
+            uint32_t k = rp[r];
+            while (k < rp[r + 1] && ed[k].x < thr) ++k;
+            return k - rp[r];
+        };
         uint32_t sum = 0;
-        for (uint32_t r = r0; r < r1; ++r) sum += ((rp[r + 1] - rp[r]) + 3) & ~3u;
+        for (uint32_t r = r0; r < r1; ++r) {
+            const uint32_t sp = split_of(r), deg = rp[r + 1] - rp[r];
+            sum += ((sp + 3) & ~3u) + ((deg - sp + 3) & ~3u);
+        }
         sh_scan[tid] = sum;
         __syncthreads();
         if (tid == 0) {
@@ -115,11 +135,16 @@ k_serve(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
         __syncthreads();
         uint32_t at = sh_scan[tid];
         for (uint32_t r = r0; r < r1; ++r) {
-            const uint32_t k0 = rp[r], deg = rp[r + 1] - k0, pad = (deg + 3) & ~3u;
-            ri[r] = make_uint2(at, pad / 4);
-            for (uint32_t j = 0; j < pad; ++j)
-                e4[at + j] = j < deg ? make_uint2(as_sh + 4 * ed[k0 + j].x, ed[k0 + j].y) : make_uint2(as_sh + 4 * P, 0u);
-            at += pad;
+            const uint32_t k0 = rp[r], deg = rp[r + 1] - k0, sp = split_of(r);
+            const uint32_t pp = (sp + 3) & ~3u, fp = (deg - sp + 3) & ~3u;
+            ri[r] = make_uint2(at, pp / 4 | (fp / 4) << 16);
+            pre[r] = 0.0f;
+            for (uint32_t j = 0; j < pp; ++j)
+                e4[at + j] = j < sp ? make_uint2(as_sh + 4 * ed[k0 + j].x, ed[k0 + j].y) : make_uint2(as_sh + 4 * P, 0u);
+            for (uint32_t j = 0; j < fp; ++j)
+                e4[at + pp + j] = sp + j < deg ? make_uint2(as_sh + 4 * ed[k0 + sp + j].x, ed[k0 + sp + j].y)
+                                               : make_uint2(as_sh + 4 * P, 0u);
+            at += pp + fp;
         }
         __syncthreads();
     }
@@ -155,23 +180,36 @@ k_serve(const CtaNet* __restrict__ nets, const uint32_t* __restrict__ lo_cat, co
         __syncthreads();
         const long long c1 = clock64();
         if (ld == 1) {
-            for (uint32_t l = 1; l < L; ++l) {
-                const uint32_t a = lo[l], b = lo[l + 1];
-                for (uint32_t r = a + tid; r < b; r += T) {
-                    const uint2 info = ri[r];
-                    const uint4* q = reinterpret_cast<const uint4*>(e4 + info.x);
-                    float acc = 0.0f;
+            // step l: the first half of the threads finishes layer l from its
+            // parked prefix sums, the second half sums layer l+1's prefixes
+            // (sources final since step l-1); one barrier per step
+            const uint32_t Th = T / 2;
+            auto run = [&](float acc, const uint4* q, uint32_t nb) -> float {
 #pragma unroll 4
-                    for (uint32_t bt = 0; bt < info.y; ++bt) {
-                        const uint4 p0 = q[2 * bt], p1 = q[2 * bt + 1];  // 4 x {source address, weight}
-                        const float v0 = chain::lds_f32(p0.x), v1 = chain::lds_f32(p0.z);
-                        const float v2 = chain::lds_f32(p1.x), v3 = chain::lds_f32(p1.z);
-                        acc = mac(acc, __uint_as_float(p0.y), v0);
-                        acc = mac(acc, __uint_as_float(p0.w), v1);
-                        acc = mac(acc, __uint_as_float(p1.y), v2);
-                        acc = mac(acc, __uint_as_float(p1.w), v3);
+                for (uint32_t bt = 0; bt < nb; ++bt) {
+                    const uint4 p0 = q[2 * bt], p1 = q[2 * bt + 1];  // 4 x {source address, weight}
+                    const float v0 = chain::lds_f32(p0.x), v1 = chain::lds_f32(p0.z);
+                    const float v2 = chain::lds_f32(p1.x), v3 = chain::lds_f32(p1.z);
+                    acc = mac(acc, __uint_as_float(p0.y), v0);
+                    acc = mac(acc, __uint_as_float(p0.w), v1);
+                    acc = mac(acc, __uint_as_float(p1.y), v2);
+                    acc = mac(acc, __uint_as_float(p1.w), v3);
+                }
+                return acc;
+            };
+            for (uint32_t l = 1; l < L; ++l) {
+                if (tid < Th) {
+                    for (uint32_t r = lo[l] + tid; r < lo[l + 1]; r += Th) {
+                        const uint2 info = ri[r];
+                        const uint4* q = reinterpret_cast<const uint4*>(e4 + info.x) + 2 * (info.y & 0xFFFFu);
+                        const float acc = run(pre[r], q, info.y >> 16);
+                        chain::sts_f32(as_sh + 4 * r, sigmoid32(acc, tab));
                     }
-                    chain::sts_f32(as_sh + 4 * r, sigmoid32(acc, tab));
+                } else if (l + 1 < L) {
+                    for (uint32_t r = lo[l + 1] + tid - Th; r < lo[l + 2]; r += Th) {
+                        const uint2 info = ri[r];
+                        pre[r] = run(0.0f, reinterpret_cast<const uint4*>(e4 + info.x), info.y & 0xFFFFu);
+                    }
                 }
                 __syncthreads();
             }

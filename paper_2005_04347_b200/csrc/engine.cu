@@ -951,6 +951,14 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
 // position -- a stable radix sort of all positions by (level, ~degree);
 // level-0 sensors sort first and are skipped.  Plus the heavy-row counts
 // per level for every threshold heavy_thr(t).
+bool level_win_enabled() {
+    static const bool on = [] {
+        const char* s = getenv("ASNN_LEVEL_WIN");
+        return s && s[0] == '1';
+    }();
+    return on;
+}
+
 int ensure_schedule(asnn_dev_layout* L) {
     if (L->sched_ready) return ASNN_OK;
     asnn_dev* dev = L->dev;
@@ -985,6 +993,23 @@ int ensure_schedule(asnn_dev_layout* L) {
     CK(cudaGetLastError());
     L->heavy_cnt.assign(nh, 0);
     CK(cudaMemcpyAsync(L->heavy_cnt.data(), hv.p, nh * 4, cudaMemcpyDeviceToHost, st));
+    // per-level source windows (k_rows_win), one network
+    DevBuf<uint32_t> d_lvl, wmin, wmax;
+    L->win_lo.assign(n_levels, 0xFFFFFFFFu);
+    L->win_hi.assign(n_levels, 0);
+    if (level_win_enabled() && G == 1 && P > S && n_levels) {
+        CK(d_lvl.alloc(n_levels + 1));
+        CK(wmin.alloc(n_levels));
+        CK(wmax.alloc(n_levels));
+        CK(cudaMemcpyAsync(d_lvl.p, L->lvl_off.data(), (n_levels + 1) * 4ull, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(wmin.p, 0xFF, n_levels * 4ull, st));
+        CK(cudaMemsetAsync(wmax.p, 0, n_levels * 4ull, st));
+        k_level_windows<<<blocks_for(P - S), kThreads, 0, st>>>(L->rtask.p, d_lvl.p, n_levels, P - S, L->edges.p,
+                                                                 wmin.p, wmax.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(L->win_lo.data(), wmin.p, n_levels * 4ull, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(L->win_hi.data(), wmax.p, n_levels * 4ull, cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaStreamSynchronize(st));
     L->sched_ready = true;
     return ASNN_OK;
@@ -1185,6 +1210,22 @@ int launch_sweep(asnn_dev_layout* L, const float* x, uint32_t n_vec, float* out,
 }
 
 // Per-layer launches (k_level, plus k_heavy on the aux branch for heavy rows).
+// k_rows_win (win_rows.cuh): a level of whole rows whose sources all lie in
+// a window of positions small enough for shared memory (two blocks per SM),
+// for batches of 128+ columns.  Opt-in (ASNN_LEVEL_WIN=1): on config 2 it
+// measured 2.10 ms per sweep against k_rows' 1.93 (profiles/r2_c2_rows_win.txt).
+uint32_t rows_win_bytes(const asnn_dev_layout* L, uint32_t l) {
+    if (l >= L->win_lo.size() || L->win_lo[l] > L->win_hi[l]) return 0;
+    const uint64_t cap = (static_cast<uint64_t>(L->max_deg) + 1) & ~1ull;
+    const uint64_t b = static_cast<uint64_t>(L->win_hi[l] - L->win_lo[l] + 1) * winrows::kTile * 4u +
+                       winrows::kRowsPerBlock * cap * 8u;
+    return b > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(b);
+}
+bool rows_win_ok(const asnn_dev_layout* L, uint32_t l, uint32_t ldA) {
+    const uint32_t b = rows_win_bytes(L, l);
+    return level_win_enabled() && ldA >= 128 && ldA % winrows::kTile == 0 && b && b <= 110u * 1024;
+}
+
 // k_rows_tma (tma_rows.cuh): the TMA-gather level kernel for ldA a multiple
 // of 128; ASNN_LEVEL_VARIANT=13 selects it (experiments).
 bool tma_rows_enabled(uint32_t ldA) { return level_variant() == 13 && ldA >= 128 && ldA % 128 == 0; }
@@ -1275,7 +1316,28 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
                 ll.warp_rows4<<<blocks_for(static_cast<uint64_t>(nrows + ns) * 32), kThreads, 0, st>>>(
                     L->edges.p, L->A.p, ldA, L->rtask.p + L->lvl_off[l] + nh, nrows,
                     segs ? L->seg.p + L->seg_short_off[l] : nullptr, ns, L->accbuf.p);
-            else if (ll.rows && tma_rows_enabled(ldA)) {
+            else if (ll.rows && !nh && !ns && !nlong && rows_win_ok(L, l, ldA)) {
+                const uint32_t bytes = rows_win_bytes(L, l);
+                static bool attr_set = false;
+                if (!attr_set) {
+                    CK(cudaFuncSetAttribute(k_rows_win, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+                    attr_set = true;
+                }
+                cudaLaunchConfig_t cfg{};
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.gridDim = dim3((ldA / winrows::kTile) *
+                                   ((nrows + winrows::kRowsPerBlock - 1) / winrows::kRowsPerBlock));
+                cfg.blockDim = dim3(winrows::kThreads);
+                cfg.dynamicSmemBytes = bytes;
+                cfg.stream = st;
+                cfg.attrs = attr;
+                cfg.numAttrs = pdl_enabled() && !fork && !prev_join && l > 1 ? 1 : 0;
+                CK(cudaLaunchKernelEx(&cfg, k_rows_win, static_cast<const uint2*>(L->edges.p), L->A.p, ldA,
+                                      static_cast<const uint4*>(L->rtask.p + L->lvl_off[l]), nrows, L->win_lo[l],
+                                      L->win_hi[l] - L->win_lo[l] + 1, (L->max_deg + 1) & ~1u));
+            } else if (ll.rows && tma_rows_enabled(ldA)) {
                 RC_(ensure_tmap_A(L, ldA));
                 static bool attr_set = false;
                 if (!attr_set) {

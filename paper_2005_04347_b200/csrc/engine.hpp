@@ -215,6 +215,7 @@ struct asnn_dev_layout {
     uint32_t max_width = 0, max_deg = 0;
     uint64_t total_edges = 0, dropped = 0;
     std::vector<uint32_t> lvl_off;  // sched offsets per global level, [n_levels + 1]
+    std::vector<uint32_t> win_lo, win_hi;  // per level: source position window (win_rows.cuh)
     std::vector<uint32_t> heavy_cnt;  // [kNumHeavyThr][n_levels + 1] rows above heavy_thr(t)
 
     asnn_b200::DevBuf<uint32_t> row_ptr;    // [total_pos + 1]

@@ -17,7 +17,6 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
-#include <unordered_set>
 #include <vector>
 
 #include "asnn_dev.h"
@@ -94,9 +93,61 @@ std::vector<std::uint32_t> powerlaw_band_starts(uint32_t n_nodes, uint32_t bands
 
 namespace {
 
-inline std::uint64_t pair_key(std::uint32_t s, std::uint32_t t) {
-    return (static_cast<std::uint64_t>(s) << 32) | t;
-}
+// Open-addressing set / map of non-zero 64-bit keys (linear probing, power-of-
+// two capacity, never shrinks): the generator's only dynamic structures, sized
+// by the connection count rather than by the forward-pair space.
+struct KeyTable {
+    std::vector<std::uint64_t> key;
+    std::vector<std::uint64_t> val;
+    std::uint64_t mask = 0;
+    explicit KeyTable(std::uint64_t n, bool with_values) {
+        std::uint64_t cap = 16;
+        while (cap < 2 * n + 2) cap <<= 1;
+        key.assign(cap, 0);
+        if (with_values) val.assign(cap, 0);
+        mask = cap - 1;
+    }
+    static std::uint64_t mix(std::uint64_t k) {
+        k ^= k >> 33;
+        k *= 0xFF51AFD7ED558CCDull;
+        return k ^ (k >> 29);
+    }
+    // slot of k: holds k, or is the empty slot where k would go
+    std::uint64_t find(std::uint64_t k) const {
+        std::uint64_t i = mix(k) & mask;
+        while (key[i] != 0 && key[i] != k) i = (i + 1) & mask;
+        return i;
+    }
+    bool insert(std::uint64_t k) {  // false when already present
+        const std::uint64_t i = find(k);
+        if (key[i] == k) return false;
+        key[i] = k;
+        return true;
+    }
+};
+
+// The forward-pair space of a banded network, by arithmetic on the bands:
+// every target of band b >= 1 has the same source range [0, start(b)), so the
+// space is piecewise regular -- pair index -> (source, target) is a search over
+// the bands (<= depth entries) and a division, with no per-node table.
+struct PairSpace {
+    const std::vector<std::uint32_t>& starts;
+    std::vector<std::uint64_t> off;  // off[b]: first pair index of band b (b >= 1)
+    std::uint32_t drop;              // sources removed per target (0, or 1 = the mandatory one)
+    PairSpace(const std::vector<std::uint32_t>& st, std::uint32_t d) : starts(st), off(st.size(), 0), drop(d) {
+        for (std::size_t b = 1; b + 1 < st.size(); ++b)
+            off[b + 1] = off[b] + static_cast<std::uint64_t>(st[b + 1] - st[b]) * (st[b] - drop);
+    }
+    std::uint64_t size() const { return off[starts.size() - 1]; }
+    // index -> target node and source rank within the target's range
+    void locate(std::uint64_t idx, std::uint32_t& node, std::uint32_t& rank) const {
+        std::size_t b = 1;
+        while (b + 2 < starts.size() && off[b + 1] <= idx) ++b;
+        const std::uint64_t w = starts[b] - drop, r = idx - off[b];
+        node = starts[b] + static_cast<std::uint32_t>(r / w);
+        rank = static_cast<std::uint32_t>(r % w);
+    }
+};
 
 }  // namespace
 
@@ -106,16 +157,27 @@ uint64_t asnn_gen_max_connections(uint32_t in, uint32_t out, uint32_t hidden, ui
     return capacity_of(band_starts(in, out, hidden, depth));
 }
 
-// Restates generate() (netgen.cpp:71-157): band layout, one mandatory
-// predecessor from the adjacent band, then uniform unused forward pairs
-// (dense: shuffled prefix of the free pairs; sparse: rejection sampling),
-// finally sorted by (source, target).  The draw order of the SplitMix64
-// stream is the reference's, so networks are byte-identical.
+// Same networks as generate() (netgen.cpp:71-157), byte for byte: the
+// SplitMix64 stream is consumed in the reference's order -- per non-input
+// node ascending a mandatory source in the adjacent band and its weight, then
+// the remaining connections as uniform unused forward pairs, then everything
+// sorted by (source, target).
+//
+// The pair selection is reorganised so memory follows the connection count,
+// not the pair space (config-scale specs have pair spaces of 10^11+):
+//  * sparse requests (netgen.cpp:129-141): the drawn pair index is decoded by
+//    band arithmetic (PairSpace) and deduplicated in a KeyTable;
+//  * dense requests (netgen.cpp:115-128): the reference shuffles a
+//    materialised list of the free pairs (target-major, sources ascending,
+//    mandatory pairs left out) and takes its prefix.  The same draws drive a
+//    virtual Fisher-Yates here: list entries are computed from their rank
+//    (each target's free sources are its range minus its one mandatory
+//    source), and only displaced ranks are stored.
 int asnn_gen_reference(uint32_t in, uint32_t out, uint32_t hidden, uint64_t conn, uint32_t depth,
                        float wmin, float wmax, uint64_t seed, asnn_corpus** result) {
     if (!result) return ASNN_E_INVALID;
     *result = nullptr;
-    // check_feasible (netgen.cpp:29-53)
+    // feasibility (netgen.cpp:29-53)
     if (in == 0 || out == 0 || depth < 2 || (depth == 2 && hidden > 0) ||
         (depth > 2 && hidden < depth - 2) || !(wmin <= wmax))
         return ASNN_E_INFEASIBLE;
@@ -123,80 +185,71 @@ int asnn_gen_reference(uint32_t in, uint32_t out, uint32_t hidden, uint64_t conn
     if (conn < static_cast<std::uint64_t>(hidden) + out || conn > capacity_of(starts))
         return ASNN_E_INFEASIBLE;
 
-    auto* c = new asnn_corpus;
-    const std::uint32_t node_count = starts.back();
-    const std::uint32_t first = in;
+    const std::uint32_t n_nodes = starts.back();
     SplitMix64 rng(seed);
-    auto band_of = [&starts](std::uint32_t id) {
-        return static_cast<std::uint32_t>(std::upper_bound(starts.begin(), starts.end(), id) -
-                                          starts.begin()) - 1;
+    struct Edge {
+        std::uint64_t key;  // source << 32 | target (unique)
+        float w;
     };
-    std::vector<std::uint64_t> keys;  // (src << 32 | dst), weight kept alongside
-    std::vector<float> weights;
-    keys.reserve(conn);
-    weights.reserve(conn);
-    std::unordered_set<std::uint64_t> used;
-    used.reserve(conn * 2);
+    std::vector<Edge> edges;
+    edges.reserve(conn);
+    auto key_of = [](std::uint32_t s, std::uint32_t t) { return (static_cast<std::uint64_t>(s) << 32) | t; };
 
-    // netgen.cpp:95-102 -- mandatory predecessor from the adjacent band.
-    for (std::uint32_t node = first; node < node_count; ++node) {
-        const std::uint32_t band = band_of(node);
-        const std::uint32_t lo = starts[band - 1], hi = starts[band];
-        const std::uint32_t pred = lo + static_cast<std::uint32_t>(rng.bounded(hi - lo));
-        used.insert(pair_key(pred, node));
-        keys.push_back(pair_key(pred, node));
-        weights.push_back(rng.uniform(wmin, wmax));
-    }
-    // netgen.cpp:104-113 -- cumulative forward-pair space per target.
-    const std::uint64_t remaining = conn - keys.size();
-    std::vector<std::uint64_t> cumulative(node_count - first + 1, 0);
-    for (std::uint32_t node = first; node < node_count; ++node)
-        cumulative[node - first + 1] = cumulative[node - first] + starts[band_of(node)];
-    const std::uint64_t pair_space = cumulative.back();
+    // mandatory sources, band by band (= node order)
+    std::vector<std::uint32_t> mand(n_nodes, 0);
+    for (std::size_t b = 1; b + 1 < starts.size(); ++b)
+        for (std::uint32_t v = starts[b]; v < starts[b + 1]; ++v) {
+            mand[v] = starts[b - 1] + static_cast<std::uint32_t>(rng.bounded(starts[b] - starts[b - 1]));
+            const float w = rng.uniform(wmin, wmax);
+            edges.push_back({key_of(mand[v], v), w});
+        }
+    const std::uint64_t n_mand = edges.size();
+    const std::uint64_t remaining = conn - n_mand;
+    const PairSpace all(starts, 0);
 
-    if (remaining * 2 > pair_space - keys.size()) {
-        // netgen.cpp:115-128 -- dense: shuffle a prefix of the free pairs.
-        std::vector<std::uint64_t> free_pairs;
-        free_pairs.reserve(pair_space - keys.size());
-        for (std::uint32_t node = first; node < node_count; ++node)
-            for (std::uint32_t pred = 0; pred < starts[band_of(node)]; ++pred)
-                if (!used.count(pair_key(pred, node))) free_pairs.push_back(pair_key(pred, node));
+    if (remaining * 2 > all.size() - n_mand) {
+        const PairSpace free_space(starts, 1);  // one mandatory source per target left out
+        KeyTable moved(remaining, true);        // rank position -> displaced rank (+1)
         for (std::uint64_t k = 0; k < remaining; ++k) {
-            const std::uint64_t j = k + rng.bounded(free_pairs.size() - k);
-            std::swap(free_pairs[k], free_pairs[j]);
-            keys.push_back(free_pairs[k]);
-            weights.push_back(rng.uniform(wmin, wmax));
+            const std::uint64_t j = k + rng.bounded(free_space.size() - k);
+            auto at = [&moved](std::uint64_t pos) {
+                const std::uint64_t i = moved.find(pos + 1);
+                return moved.key[i] ? moved.val[i] - 1 : pos;
+            };
+            const std::uint64_t pick = at(j);
+            const std::uint64_t i = moved.find(j + 1);
+            moved.key[i] = j + 1;
+            moved.val[i] = at(k) + 1;  // position k is never read again
+            std::uint32_t v, r;
+            free_space.locate(pick, v, r);
+            const float w = rng.uniform(wmin, wmax);
+            edges.push_back({key_of(r < mand[v] ? r : r + 1, v), w});
         }
     } else {
-        // netgen.cpp:129-141 -- sparse: rejection-sample the pair space.
-        for (std::uint64_t k = 0; k < remaining;) {
-            const std::uint64_t idx = rng.bounded(pair_space);
-            const auto it = std::upper_bound(cumulative.begin(), cumulative.end(), idx);
-            const std::uint32_t slot = static_cast<std::uint32_t>(it - cumulative.begin()) - 1;
-            const std::uint32_t node = first + slot;
-            const std::uint32_t pred = static_cast<std::uint32_t>(idx - cumulative[slot]);
-            if (!used.insert(pair_key(pred, node)).second) continue;
-            keys.push_back(pair_key(pred, node));
-            weights.push_back(rng.uniform(wmin, wmax));
-            ++k;
+        KeyTable used(conn, false);
+        for (std::uint64_t e = 0; e < n_mand; ++e) used.insert(edges[e].key);
+        while (edges.size() < conn) {
+            std::uint32_t v, s;
+            all.locate(rng.bounded(all.size()), v, s);
+            if (!used.insert(key_of(s, v))) continue;  // a duplicate consumes no weight draw
+            const float w = rng.uniform(wmin, wmax);
+            edges.push_back({key_of(s, v), w});
         }
     }
-    // netgen.cpp:143-145 -- sort by (source, target); keys are unique.
-    std::vector<std::uint32_t> order(keys.size());
-    for (std::uint32_t i = 0; i < order.size(); ++i) order[i] = i;
-    std::sort(order.begin(), order.end(),
-              [&keys](std::uint32_t a, std::uint32_t b) { return keys[a] < keys[b]; });
-    c->src.resize(keys.size());
-    c->dst.resize(keys.size());
-    c->w.resize(keys.size());
-    for (std::size_t i = 0; i < order.size(); ++i) {
-        c->src[i] = static_cast<std::uint32_t>(keys[order[i]] >> 32);
-        c->dst[i] = static_cast<std::uint32_t>(keys[order[i]] & 0xFFFFFFFFu);
-        c->w[i] = weights[order[i]];
+    std::sort(edges.begin(), edges.end(), [](const Edge& x, const Edge& y) { return x.key < y.key; });
+
+    auto* c = new asnn_corpus;
+    c->src.resize(edges.size());
+    c->dst.resize(edges.size());
+    c->w.resize(edges.size());
+    for (std::size_t i = 0; i < edges.size(); ++i) {
+        c->src[i] = static_cast<std::uint32_t>(edges[i].key >> 32);
+        c->dst[i] = static_cast<std::uint32_t>(edges[i].key);
+        c->w[i] = edges[i].w;
     }
-    // netgen.cpp:147-156 -- dense ids, inputs = band 0, outputs = last band.
-    c->nodes.resize(node_count);
-    for (std::uint32_t i = 0; i < node_count; ++i) c->nodes[i] = i;
+    // dense ids; inputs = band 0, outputs = the last band (netgen.cpp:147-156)
+    c->nodes.resize(n_nodes);
+    for (std::uint32_t i = 0; i < n_nodes; ++i) c->nodes[i] = i;
     c->inputs.resize(in);
     for (std::uint32_t i = 0; i < in; ++i) c->inputs[i] = i;
     c->outputs.resize(out);

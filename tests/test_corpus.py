@@ -86,3 +86,29 @@ def test_powerlaw_shape(oracle):
     deg = np.bincount(net.target, minlength=20000)[64:]
     assert deg.max() > 10 * np.median(deg)          # heavy tail
     assert digest(net) == digest(A.generate_powerlaw(20000, 10, 64, 32, 400000, 2.1, 5))
+
+
+@pytest.mark.parametrize("shape", [
+    (3, 2, 12, 1.0, 4),      # full capacity: the dense branch takes every free pair
+    (3, 2, 12, 0.8, 4),      # dense (more than half the free pairs)
+    (1, 1, 6, 0.9, 5),       # one input: band 1 has no free source besides its mandatory one
+    (5, 3, 0, 1.0, 2),       # depth 2, no hidden band
+    (5, 3, 0, 0.6, 2),
+    (2, 2, 40, 0.55, 8),
+    (8, 4, 200, 0.3, 6),     # sparse, rejection with duplicates
+])
+def test_generate_dense_and_edge_specs_match_reference(ref, shape):
+    """The dense branch (netgen.cpp:115-128, a shuffled prefix of the free
+    pairs) and the sparse one (:129-141) near their switch-over and at the
+    capacity limit, against the reference's own generate."""
+    i, o, h, frac, d = shape
+    cap = A.max_connections(A.GenSpec(i, o, h, 0, d))
+    lo = h + o
+    for seed in range(6):
+        conn = max(lo, int(lo + (cap - lo) * frac))
+        spec = A.GenSpec(i, o, h, conn, d, -2.0, 2.0, 1000 + seed)
+        a = ref.generate(spec).arrays()
+        net = A.generate(spec)
+        for k in ("nodes", "inputs", "outputs", "source", "target"):
+            assert np.array_equal(a[k], getattr(net, k)), (shape, seed, k)
+        assert np.array_equal(a["weight"].view(np.uint32), net.weight.view(np.uint32))

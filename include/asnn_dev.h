@@ -185,6 +185,51 @@ int asnn_dev_layout_download(asnn_dev_layout* layout, uint32_t net_index, uint32
                              uint32_t* node_ids, uint64_t* row_ptr, uint32_t* in_nodes,
                              float* in_weights, uint32_t* input_order);
 
+/* ---- one-call eval_parallel (the per-call drop-in, once.cu) ----------------
+ * Replaces eval_parallel(layout, inputs, cfg) with Backend::DeviceCompute
+ * (/root/reference/proj/src/eval.cpp:49-80, seam at :51-52) when the layout
+ * exists for one call only (the reference passes a host LayeredLayout to
+ * every call and may mutate it in between, asnn_main.cpp:264-278).  Nothing
+ * is renumbered or kept: the state stays id-indexed as in the reference.
+ *
+ *   asnn_eval_buf_stage  -- page-locked arrays sized from dims; the caller
+ *                           writes the layout's CSR straight into them
+ *                           (layout.hpp:13-37: ids, row_ptr, predecessor ids
+ *                           in stored order, weights) and, per layer-0 node,
+ *                           inputs[id] of make_state (eval.cpp:25-35)
+ *   asnn_eval_buf_run    -- one kernel (plus one DMA for larger layouts);
+ *                           writes state.outputs [id_bound] (unassigned ids
+ *                           0.0f).  ASNN_E_INVALID for malformed layouts
+ *                           (layer table, row_ptr or ids out of range).
+ * One buffer per calling thread; runs on one handle serialise. */
+typedef struct asnn_eval_buf asnn_eval_buf;
+typedef struct asnn_eval_dims {
+    uint32_t total_layers;
+    uint32_t node_count;
+    uint32_t sensor_count;  /* layer 0 = nodes_per_layer[0] */
+    uint32_t id_bound;
+    uint64_t edge_count;    /* < 2^32 */
+} asnn_eval_dims;
+typedef struct asnn_eval_stage {
+    uint32_t* layer_offsets; /* [total_layers + 1] */
+    uint32_t* node_ids;      /* [node_count] */
+    uint32_t* row_ptr;       /* [node_count + 1], 32-bit */
+    uint32_t* in_nodes;      /* [edge_count] */
+    float* in_weights;       /* [edge_count] */
+    float* sensor_inputs;    /* [sensor_count] inputs[node_ids[k]] */
+} asnn_eval_stage;
+int asnn_eval_buf_create(asnn_dev* dev, asnn_eval_buf** out);
+void asnn_eval_buf_free(asnn_eval_buf* buf);
+int asnn_eval_buf_stage(asnn_eval_buf* buf, const asnn_eval_dims* dims, asnn_eval_stage* stage);
+int asnn_eval_buf_run(asnn_eval_buf* buf, float* state_outputs);
+/* kernel variant of the last run: 0 zero-copy into shared memory, 1 DMA +
+ * one CTA, 2 DMA + cooperative grid (ASNN_ONCE_MODE=1|2 forces one) */
+int asnn_eval_buf_mode(const asnn_eval_buf* buf, uint32_t* mode);
+/* The same from a layout descriptor and one input vector (make_state on the
+ * host; ASNN_E_ARITY when n_x != n_inputs, eval.cpp:26-28). */
+int asnn_dev_eval_layout(asnn_dev* dev, const asnn_layout_desc* layout, const float* x, uint64_t n_x,
+                         float* state_outputs);
+
 /* ---- activation -----------------------------------------------------------
  * eval_parallel(DeviceCompute) over a batch: x is [n_vec][n_inputs] per
  * network (networks concatenated), `out` (optional) receives the declared

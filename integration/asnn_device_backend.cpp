@@ -5,8 +5,8 @@
 // engine.  It is compiled against the reference's own headers; the only
 // change to the reference itself is the two-line branch at eval.cpp:51-52
 // shown in INTEGRATION.md.  It converts the reference's LayeredLayout
-// (layout.hpp:27-37) to the C-ABI's asnn_layout_desc, uploads it on every
-// call (the reference mutates layouts in place between evaluations,
+// (layout.hpp:27-37) into the C-ABI's page-locked staging (asnn_eval_buf,
+// once.cu) on every call (the reference mutates layouts in place between evaluations,
 // asnn_main.cpp:264-278), activates one vector and maps status codes back to
 // the reference's exception types (errors.hpp:9-55).
 //
@@ -61,46 +61,56 @@ ActivationState eval_device(const LayeredLayout& layout, std::span<const float> 
         throw InputArityMismatch("expected " + std::to_string(layout.input_order.size()) +
                                  " input values, got " + std::to_string(input_values.size()));
     asnn_dev* dev = device();
-
-    // LayeredLayout -> CSR (layout.hpp:13-37)
-    std::vector<std::uint32_t> ids(layout.nodes.size());
-    std::vector<std::uint64_t> row_ptr(layout.nodes.size() + 1, 0);
-    std::size_t edges = 0;
-    for (const FlatNode& n : layout.nodes) edges += n.in_nodes.size();
-    std::vector<std::uint32_t> in_nodes;
-    std::vector<float> in_weights;
-    in_nodes.reserve(edges);
-    in_weights.reserve(edges);
-    for (std::size_t k = 0; k < layout.nodes.size(); ++k) {
-        const FlatNode& n = layout.nodes[k];
-        ids[k] = n.id;
-        in_nodes.insert(in_nodes.end(), n.in_nodes.begin(), n.in_nodes.end());
-        in_weights.insert(in_weights.end(), n.in_weights.begin(), n.in_weights.end());
-        row_ptr[k + 1] = in_nodes.size();
+    // one page-locked staging buffer per calling thread (once.cu): the
+    // LayeredLayout's AoS nodes are written straight into it, no copy between
+    struct Buf {
+        asnn_eval_buf* b = nullptr;
+        ~Buf() { asnn_eval_buf_free(b); }
+    };
+    thread_local Buf buf;
+    if (!buf.b) {
+        const int rc = asnn_eval_buf_create(dev, &buf.b);
+        if (rc) raise(rc, dev);
     }
-    asnn_layout_desc d{};
-    d.total_layers = layout.total_layers;
-    d.layer_offsets = layout.layer_offsets.data();
-    d.node_count = static_cast<std::uint32_t>(layout.nodes.size());
-    d.node_ids = ids.data();
-    d.row_ptr = row_ptr.data();
-    d.in_nodes = in_nodes.data();
-    d.in_weights = in_weights.data();
-    d.n_inputs = static_cast<std::uint32_t>(layout.input_order.size());
-    d.input_order = layout.input_order.data();
-    d.id_bound = layout.id_bound;
-
-    asnn_dev_layout* dl = nullptr;
-    int rc = asnn_dev_upload_layout(dev, &d, &dl);
-    if (rc) raise(rc, dev);
+    const std::size_t N = layout.nodes.size();
+    // make_state (eval.cpp:29-33)
     ActivationState state;
-    state.inputs.assign(layout.id_bound, 0.0f);  // make_state, eval.cpp:29-33
+    state.inputs.assign(layout.id_bound, 0.0f);
     for (std::size_t i = 0; i < input_values.size(); ++i)
         state.inputs[layout.input_order[i]] = input_values[i];
-    state.outputs.assign(layout.id_bound, 0.0f);
-    rc = asnn_dev_activate(dl, input_values.data(), 1, input_values.size(), nullptr,
-                           state.outputs.data());
-    asnn_dev_free_layout(dl);
+    asnn_eval_dims dims{};
+    dims.total_layers = layout.total_layers;
+    dims.node_count = static_cast<std::uint32_t>(N);
+    dims.sensor_count = layout.total_layers ? layout.nodes_per_layer[0] : 0;
+    dims.id_bound = layout.id_bound;
+    std::uint64_t edges = 0;
+    for (const FlatNode& n : layout.nodes) edges += n.in_nodes.size();
+    dims.edge_count = edges;
+    asnn_eval_stage s{};
+    int rc = asnn_eval_buf_stage(buf.b, &dims, &s);
+    if (rc) raise(rc, dev);
+    // LayeredLayout -> CSR (layout.hpp:13-37)
+    std::copy(layout.layer_offsets.begin(), layout.layer_offsets.end(), s.layer_offsets);
+    std::uint32_t at = 0;
+    for (std::size_t k = 0; k < N; ++k) {
+        s.row_ptr[k] = at;
+        at += static_cast<std::uint32_t>(layout.nodes[k].in_nodes.size());
+    }
+    s.row_ptr[N] = at;
+    const std::int64_t n64 = static_cast<std::int64_t>(N);
+#pragma omp parallel for schedule(static) if (edges > (1u << 18))
+    for (std::int64_t k = 0; k < n64; ++k) {
+        const FlatNode& n = layout.nodes[k];
+        s.node_ids[k] = n.id;
+        std::copy(n.in_nodes.begin(), n.in_nodes.end(), s.in_nodes + s.row_ptr[k]);
+        std::copy(n.in_weights.begin(), n.in_weights.end(), s.in_weights + s.row_ptr[k]);
+    }
+    for (std::uint32_t k = 0; k < dims.sensor_count; ++k) {
+        const NodeId id = layout.nodes[k].id;
+        s.sensor_inputs[k] = id < layout.id_bound ? state.inputs[id] : 0.0f;
+    }
+    state.outputs.resize(layout.id_bound);
+    rc = asnn_eval_buf_run(buf.b, state.outputs.data());
     if (rc) raise(rc, dev);
     return state;
 }

@@ -11,7 +11,7 @@ from .api import (  # noqa: F401
     InfeasibleSpec, InputArityMismatch, IoError, LayerAssignment, LayeredLayout, LayerOutOfRange,
     Network, OutputUnreachable, ParallelConfig, ParseError, RequiredSet, SplitMix64, UnassignedOutput,
     ValidationError, compute_required, normalize, parse_network, read_network, validate,
-    corpus_spec, depth, device_count, eval_parallel, eval_parallel_batch, flatten, generate,
+    corpus_spec, depth, device_count, eval_once, EvalBuffer, eval_parallel, eval_parallel_batch, flatten, generate,
     generate_mlp, generate_powerlaw, layer_slice_bounds, make_network, max_connections,
     max_layer_width, random_spec, read_outputs, segment, unassigned_outputs,
 )

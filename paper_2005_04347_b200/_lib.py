@@ -54,6 +54,21 @@ class LayoutDesc(C.Structure):
     ]
 
 
+class EvalDims(C.Structure):
+    _fields_ = [
+        ("total_layers", C.c_uint32), ("node_count", C.c_uint32),
+        ("sensor_count", C.c_uint32), ("id_bound", C.c_uint32),
+        ("edge_count", C.c_uint64),
+    ]
+
+
+class EvalStage(C.Structure):
+    _fields_ = [
+        ("layer_offsets", u32p), ("node_ids", u32p), ("row_ptr", u32p),
+        ("in_nodes", u32p), ("in_weights", f32p), ("sensor_inputs", f32p),
+    ]
+
+
 class LayoutInfo(C.Structure):
     _fields_ = [
         ("n_networks", C.c_uint32), ("total_layers", C.c_uint32),
@@ -94,6 +109,12 @@ PROTOTYPES = {
     "asnn_dev_network_info": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(LayoutInfo)]),
     "asnn_dev_layout_download": (C.c_int, [C.c_void_p, C.c_uint32, u32p, u32p, u64p, u32p, f32p, u32p]),
     "asnn_dev_activate": (C.c_int, [C.c_void_p, f32p, C.c_uint32, C.c_uint64, f32p, f32p]),
+    "asnn_eval_buf_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "asnn_eval_buf_free": (None, [C.c_void_p]),
+    "asnn_eval_buf_stage": (C.c_int, [C.c_void_p, C.POINTER(EvalDims), C.POINTER(EvalStage)]),
+    "asnn_eval_buf_run": (C.c_int, [C.c_void_p, f32p]),
+    "asnn_eval_buf_mode": (C.c_int, [C.c_void_p, u32p]),
+    "asnn_dev_eval_layout": (C.c_int, [C.c_void_p, C.POINTER(LayoutDesc), f32p, C.c_uint64, f32p]),
     "asnn_dev_activate_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p]),
     "asnn_dev_server_start": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "asnn_dev_server_activate": (C.c_int, [C.c_void_p, f32p, C.c_uint32, C.c_uint64, f32p]),

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 import threading
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
@@ -302,6 +303,7 @@ class Device:
             raise BackendUnavailable(f"no CUDA device {index} for the device-compute backend")
         self.h = h
         self.index = index
+        self.sweep_mode = int(os.environ.get("ASNN_SWEEP_MODE", "0") or 0) % 5
 
     @classmethod
     def get(cls, index: int = 0) -> "Device":
@@ -325,6 +327,7 @@ class Device:
         where eligible), 2 one CTA per (network, slice), 3 one launch per level
         with whole rows only."""
         self.check(self.lib.asnn_dev_set_sweep_mode(self.h, int(mode)))
+        self.sweep_mode = int(mode)
 
     def set_heavy_threshold(self, min_in_degree: Optional[int]):
         """Rows above this in-degree use the streamed heavy kernel (None = off)."""
@@ -788,8 +791,86 @@ def eval_parallel(layout: LayeredLayout, input_values, cfg: ParallelConfig = Par
     x = _f32(input_values)
     if len(x) != len(layout.input_order):
         raise InputArityMismatch(f"expected {len(layout.input_order)} input values, got {len(x)}")
-    states = eval_parallel_batch(layout, x[None, :], cfg)
-    return states[0]
+    if Device.get(cfg.device).sweep_mode:
+        # an explicitly chosen sweep strategy runs on an uploaded layout
+        return eval_parallel_batch(layout, x[None, :], cfg)[0]
+    inputs = np.zeros(layout.id_bound, np.float32)
+    inputs[layout.input_order] = x   # make_state, eval.cpp:32-33 (last duplicate wins)
+    return ActivationState(inputs, eval_once(layout, x, cfg.device))
+
+
+def eval_once(layout: LayeredLayout, x, device: int = 0) -> np.ndarray:
+    """One eval_parallel call on a layout that exists for this call only
+    (asnn_dev_eval_layout, once.cu): returns state.outputs [id_bound]."""
+    dev = Device.get(device)
+    x = _f32(x)
+    out = np.empty(layout.id_bound, np.float32)
+    d = layout.desc()
+    dev.check(dev.lib.asnn_dev_eval_layout(dev.h, C.byref(d), _lib.ptr(x, C.c_float), len(x),
+                                           _lib.ptr(out, C.c_float)))
+    return out
+
+
+class EvalBuffer:
+    """asnn_eval_buf: page-locked staging the caller writes a layout into, then
+    one device call (once.cu).  `stage` returns numpy views of the staged arrays."""
+
+    def __init__(self, device: int = 0):
+        self.dev = Device.get(device)
+        self.h = C.c_void_p()
+        self.dev.check(self.dev.lib.asnn_eval_buf_create(self.dev.h, C.byref(self.h)))
+
+    def stage(self, total_layers: int, node_count: int, sensor_count: int, id_bound: int,
+              edge_count: int) -> dict:
+        d = _lib.EvalDims(total_layers, node_count, sensor_count, id_bound, edge_count)
+        st = _lib.EvalStage()
+        self.dev.check(self.dev.lib.asnn_eval_buf_stage(self.h, C.byref(d), C.byref(st)))
+        self.id_bound = id_bound
+
+        def view(p, n, t):
+            return np.ctypeslib.as_array(p, shape=(max(n, 1),))[:n].view(t) if n else np.zeros(0, t)
+        return {"layer_offsets": view(st.layer_offsets, total_layers + 1, np.uint32),
+                "node_ids": view(st.node_ids, node_count, np.uint32),
+                "row_ptr": view(st.row_ptr, node_count + 1, np.uint32),
+                "in_nodes": view(st.in_nodes, edge_count, np.uint32),
+                "in_weights": view(st.in_weights, edge_count, np.float32),
+                "sensor_inputs": view(st.sensor_inputs, sensor_count, np.float32)}
+
+    def stage_layout(self, layout: LayeredLayout, x) -> None:
+        x = _f32(x)
+        n = len(layout.node_ids)
+        ns = int(layout.layer_offsets[1]) if layout.total_layers else 0
+        a = self.stage(layout.total_layers, n, ns, layout.id_bound, int(layout.row_ptr[-1]) if n else 0)
+        a["layer_offsets"][:] = layout.layer_offsets
+        a["node_ids"][:] = layout.node_ids
+        a["row_ptr"][:] = layout.row_ptr
+        a["in_nodes"][:] = layout.in_nodes
+        a["in_weights"][:] = layout.in_weights
+        inputs = np.zeros(layout.id_bound, np.float32)
+        inputs[layout.input_order] = x
+        a["sensor_inputs"][:] = inputs[layout.node_ids[:ns]]
+
+    def run(self) -> np.ndarray:
+        out = np.empty(self.id_bound, np.float32)
+        self.dev.check(self.dev.lib.asnn_eval_buf_run(self.h, _lib.ptr(out, C.c_float)))
+        return out
+
+    @property
+    def mode(self) -> int:
+        m = C.c_uint32(0)
+        self.dev.check(self.dev.lib.asnn_eval_buf_mode(self.h, C.byref(m)))
+        return m.value
+
+    def free(self):
+        if self.h:
+            self.dev.lib.asnn_eval_buf_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def eval_parallel_batch(layout: LayeredLayout, X, cfg: ParallelConfig = ParallelConfig(

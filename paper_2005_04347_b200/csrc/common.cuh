@@ -137,7 +137,7 @@ __device__ __forceinline__ float sigmoid32_path(float x, bool& exact) {
 // latency-bound one-column sweeps (config 3: 2.82 -> 2.70 ms) run a tighter
 // loop without its inlined body; column groups (V = 4) keep it inline
 // (config 5 measured 4% slower out of line, profiles/r1_light_variants.txt).
-__device__ __noinline__ float sigmoid32_exact_call(float x) { return sigmoid32_exact(x); }
+static __device__ __noinline__ float sigmoid32_exact_call(float x) { return sigmoid32_exact(x); }
 
 template <class TabLoad = ExpTabGlobal>
 __device__ __forceinline__ float sigmoid32(float x, TabLoad tab = TabLoad()) {

@@ -1770,6 +1770,7 @@ void asnn_dev_close(asnn_dev* dev) {
     if (!dev) return;
     cudaSetDevice(dev->device);
     cudaStreamSynchronize(dev->stream);
+    asnn_eval_buf_free(dev->once);
     release_comm(dev);
     for (cudaEvent_t ev : {dev->ev0, dev->ev1, dev->ev2, dev->ev3, dev->ev4, dev->stage_ev[0], dev->stage_ev[1]})
         if (ev) cudaEventDestroy(ev);

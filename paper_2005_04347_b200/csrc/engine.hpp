@@ -143,6 +143,7 @@ struct asnn_dev {
     // multi-process job (asnn_dev_comm_init) or a member of an asnn_group
     void* comm = nullptr;
     int comm_rank = 0, comm_size = 1;
+    asnn_eval_buf* once = nullptr;  // asnn_dev_eval_layout's staging (once.cu)
 };
 
 namespace asnn_b200 {

@@ -1,0 +1,438 @@
+// once.cu -- eval_parallel of a layout that lives for ONE call (the per-call
+// drop-in, eval.cpp:49-80 behind the seam at :51-52).
+//
+// The reference hands every eval_parallel call a host LayeredLayout and the
+// caller may mutate it between calls (asnn_main.cpp:264-278), so nothing can
+// be kept on the device across calls.  The resident path (engine.cu:
+// upload_layout -> renumbering, schedules, CUDA graphs) pays ~200 us of fixed
+// cost for structures that only amortise over many sweeps; this path keeps
+// the reference's own id-indexed state and runs the whole call as
+//
+//   caller writes the CSR straight into page-locked staging (asnn_eval_buf_stage)
+//   -> [small]  one kernel: one CTA pulls the staged layout over PCIe into
+//               shared memory (zero-copy, every load in flight at once) and
+//               sweeps the layers there, __syncthreads between layers
+//   -> [medium] one DMA, then one CTA with the state in shared memory
+//   -> [large]  one DMA, then one cooperative grid with the state in L2,
+//               grid.sync() between layers
+//   -> state.outputs written by the kernel into mapped host memory.
+//
+// Arithmetic is activate_node (eval.cpp:16-23): the stored predecessor order,
+// __fmul_rn / __fadd_rn (no contraction), sigmoid32 bit for bit; sensors
+// (layer 0) take sigmoid32(inputs[id]) where the caller did make_state
+// (eval.cpp:25-35) and staged inputs[id] per sensor.  Malformed layouts
+// (ids or predecessors >= id_bound, row_ptr out of order) are flagged by the
+// kernel without any out-of-bounds access and reported as ASNN_E_INVALID.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "engine.hpp"
+
+using namespace asnn_b200;
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr uint32_t kSmemCap = 227 * 1024;
+
+// Byte offsets of the staged arrays inside the blob (16-byte aligned).
+struct OnceOff {
+    uint32_t lo, ids, rp, src, w, sx, bytes;
+};
+
+struct OnceArgs {
+    const uint8_t* blob;  // staged layout: mapped host (mode 0) or device copy
+    OnceOff off;
+    float* op;            // [idb] state in global memory (mode 2)
+    float* out;           // [idb] state.outputs, mapped host memory
+    uint32_t* err;        // mapped host flag
+    uint32_t L, N, idb, ns;
+    uint32_t E;
+};
+
+__device__ __forceinline__ uint32_t ld_u32(const uint32_t* p, bool global_ro) {
+    return global_ro ? __ldg(p) : *p;
+}
+
+// kMode 0: blob in mapped host memory, copied into shared memory by the CTA
+//          (followed by the state); everything after the copy is on-chip.
+// kMode 1: blob in device memory (one DMA); state in shared memory.
+// kMode 2: blob in device memory; state in global memory (L2), grid-wide.
+template <int kMode>
+__global__ void __launch_bounds__(1024) k_once(const OnceArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t nthr = gridDim.x * blockDim.x;
+    const uint32_t op_bytes = (a.idb * 4 + 15) & ~15u;
+    float* op = kMode == 2 ? a.op : reinterpret_cast<float*>(smem);
+    const uint8_t* base = a.blob;
+    if constexpr (kMode == 0) {
+        // zero-copy pull of the staged layout: independent 16-byte loads
+        const uint4* s = reinterpret_cast<const uint4*>(a.blob);
+        uint4* d = reinterpret_cast<uint4*>(smem + op_bytes);
+        for (uint32_t i = threadIdx.x; i < a.off.bytes / 16; i += blockDim.x) d[i] = s[i];
+        base = smem + op_bytes;
+    }
+    constexpr bool ro = kMode != 0;
+    const uint32_t* lo = reinterpret_cast<const uint32_t*>(base + a.off.lo);
+    const uint32_t* ids = reinterpret_cast<const uint32_t*>(base + a.off.ids);
+    const uint32_t* rp = reinterpret_cast<const uint32_t*>(base + a.off.rp);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(base + a.off.src);
+    const float* w = reinterpret_cast<const float*>(base + a.off.w);
+    const float* sx = reinterpret_cast<const float*>(base + a.off.sx);
+
+    auto sync = [] {
+        if constexpr (kMode == 2) cg::this_grid().sync();
+        else __syncthreads();
+    };
+    // the state read another CTA wrote: L2 only (L1 is not coherent)
+    auto rd = [&](uint32_t u) -> float {
+        if constexpr (kMode == 2) return __ldcg(op + u);
+        else return op[u];
+    };
+
+    for (uint32_t i = tid; i < a.idb; i += nthr) op[i] = 0.0f;  // make_state: outputs zero
+    sync();
+    uint32_t bad = 0;
+    // layer 0: sensors, sigmoid32(inputs[id]) (eval.cpp:17)
+    for (uint32_t i = tid; i < a.ns; i += nthr) {
+        const uint32_t id = ld_u32(ids + i, ro);
+        const float v = sigmoid32(ro ? __ldg(sx + i) : sx[i]);
+        if (id < a.idb) op[id] = v;
+        else bad = 1;
+    }
+    for (uint32_t l = 1; l < a.L; ++l) {
+        sync();
+        const uint32_t b = ld_u32(lo + l, ro), e = ld_u32(lo + l + 1, ro);
+        for (uint32_t i = b + tid; i < e; i += nthr) {
+            const uint32_t id = ld_u32(ids + i, ro);
+            uint32_t k = ld_u32(rp + i, ro);
+            uint32_t ke = ld_u32(rp + i + 1, ro);
+            if (ke < k || ke > a.E) {
+                bad = 1;
+                ke = k;
+            }
+            float s = 0.0f;
+            // predecessors in the stored order; four loads ahead of the chain
+            for (; k + 4 <= ke; k += 4) {
+                uint32_t u[4];
+                float wv[4], v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    u[j] = ld_u32(src + k + j, ro);
+                    wv[j] = ro ? __ldg(w + k + j) : w[k + j];
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    bad |= u[j] >= a.idb;
+                    v[j] = u[j] < a.idb ? rd(u[j]) : 0.0f;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) s = __fadd_rn(s, __fmul_rn(wv[j], v[j]));
+            }
+            for (; k < ke; ++k) {
+                const uint32_t u = ld_u32(src + k, ro);
+                const float wk = ro ? __ldg(w + k) : w[k];
+                bad |= u >= a.idb;
+                s = __fadd_rn(s, __fmul_rn(wk, u < a.idb ? rd(u) : 0.0f));
+            }
+            const float y = sigmoid32(s);
+            if (id < a.idb) op[id] = y;
+            else bad = 1;
+        }
+    }
+    sync();
+    for (uint32_t i = tid; i < a.idb; i += nthr) a.out[i] = kMode == 2 ? __ldcg(op + i) : op[i];
+    if (bad) *reinterpret_cast<volatile uint32_t*>(a.err) = 1u;
+}
+
+uint32_t align16(uint64_t b) { return static_cast<uint32_t>((b + 15) & ~15ull); }
+
+}  // namespace
+
+struct asnn_eval_buf {
+    asnn_dev* dev = nullptr;
+    asnn_eval_dims dims{};
+    OnceOff off{};
+    bool staged = false;
+    PinnedBuf blob;            // page-locked (mapped) staging of the layout
+    uint8_t* dblob = nullptr;  // device copy (modes 1, 2)
+    size_t dblob_bytes = 0;
+    float* op = nullptr;       // global state (mode 2)
+    size_t op_n = 0;
+    float* out_h = nullptr;    // mapped state.outputs
+    size_t out_n = 0;
+    uint32_t* err_h = nullptr;
+    uint32_t last_mode = 0;
+    ~asnn_eval_buf() {
+        if (dblob) cudaFree(dblob);
+        if (op) cudaFree(op);
+        if (out_h) cudaFreeHost(out_h);
+        if (err_h) cudaFreeHost(err_h);
+    }
+};
+
+#define CK(expr)                                                 \
+    do {                                                         \
+        cudaError_t _e = (expr);                                 \
+        if (_e != cudaSuccess) return cuda_fail(dev, _e, #expr); \
+    } while (0)
+
+extern "C" {
+
+int asnn_eval_buf_create(asnn_dev* dev, asnn_eval_buf** out) {
+    if (!dev || !out) return ASNN_E_INVALID;
+    *out = nullptr;
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    CK(cudaSetDevice(dev->device));
+    auto* b = new asnn_eval_buf;
+    b->dev = dev;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&b->err_h), 16, cudaHostAllocMapped);
+    if (e != cudaSuccess) {
+        b->err_h = nullptr;
+        delete b;
+        return cuda_fail(dev, e, "eval buffer flag");
+    }
+    *b->err_h = 0;
+    *out = b;
+    return ASNN_OK;
+}
+
+void asnn_eval_buf_free(asnn_eval_buf* b) {
+    if (!b) return;
+    std::lock_guard<std::recursive_mutex> lk(b->dev->mu);
+    cudaSetDevice(b->dev->device);
+    cudaStreamSynchronize(b->dev->stream);
+    delete b;
+}
+
+int asnn_eval_buf_stage(asnn_eval_buf* b, const asnn_eval_dims* d, asnn_eval_stage* s) {
+    if (!b || !d || !s) return ASNN_E_INVALID;
+    asnn_dev* dev = b->dev;
+    b->staged = false;
+    if (d->edge_count >= 0xFFFFFFFFull) return fail(dev, ASNN_E_INVALID, "more than 2^32-1 edges");
+    if (d->sensor_count > d->node_count) return fail(dev, ASNN_E_INVALID, "sensor_count > node_count");
+    if (d->total_layers == 0 && d->node_count) return fail(dev, ASNN_E_INVALID, "layers missing");
+    OnceOff o{};
+    uint64_t at = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint32_t r = static_cast<uint32_t>(at);
+        at += align16(bytes);
+        return r;
+    };
+    o.lo = take(4ull * (d->total_layers + 1));
+    o.ids = take(4ull * d->node_count);
+    o.rp = take(4ull * (d->node_count + 1));
+    o.sx = take(4ull * d->sensor_count);
+    o.src = take(4ull * d->edge_count);
+    o.w = take(4ull * d->edge_count);
+    if (at >= (1ull << 32)) return fail(dev, ASNN_E_INVALID, "layout too large for one call");
+    o.bytes = static_cast<uint32_t>(at);
+    {
+        // page-locked staging is mapped for the zero-copy kernel (UVA)
+        cudaSetDevice(dev->device);
+        cudaError_t e = b->blob.ensure(std::max<uint64_t>(at, 64));
+        if (e != cudaSuccess) return cuda_fail(dev, e, "eval staging");
+    }
+    uint8_t* p = static_cast<uint8_t*>(b->blob.p);
+    s->layer_offsets = reinterpret_cast<uint32_t*>(p + o.lo);
+    s->node_ids = reinterpret_cast<uint32_t*>(p + o.ids);
+    s->row_ptr = reinterpret_cast<uint32_t*>(p + o.rp);
+    s->in_nodes = reinterpret_cast<uint32_t*>(p + o.src);
+    s->in_weights = reinterpret_cast<float*>(p + o.w);
+    s->sensor_inputs = reinterpret_cast<float*>(p + o.sx);
+    b->dims = *d;
+    b->off = o;
+    b->staged = true;
+    return ASNN_OK;
+}
+
+int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
+    if (!b) return ASNN_E_INVALID;
+    asnn_dev* dev = b->dev;
+    if (!b->staged) return fail(dev, ASNN_E_INVALID, "nothing staged");
+    const asnn_eval_dims d = b->dims;
+    if (d.id_bound && !state_outputs) return fail(dev, ASNN_E_INVALID, "null state");
+    const uint8_t* hp = static_cast<const uint8_t*>(b->blob.p);
+    const uint32_t* lo = reinterpret_cast<const uint32_t*>(hp + b->off.lo);
+    const uint32_t* rp = reinterpret_cast<const uint32_t*>(hp + b->off.rp);
+    // layer table on the host (L + 1 reads): the kernel indexes with it
+    uint32_t max_w = 0;
+    if (d.total_layers) {
+        if (lo[0] != 0) return fail(dev, ASNN_E_INVALID, "layer_offsets[0] != 0");
+        for (uint32_t l = 0; l < d.total_layers; ++l) {
+            if (lo[l + 1] < lo[l]) return fail(dev, ASNN_E_INVALID, "layer_offsets decrease");
+            max_w = std::max(max_w, lo[l + 1] - lo[l]);
+        }
+        if (lo[d.total_layers] != d.node_count)
+            return fail(dev, ASNN_E_INVALID, "layer_offsets do not cover node_count");
+        if (lo[1] != d.sensor_count) return fail(dev, ASNN_E_INVALID, "layer 0 size != sensor_count");
+    }
+    if (d.node_count && (rp[0] != 0 || rp[d.node_count] != d.edge_count))
+        return fail(dev, ASNN_E_INVALID, "row_ptr does not span the edges");
+
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    CK(cudaSetDevice(dev->device));
+    cudaStream_t st = dev->stream;
+    const uint32_t idb = d.id_bound;
+    if (idb == 0) return ASNN_OK;
+    if (b->out_n < idb) {
+        if (b->out_h) cudaFreeHost(b->out_h);
+        b->out_h = nullptr;
+        b->out_n = 0;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&b->out_h), 4ull * idb, cudaHostAllocMapped));
+        b->out_n = idb;
+    }
+    // write the state straight into the caller's buffer when it is page-locked
+    float* out_dev = nullptr;
+    {
+        cudaPointerAttributes pa;
+        if (cudaPointerGetAttributes(&pa, state_outputs) == cudaSuccess && pa.type == cudaMemoryTypeHost)
+            out_dev = static_cast<float*>(pa.devicePointer);
+        cudaGetLastError();
+    }
+    const bool direct = out_dev != nullptr;
+    if (!direct) CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&out_dev), b->out_h, 0));
+    uint32_t* err_dev = nullptr;
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&err_dev), b->err_h, 0));
+    *reinterpret_cast<volatile uint32_t*>(b->err_h) = 0;
+
+    const uint32_t op_bytes = align16(4ull * idb);
+    const uint32_t blob = b->off.bytes;
+    // mode: 0 = zero-copy into shared, 1 = DMA + shared state, 2 = DMA + grid
+    uint32_t mode;
+    if (op_bytes + static_cast<uint64_t>(blob) <= kSmemCap - 1024 && blob <= (96u << 10)) mode = 0;
+    else if (op_bytes <= kSmemCap - 1024 && d.edge_count <= (192u << 10)) mode = 1;
+    else mode = 2;
+    if (const char* m = getenv("ASNN_ONCE_MODE")) {
+        const int f = atoi(m);
+        if (f == 1 && op_bytes <= kSmemCap - 1024) mode = 1;
+        if (f == 2) mode = 2;
+    }
+    b->last_mode = mode;
+
+    OnceArgs a{};
+    a.off = b->off;
+    a.out = out_dev;
+    a.err = err_dev;
+    a.L = d.total_layers;
+    a.N = d.node_count;
+    a.idb = idb;
+    a.ns = d.sensor_count;
+    a.E = static_cast<uint32_t>(d.edge_count);
+    if (mode == 0) {
+        void* hb = nullptr;
+        CK(cudaHostGetDevicePointer(&hb, b->blob.p, 0));
+        a.blob = static_cast<const uint8_t*>(hb);
+    } else {
+        if (b->dblob_bytes < blob) {
+            if (b->dblob) cudaFree(b->dblob);
+            b->dblob = nullptr;
+            b->dblob_bytes = 0;
+            CK(cudaMalloc(&b->dblob, blob));
+            b->dblob_bytes = blob;
+        }
+        CK(cudaMemcpyAsync(b->dblob, b->blob.p, blob, cudaMemcpyHostToDevice, st));
+        a.blob = b->dblob;
+    }
+    if (mode == 2) {
+        if (b->op_n < idb) {
+            if (b->op) cudaFree(b->op);
+            b->op = nullptr;
+            b->op_n = 0;
+            CK(cudaMalloc(&b->op, 4ull * idb));
+            b->op_n = idb;
+        }
+        a.op = b->op;
+        constexpr int kT = 256;
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_once<2>, kT, 0));
+        if (per_sm < 1) return fail(dev, ASNN_E_CUDA, "cooperative kernel does not fit");
+        const uint32_t cap = static_cast<uint32_t>(per_sm) * static_cast<uint32_t>(dev->sm_count);
+        const uint32_t want = std::max<uint32_t>((max_w + kT - 1) / kT, (idb + 8 * kT - 1) / (8 * kT));
+        const uint32_t blocks = std::max<uint32_t>(1, std::min(cap, want));
+        void* args[] = {&a};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_once<2>), blocks, kT, args, 0, st));
+    } else {
+        const uint32_t smem = op_bytes + (mode == 0 ? blob : 0);
+        const uint32_t T = std::min<uint32_t>(1024, std::max<uint32_t>(128, (max_w + 31) / 32 * 32));
+        auto fn = mode == 0 ? k_once<0> : k_once<1>;
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        fn<<<1, T, smem, st>>>(a);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(st));
+    if (*reinterpret_cast<volatile uint32_t*>(b->err_h))
+        return fail(dev, ASNN_E_INVALID, "malformed layout: node id, predecessor id or row_ptr out of range");
+    if (!direct) std::memcpy(state_outputs, b->out_h, 4ull * idb);
+    return ASNN_OK;
+}
+
+int asnn_eval_buf_mode(const asnn_eval_buf* b, uint32_t* mode) {
+    if (!b || !mode) return ASNN_E_INVALID;
+    *mode = b->last_mode;
+    return ASNN_OK;
+}
+
+// Convenience: a layout descriptor + input vector (make_state on the host,
+// eval.cpp:25-35), staged and run through a temporary buffer.
+int asnn_dev_eval_layout(asnn_dev* dev, const asnn_layout_desc* d, const float* x, uint64_t n_x,
+                         float* state_outputs) {
+    if (!dev || !d) return ASNN_E_INVALID;
+    if (n_x != d->n_inputs)
+        return fail(dev, ASNN_E_ARITY,
+                    "expected " + std::to_string(d->n_inputs) + " input values, got " + std::to_string(n_x));
+    if (n_x && !x) return fail(dev, ASNN_E_INVALID, "null input");
+    if (d->node_count && (!d->layer_offsets || !d->node_ids || !d->row_ptr))
+        return fail(dev, ASNN_E_INVALID, "null layout array");
+    if (d->total_layers && d->layer_offsets[d->total_layers] != d->node_count)
+        return fail(dev, ASNN_E_INVALID, "layer_offsets do not cover node_count");
+    const uint64_t E = d->node_count ? d->row_ptr[d->node_count] : 0;
+    for (uint32_t i = 0; i < d->n_inputs; ++i)
+        if (d->input_order[i] >= d->id_bound) return fail(dev, ASNN_E_INVALID, "input id >= id_bound");
+    // the handle's own buffer, held under the handle's lock for the whole call
+    std::lock_guard<std::recursive_mutex> lk(dev->mu);
+    if (!dev->once) {
+        int rc0 = asnn_eval_buf_create(dev, &dev->once);
+        if (rc0) return rc0;
+    }
+    asnn_eval_buf* b = dev->once;
+    int rc = ASNN_OK;
+    asnn_eval_dims dims{};
+    dims.total_layers = d->total_layers;
+    dims.node_count = d->node_count;
+    dims.sensor_count = d->total_layers ? d->layer_offsets[1] : 0;
+    dims.id_bound = d->id_bound;
+    dims.edge_count = E;
+    asnn_eval_stage s{};
+    rc = asnn_eval_buf_stage(b, &dims, &s);
+    if (rc == ASNN_OK) {
+        if (d->total_layers) std::memcpy(s.layer_offsets, d->layer_offsets, 4ull * (d->total_layers + 1));
+        if (d->node_count) std::memcpy(s.node_ids, d->node_ids, 4ull * d->node_count);
+        for (uint64_t i = 0; i <= d->node_count && d->node_count; ++i) {
+            if (d->row_ptr[i] > E || (i && d->row_ptr[i] < d->row_ptr[i - 1]))
+                return fail(dev, ASNN_E_INVALID, "row_ptr decreases");
+            s.row_ptr[i] = static_cast<uint32_t>(d->row_ptr[i]);
+        }
+        if (E) {
+            std::memcpy(s.in_nodes, d->in_nodes, 4 * E);
+            std::memcpy(s.in_weights, d->in_weights, 4 * E);
+        }
+        // make_state: inputs[input_order[i]] = x[i], the last duplicate wins
+        std::vector<float> in(d->id_bound, 0.0f);
+        for (uint32_t i = 0; i < d->n_inputs; ++i) in[d->input_order[i]] = x[i];
+        for (uint32_t k = 0; k < dims.sensor_count; ++k) {
+            const uint32_t id = d->node_ids[k];
+            s.sensor_inputs[k] = id < d->id_bound ? in[id] : 0.0f;
+        }
+        rc = asnn_eval_buf_run(b, state_outputs);
+    }
+    return rc;
+}
+
+}  // extern "C"

@@ -13,6 +13,8 @@
 // Built here into oracle/_ref/libasnn_ref_dev.so (oracle/Makefile) so the GPU
 // tests can run the reference's own evaluators and this backend side by side.
 #include <chrono>
+#include <omp.h>
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <mutex>
@@ -52,6 +54,26 @@ asnn_dev* device() {
     return dev;
 }
 
+// Phase clock of eval_device for tools/once_probe.py (off unless enabled by
+// ref_dev_phase_clock): make_state, sizes, staging fill, device run.
+namespace {
+struct PhaseClock {
+    bool on = false;
+    double acc[4] = {0, 0, 0, 0};
+    std::chrono::steady_clock::time_point t;
+    void start() {
+        if (on) t = std::chrono::steady_clock::now();
+    }
+    void lap(int i) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        acc[i] += std::chrono::duration<double, std::micro>(n - t).count();
+        t = n;
+    }
+};
+thread_local PhaseClock phase_clock;
+}  // namespace
+
 // eval_parallel(..., Backend::DeviceCompute): same contract as eval.cpp:49-80.
 ActivationState eval_device(const LayeredLayout& layout, std::span<const float> input_values,
                             const ParallelConfig& cfg) {
@@ -73,45 +95,63 @@ ActivationState eval_device(const LayeredLayout& layout, std::span<const float> 
         if (rc) raise(rc, dev);
     }
     const std::size_t N = layout.nodes.size();
+    phase_clock.start();
     // make_state (eval.cpp:29-33)
     ActivationState state;
     state.inputs.assign(layout.id_bound, 0.0f);
     for (std::size_t i = 0; i < input_values.size(); ++i)
         state.inputs[layout.input_order[i]] = input_values[i];
+    phase_clock.lap(0);
     asnn_eval_dims dims{};
     dims.total_layers = layout.total_layers;
     dims.node_count = static_cast<std::uint32_t>(N);
     dims.sensor_count = layout.total_layers ? layout.nodes_per_layer[0] : 0;
     dims.id_bound = layout.id_bound;
-    std::uint64_t edges = 0;
-    for (const FlatNode& n : layout.nodes) edges += n.in_nodes.size();
+    // LayeredLayout -> CSR (layout.hpp:13-37).  Large layouts are converted by
+    // all host threads: per-chunk edge totals, then each chunk writes its
+    // row_ptr run and copies its nodes' predecessors.
+    const std::int64_t n64 = static_cast<std::int64_t>(N);
+    const int nt = N >= 4096 ? std::max(1, omp_get_max_threads()) : 1;
+    std::vector<std::uint64_t> part(nt + 1, 0);
+    auto chunk = [&](int i) { return n64 * i / nt; };
+#pragma omp parallel num_threads(nt) if (nt > 1)
+    {
+        const int i = nt > 1 ? omp_get_thread_num() : 0;
+        std::uint64_t e = 0;
+        for (std::int64_t k = chunk(i); k < chunk(i + 1); ++k) e += layout.nodes[k].in_nodes.size();
+        part[i + 1] = e;
+    }
+    for (int i = 0; i < nt; ++i) part[i + 1] += part[i];
+    const std::uint64_t edges = part[nt];
     dims.edge_count = edges;
     asnn_eval_stage s{};
+    phase_clock.lap(1);
     int rc = asnn_eval_buf_stage(buf.b, &dims, &s);
     if (rc) raise(rc, dev);
-    // LayeredLayout -> CSR (layout.hpp:13-37)
     std::copy(layout.layer_offsets.begin(), layout.layer_offsets.end(), s.layer_offsets);
-    std::uint32_t at = 0;
-    for (std::size_t k = 0; k < N; ++k) {
-        s.row_ptr[k] = at;
-        at += static_cast<std::uint32_t>(layout.nodes[k].in_nodes.size());
+#pragma omp parallel num_threads(nt) if (nt > 1)
+    {
+        const int i = nt > 1 ? omp_get_thread_num() : 0;
+        auto at = static_cast<std::uint32_t>(part[i]);
+        for (std::int64_t k = chunk(i); k < chunk(i + 1); ++k) {
+            const FlatNode& n = layout.nodes[k];
+            s.node_ids[k] = n.id;
+            s.row_ptr[k] = at;
+            std::copy(n.in_nodes.begin(), n.in_nodes.end(), s.in_nodes + at);
+            std::copy(n.in_weights.begin(), n.in_weights.end(), s.in_weights + at);
+            at += static_cast<std::uint32_t>(n.in_nodes.size());
+        }
     }
-    s.row_ptr[N] = at;
-    const std::int64_t n64 = static_cast<std::int64_t>(N);
-#pragma omp parallel for schedule(static) if (edges > (1u << 18))
-    for (std::int64_t k = 0; k < n64; ++k) {
-        const FlatNode& n = layout.nodes[k];
-        s.node_ids[k] = n.id;
-        std::copy(n.in_nodes.begin(), n.in_nodes.end(), s.in_nodes + s.row_ptr[k]);
-        std::copy(n.in_weights.begin(), n.in_weights.end(), s.in_weights + s.row_ptr[k]);
-    }
+    s.row_ptr[N] = static_cast<std::uint32_t>(edges);
     for (std::uint32_t k = 0; k < dims.sensor_count; ++k) {
         const NodeId id = layout.nodes[k].id;
         s.sensor_inputs[k] = id < layout.id_bound ? state.inputs[id] : 0.0f;
     }
     state.outputs.resize(layout.id_bound);
+    phase_clock.lap(2);
     rc = asnn_eval_buf_run(buf.b, state.outputs.data());
     if (rc) raise(rc, dev);
+    phase_clock.lap(3);
     return state;
 }
 
@@ -153,6 +193,13 @@ void stats_us(const std::vector<double>& s, double* mean, double* sd) {
     *sd = s.size() > 1 ? std::sqrt(q / (s.size() - 1)) : 0.0;
 }
 }  // namespace
+
+extern "C" void ref_dev_phase_clock(int on, double* acc4) {
+    if (acc4)
+        for (int i = 0; i < 4; ++i) acc4[i] = asnn::phase_clock.acc[i];
+    asnn::phase_clock = asnn::PhaseClock{};
+    asnn::phase_clock.on = on != 0;
+}
 
 extern "C" int ref_dev_eval_timed(const asnn::LayeredLayout* layout, const float* x, std::uint32_t n_x,
                                   std::uint32_t warmup, std::uint32_t reps, double* mean_us, double* sd_us) {

@@ -151,6 +151,207 @@ __global__ void __launch_bounds__(1024) k_once(const OnceArgs a) {
     if (bad) *reinterpret_cast<volatile uint32_t*>(a.err) = 1u;
 }
 
+// ---- pipelined sweep (modes 1 and 2) ---------------------------------------
+// The layers are cut into items of T consecutive nodes (one node per thread).
+// A CTA walks its items (mode 1: all of them; mode 2: chunk k of layer l goes
+// to CTA k mod G) with a five-slot ring of row_ptr / id slices and a
+// three-slot ring of edge slices in shared memory, filled by cp.async: while
+// item t is summed, item t+2's edges and item t+4's row_ptr / ids are in
+// flight (one cp.async group per item, waited one item behind), so the dependent
+// chain of an item touches shared memory only (and the state: shared in mode
+// 1, L2 in mode 2).  Items whose edges exceed a slot read them from global
+// memory instead.  The layer table sits in shared memory when it fits.
+__device__ __forceinline__ void cpa4(void* d, const void* s) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(d))),
+                 "l"(s)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+struct Item {
+    uint32_t l, k;  // layer, chunk within the layer; l >= L: none
+};
+
+constexpr uint32_t kLoSmem = 4096;  // layer-table entries kept in shared memory
+
+__host__ __device__ constexpr uint32_t pipe_ring_bytes(uint32_t T, uint32_t L) {
+    return 4 * (5 * (T + 1) + 5 * T + 2) + 4 * ((L + 1 <= kLoSmem ? L + 1 : 0) + 3) / 4 * 4;
+}
+
+template <bool kGrid>
+__global__ void __launch_bounds__(512) k_once_pipe(const OnceArgs a, uint32_t ecap, uint32_t tsh) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t T = 1u << tsh, t = threadIdx.x;  // blockDim.x == T
+    const uint32_t G = kGrid ? gridDim.x : 1u, c = kGrid ? blockIdx.x : 0u;
+    const uint32_t op_bytes = kGrid ? 0u : (a.idb * 4 + 15) & ~15u;
+    float* op = kGrid ? a.op : reinterpret_cast<float*>(smem);
+    uint32_t* rp_s = reinterpret_cast<uint32_t*>(smem + op_bytes);  // [5][T + 1]
+    uint32_t* id_s = rp_s + 5 * (T + 1);                              // [5][T]
+    uint32_t* lo_s = id_s + 5 * T + 2;                                // [L + 1] when it fits
+    const bool lo_in_smem = a.L + 1 <= kLoSmem;
+    uint32_t* es = lo_s + (lo_in_smem ? (a.L + 1 + 3) / 4 * 4 : 0);   // [3][ecap] sources
+    float* ew = reinterpret_cast<float*>(es + 3 * ecap);              // [3][ecap] weights
+    const uint32_t* lo_g = reinterpret_cast<const uint32_t*>(a.blob + a.off.lo);
+    const uint32_t* ids = reinterpret_cast<const uint32_t*>(a.blob + a.off.ids);
+    const uint32_t* rp = reinterpret_cast<const uint32_t*>(a.blob + a.off.rp);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.blob + a.off.src);
+    const float* w = reinterpret_cast<const float*>(a.blob + a.off.w);
+    const float* sx = reinterpret_cast<const float*>(a.blob + a.off.sx);
+    const uint32_t gt = c * T + t, nthr = G * T;
+    if (lo_in_smem)
+        for (uint32_t i = t; i <= a.L; i += T) lo_s[i] = __ldg(lo_g + i);
+    __syncthreads();
+    const uint32_t* lo = lo_in_smem ? lo_s : lo_g;
+
+    auto nch = [&](uint32_t l) { return (lo[l + 1] - lo[l] + T - 1) >> tsh; };
+    auto norm = [&](Item it) {
+        while (it.l < a.L && it.k >= nch(it.l)) {
+            ++it.l;
+            it.k = c;
+        }
+        return it;
+    };
+    auto next = [&](Item it) { return it.l < a.L ? norm(Item{it.l, it.k + G}) : it; };
+    auto span = [&](Item it, uint32_t& b, uint32_t& n) {
+        b = lo[it.l] + (it.k << tsh);
+        n = min(T, lo[it.l + 1] - b);
+    };
+    auto meta = [&](Item it, uint32_t slot) {
+        if (it.l >= a.L) return;
+        uint32_t b, n;
+        span(it, b, n);
+        for (uint32_t j = t; j <= n; j += T) cpa4(rp_s + slot * (T + 1) + j, rp + b + j);
+        for (uint32_t j = t; j < n; j += T) cpa4(id_s + slot * T + j, ids + b + j);
+    };
+    // edges of an item whose row_ptr slice is in `slot`; false: read globally
+    auto staged = [&](Item it, uint32_t slot, uint32_t& e0, uint32_t& m) {
+        uint32_t b, n;
+        span(it, b, n);
+        e0 = rp_s[slot * (T + 1)];
+        const uint32_t e1 = rp_s[slot * (T + 1) + n];
+        m = e1 - e0;
+        return e1 >= e0 && e1 <= a.E && e1 - e0 <= ecap;
+    };
+    auto edges = [&](Item it, uint32_t slot, uint32_t eslot) {
+        if (it.l >= a.L) return;
+        uint32_t e0, m;
+        if (!staged(it, slot, e0, m)) return;
+        for (uint32_t j = t; j < m; j += T) {
+            cpa4(es + eslot * ecap + j, src + e0 + j);
+            cpa4(ew + eslot * ecap + j, w + e0 + j);
+        }
+    };
+    auto layer_sync = [&] {
+        if constexpr (kGrid) cg::this_grid().sync();
+        else __syncthreads();
+    };
+    auto rd = [&](uint32_t u) -> float {
+        if constexpr (kGrid) return __ldcg(op + u);
+        else return op[u];
+    };
+
+    // items t .. t+4 of this CTA
+    Item i0 = norm(Item{1, c});
+    Item i1 = next(i0);
+    Item i2 = next(i1);
+    Item i3 = next(i2);
+    meta(i0, 0);
+    meta(i1, 1);
+    meta(i2, 2);
+    meta(i3, 3);
+    cpa_commit();
+    for (uint32_t i = gt; i < a.idb; i += nthr) op[i] = 0.0f;  // make_state: outputs zero
+    layer_sync();
+    uint32_t bad = 0;
+    for (uint32_t i = gt; i < a.ns; i += nthr) {  // layer 0: sensors (eval.cpp:17)
+        const uint32_t id = __ldg(ids + i);
+        const float v = sigmoid32(__ldg(sx + i));
+        if (id < a.idb) op[id] = v;
+        else bad = 1;
+    }
+    cpa_wait_all();
+    layer_sync();
+    edges(i0, 0, 0);
+    edges(i1, 1, 1);
+    cpa_commit();
+    // layers with no item of this CTA before its first one
+    if constexpr (kGrid)
+        for (uint32_t l = 1; l < min(i0.l, a.L); ++l) layer_sync();
+    cpa_wait_all();
+    __syncthreads();
+    // ring slots of item t: s0 (row_ptr / ids, of 5) and e_cur (edges, of 3)
+    for (uint32_t s0 = 0, e_cur = 0; i0.l < a.L; s0 = s0 == 4 ? 0 : s0 + 1, e_cur = e_cur == 2 ? 0 : e_cur + 1) {
+        const Item i4 = next(i3);
+        meta(i4, s0 == 0 ? 4 : s0 - 1);
+        edges(i2, s0 >= 3 ? s0 - 3 : s0 + 2, e_cur == 0 ? 2 : e_cur - 1);
+        cpa_commit();
+        {
+            uint32_t b, n, e0, m;
+            span(i0, b, n);
+            const bool st = staged(i0, s0, e0, m);
+            if (t < n) {
+                const uint32_t id = id_s[s0 * T + t];
+                uint32_t k = rp_s[s0 * (T + 1) + t], ke = rp_s[s0 * (T + 1) + t + 1];
+                if (ke < k || ke > a.E || (st && (k < e0))) {
+                    bad = 1;
+                    ke = k;
+                }
+                float sum = 0.0f;
+                if (st) {
+                    const uint32_t* es_ = es + e_cur * ecap - e0;
+                    const float* ew_ = ew + e_cur * ecap - e0;
+                    for (; k + 4 <= ke; k += 4) {
+                        uint32_t u[4];
+                        float wv[4], v[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            u[j] = es_[k + j];
+                            wv[j] = ew_[k + j];
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            bad |= u[j] >= a.idb;
+                            v[j] = u[j] < a.idb ? rd(u[j]) : 0.0f;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) sum = __fadd_rn(sum, __fmul_rn(wv[j], v[j]));
+                    }
+                    for (; k < ke; ++k) {
+                        const uint32_t u = es_[k];
+                        bad |= u >= a.idb;
+                        sum = __fadd_rn(sum, __fmul_rn(ew_[k], u < a.idb ? rd(u) : 0.0f));
+                    }
+                } else {
+                    for (; k < ke; ++k) {
+                        const uint32_t u = __ldg(src + k);
+                        bad |= u >= a.idb;
+                        sum = __fadd_rn(sum, __fmul_rn(__ldg(w + k), u < a.idb ? rd(u) : 0.0f));
+                    }
+                }
+                const float y = sigmoid32(sum);
+                if (id < a.idb) op[id] = y;
+                else bad = 1;
+            }
+        }
+        if constexpr (kGrid) {
+            const uint32_t to = i1.l < a.L ? i1.l : a.L;
+            for (uint32_t l = i0.l; l < to; ++l) layer_sync();
+        }
+        cpa_wait_1();  // everything issued before this item; this item's copies fly on
+        __syncthreads();
+        i0 = i1;
+        i1 = i2;
+        i2 = i3;
+        i3 = i4;
+    }
+    cpa_wait_all();
+    __syncthreads();
+    for (uint32_t i = gt; i < a.idb; i += nthr) a.out[i] = kGrid ? __ldcg(op + i) : op[i];
+    if (bad) *reinterpret_cast<volatile uint32_t*>(a.err) = 1u;
+}
+
 uint32_t align16(uint64_t b) { return static_cast<uint32_t>((b + 15) & ~15ull); }
 
 }  // namespace
@@ -304,15 +505,23 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
 
     const uint32_t op_bytes = align16(4ull * idb);
     const uint32_t blob = b->off.bytes;
-    // mode: 0 = zero-copy into shared, 1 = DMA + shared state, 2 = DMA + grid
+    // mode: 0 = zero-copy into shared memory, 1 = DMA + one CTA (state in
+    // shared memory, pipelined), 2 = DMA + cooperative grid (state in L2,
+    // pipelined); 3 / 4 = 1 / 2 without the cp.async rings (experiments)
+    uint32_t t1sh = 6;  // one-CTA item width: a power of two in [64, 512] covering the widest layer
+    while (t1sh < 9 && (1u << t1sh) < max_w) ++t1sh;
+    const uint32_t T1 = 1u << t1sh;
+    const uint32_t ring1 = pipe_ring_bytes(T1, d.total_layers);
+    const uint32_t fit1 = kSmemCap - 1024 > op_bytes + ring1 ? (kSmemCap - 1024 - op_bytes - ring1) / 24 : 0;
     uint32_t mode;
     if (op_bytes + static_cast<uint64_t>(blob) <= kSmemCap - 1024 && blob <= (96u << 10)) mode = 0;
-    else if (op_bytes <= kSmemCap - 1024 && d.edge_count <= (192u << 10)) mode = 1;
-    else mode = 2;
+    else if (fit1 >= 1024 && d.edge_count <= (256u << 10)) mode = 1;
+    else mode = d.total_layers <= 32 ? 2 : 4;  // deep: grid-wide syncs bind, the rings do not pay
     if (const char* m = getenv("ASNN_ONCE_MODE")) {
         const int f = atoi(m);
-        if (f == 1 && op_bytes <= kSmemCap - 1024) mode = 1;
-        if (f == 2) mode = 2;
+        if ((f == 1 && fit1 >= 256) || f == 2) mode = static_cast<uint32_t>(f);
+        if (f == 3 && op_bytes <= kSmemCap - 1024) mode = 3;
+        if (f == 4) mode = 4;
     }
     b->last_mode = mode;
 
@@ -340,7 +549,7 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
         CK(cudaMemcpyAsync(b->dblob, b->blob.p, blob, cudaMemcpyHostToDevice, st));
         a.blob = b->dblob;
     }
-    if (mode == 2) {
+    if (mode == 2 || mode == 4) {
         if (b->op_n < idb) {
             if (b->op) cudaFree(b->op);
             b->op = nullptr;
@@ -349,15 +558,29 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
             b->op_n = idb;
         }
         a.op = b->op;
-        constexpr int kT = 256;
+        constexpr uint32_t kT = 256, kEcap = 4096;
+        const void* fn = mode == 2 ? reinterpret_cast<const void*>(k_once_pipe<true>)
+                                   : reinterpret_cast<const void*>(k_once<2>);
+        const uint32_t smem = mode == 2 ? pipe_ring_bytes(kT, d.total_layers) + 3 * kEcap * 8 : 0;
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_once<2>, kT, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kT, smem));
         if (per_sm < 1) return fail(dev, ASNN_E_CUDA, "cooperative kernel does not fit");
         const uint32_t cap = static_cast<uint32_t>(per_sm) * static_cast<uint32_t>(dev->sm_count);
-        const uint32_t want = std::max<uint32_t>((max_w + kT - 1) / kT, (idb + 8 * kT - 1) / (8 * kT));
+        const uint32_t want = mode == 2 ? (max_w + kT - 1) / kT
+                                        : std::max<uint32_t>((max_w + kT - 1) / kT, (idb + 8 * kT - 1) / (8 * kT));
         const uint32_t blocks = std::max<uint32_t>(1, std::min(cap, want));
-        void* args[] = {&a};
-        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_once<2>), blocks, kT, args, 0, st));
+        uint32_t ecap = kEcap, tsh = 8;
+        void* args2[] = {&a, &ecap, &tsh};
+        void* args4[] = {&a};
+        CK(cudaLaunchCooperativeKernel(fn, blocks, kT, mode == 2 ? args2 : args4, smem, st));
+    } else if (mode == 1) {
+        const uint32_t ecap = std::min<uint32_t>(fit1, 1u << 16);
+        const uint32_t smem = op_bytes + ring1 + ecap * 24;
+        if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_once_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        k_once_pipe<false><<<1, T1, smem, st>>>(a, ecap, t1sh);
+        CK(cudaGetLastError());
     } else {
         const uint32_t smem = op_bytes + (mode == 0 ? blob : 0);
         const uint32_t T = std::min<uint32_t>(1024, std::max<uint32_t>(128, (max_w + 31) / 32 * 32));
@@ -369,7 +592,15 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     CK(cudaStreamSynchronize(st));
     if (*reinterpret_cast<volatile uint32_t*>(b->err_h))
         return fail(dev, ASNN_E_INVALID, "malformed layout: node id, predecessor id or row_ptr out of range");
-    if (!direct) std::memcpy(state_outputs, b->out_h, 4ull * idb);
+    if (!direct) {
+        // state back into the caller's (pageable) array, all host threads for large states
+        const int64_t nb = (static_cast<int64_t>(idb) + 16383) / 16384;
+#pragma omp parallel for schedule(static) if (nb > 4)
+        for (int64_t i = 0; i < nb; ++i) {
+            const uint64_t o = static_cast<uint64_t>(i) * 16384;
+            std::memcpy(state_outputs + o, b->out_h + o, 4ull * std::min<uint64_t>(16384, idb - o));
+        }
+    }
     return ASNN_OK;
 }
 

@@ -17,7 +17,7 @@ from test_gpu_activate import to_layout
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["auto", "1", "2"], ids=["auto", "dma-cta", "dma-grid"])
+@pytest.fixture(params=["auto", "1", "2", "3", "4"], ids=["auto", "dma-cta", "dma-grid", "cta-plain", "grid-plain"])
 def once_mode(request):
     old = os.environ.get("ASNN_ONCE_MODE")
     if request.param == "auto":

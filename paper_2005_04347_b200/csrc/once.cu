@@ -154,10 +154,11 @@ __global__ void __launch_bounds__(1024) k_once(const OnceArgs a) {
 // ---- pipelined sweep (modes 1 and 2) ---------------------------------------
 // The layers are cut into items of T consecutive nodes (one node per thread).
 // A CTA walks its items (mode 1: all of them; mode 2: chunk k of layer l goes
-// to CTA k mod G) with a five-slot ring of row_ptr / id slices and a
-// three-slot ring of edge slices in shared memory, filled by cp.async: while
-// item t is summed, item t+2's edges and item t+4's row_ptr / ids are in
-// flight (one cp.async group per item, waited one item behind), so the dependent
+// to CTA k mod G) with a seven-slot ring of row_ptr / id slices and a
+// four-slot ring of edge slices in shared memory, filled by cp.async: while
+// item t is summed, items t+1..t+3's edges and t+1..t+6's row_ptr / ids are in
+// flight (one cp.async group per item, waited two items behind; the staged
+// layout is first prefetched into L2), so the dependent
 // chain of an item touches shared memory only (and the state: shared in mode
 // 1, L2 in mode 2).  Items whose edges exceed a slot read them from global
 // memory instead.  The layer table sits in shared memory when it fits.
@@ -168,16 +169,19 @@ __device__ __forceinline__ void cpa4(void* d, const void* s) {
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void cpa_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_2() { asm volatile("cp.async.wait_group 2;" ::: "memory"); }
 
 struct Item {
     uint32_t l, k;  // layer, chunk within the layer; l >= L: none
 };
 
 constexpr uint32_t kLoSmem = 4096;  // layer-table entries kept in shared memory
+// prefetch distances (items): edges kDE ahead, row_ptr / ids kDM ahead; an
+// item's copies must land within kDE - 1 items (cp.async.wait_group kDE - 1)
+constexpr uint32_t kDE = 3, kDM = kDE + 3, kES = kDE + 1, kMS = kDM + 1;
 
 __host__ __device__ constexpr uint32_t pipe_ring_bytes(uint32_t T, uint32_t L) {
-    return 4 * (5 * (T + 1) + 5 * T + 2) + 4 * ((L + 1 <= kLoSmem ? L + 1 : 0) + 3) / 4 * 4;
+    return 4 * (kMS * (T + 1) + kMS * T + 1) + 4 * ((L + 1 <= kLoSmem ? L + 1 : 0) + 3) / 4 * 4;
 }
 
 template <bool kGrid>
@@ -187,12 +191,12 @@ __global__ void __launch_bounds__(512) k_once_pipe(const OnceArgs a, uint32_t ec
     const uint32_t G = kGrid ? gridDim.x : 1u, c = kGrid ? blockIdx.x : 0u;
     const uint32_t op_bytes = kGrid ? 0u : (a.idb * 4 + 15) & ~15u;
     float* op = kGrid ? a.op : reinterpret_cast<float*>(smem);
-    uint32_t* rp_s = reinterpret_cast<uint32_t*>(smem + op_bytes);  // [5][T + 1]
-    uint32_t* id_s = rp_s + 5 * (T + 1);                              // [5][T]
-    uint32_t* lo_s = id_s + 5 * T + 2;                                // [L + 1] when it fits
+    uint32_t* rp_s = reinterpret_cast<uint32_t*>(smem + op_bytes);  // [kMS][T + 1]
+    uint32_t* id_s = rp_s + kMS * (T + 1);                            // [kMS][T]
+    uint32_t* lo_s = id_s + kMS * T + 1;                              // [L + 1] when it fits
     const bool lo_in_smem = a.L + 1 <= kLoSmem;
-    uint32_t* es = lo_s + (lo_in_smem ? (a.L + 1 + 3) / 4 * 4 : 0);   // [3][ecap] sources
-    float* ew = reinterpret_cast<float*>(es + 3 * ecap);              // [3][ecap] weights
+    uint32_t* es = lo_s + (lo_in_smem ? (a.L + 1 + 3) / 4 * 4 : 0);   // [kES][ecap] sources
+    float* ew = reinterpret_cast<float*>(es + kES * ecap);            // [kES][ecap] weights
     const uint32_t* lo_g = reinterpret_cast<const uint32_t*>(a.blob + a.off.lo);
     const uint32_t* ids = reinterpret_cast<const uint32_t*>(a.blob + a.off.ids);
     const uint32_t* rp = reinterpret_cast<const uint32_t*>(a.blob + a.off.rp);
@@ -200,6 +204,11 @@ __global__ void __launch_bounds__(512) k_once_pipe(const OnceArgs a, uint32_t ec
     const float* w = reinterpret_cast<const float*>(a.blob + a.off.w);
     const float* sx = reinterpret_cast<const float*>(a.blob + a.off.sx);
     const uint32_t gt = c * T + t, nthr = G * T;
+    // the staged layout into L2 first (one DMA put it in HBM): the rings'
+    // copies then wait on L2, not DRAM
+    for (uint32_t o = gt * 16384u; o < a.off.bytes; o += nthr * 16384u)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.blob + o), "r"(min(16384u, a.off.bytes - o))
+                     : "memory");
     if (lo_in_smem)
         for (uint32_t i = t; i <= a.L; i += T) lo_s[i] = __ldg(lo_g + i);
     __syncthreads();
@@ -252,15 +261,15 @@ __global__ void __launch_bounds__(512) k_once_pipe(const OnceArgs a, uint32_t ec
         else return op[u];
     };
 
-    // items t .. t+4 of this CTA
+    // items t .. t+kDM of this CTA
     Item i0 = norm(Item{1, c});
-    Item i1 = next(i0);
-    Item i2 = next(i1);
-    Item i3 = next(i2);
+    Item i1 = next(i0), i2 = next(i1), i3 = next(i2), i4 = next(i3), i5 = next(i4);
     meta(i0, 0);
     meta(i1, 1);
     meta(i2, 2);
     meta(i3, 3);
+    meta(i4, 4);
+    meta(i5, 5);
     cpa_commit();
     for (uint32_t i = gt; i < a.idb; i += nthr) op[i] = 0.0f;  // make_state: outputs zero
     layer_sync();
@@ -275,17 +284,19 @@ __global__ void __launch_bounds__(512) k_once_pipe(const OnceArgs a, uint32_t ec
     layer_sync();
     edges(i0, 0, 0);
     edges(i1, 1, 1);
+    edges(i2, 2, 2);
     cpa_commit();
     // layers with no item of this CTA before its first one
     if constexpr (kGrid)
         for (uint32_t l = 1; l < min(i0.l, a.L); ++l) layer_sync();
     cpa_wait_all();
     __syncthreads();
-    // ring slots of item t: s0 (row_ptr / ids, of 5) and e_cur (edges, of 3)
-    for (uint32_t s0 = 0, e_cur = 0; i0.l < a.L; s0 = s0 == 4 ? 0 : s0 + 1, e_cur = e_cur == 2 ? 0 : e_cur + 1) {
-        const Item i4 = next(i3);
-        meta(i4, s0 == 0 ? 4 : s0 - 1);
-        edges(i2, s0 >= 3 ? s0 - 3 : s0 + 2, e_cur == 0 ? 2 : e_cur - 1);
+    // ring slots of item t: s0 (row_ptr / ids, of kMS = 7) and e_cur (edges, of kES = 4)
+    for (uint32_t s0 = 0, e_cur = 0; i0.l < a.L;
+         s0 = s0 == kMS - 1 ? 0 : s0 + 1, e_cur = e_cur == kES - 1 ? 0 : e_cur + 1) {
+        const Item i6 = next(i5);
+        meta(i6, s0 == 0 ? kMS - 1 : s0 - 1);                                  // (t + 6) mod 7
+        edges(i3, s0 + 3 >= kMS ? s0 + 3 - kMS : s0 + 3, e_cur == 0 ? kES - 1 : e_cur - 1);  // t + 3
         cpa_commit();
         {
             uint32_t b, n, e0, m;
@@ -339,12 +350,14 @@ __global__ void __launch_bounds__(512) k_once_pipe(const OnceArgs a, uint32_t ec
             const uint32_t to = i1.l < a.L ? i1.l : a.L;
             for (uint32_t l = i0.l; l < to; ++l) layer_sync();
         }
-        cpa_wait_1();  // everything issued before this item; this item's copies fly on
+        cpa_wait_2();  // copies issued two items ago and earlier; the last two items' fly on
         __syncthreads();
         i0 = i1;
         i1 = i2;
         i2 = i3;
         i3 = i4;
+        i4 = i5;
+        i5 = i6;
     }
     cpa_wait_all();
     __syncthreads();
@@ -512,7 +525,7 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     while (t1sh < 9 && (1u << t1sh) < max_w) ++t1sh;
     const uint32_t T1 = 1u << t1sh;
     const uint32_t ring1 = pipe_ring_bytes(T1, d.total_layers);
-    const uint32_t fit1 = kSmemCap - 1024 > op_bytes + ring1 ? (kSmemCap - 1024 - op_bytes - ring1) / 24 : 0;
+    const uint32_t fit1 = kSmemCap - 1024 > op_bytes + ring1 ? (kSmemCap - 1024 - op_bytes - ring1) / (8 * kES) : 0;
     uint32_t mode;
     if (op_bytes + static_cast<uint64_t>(blob) <= kSmemCap - 1024 && blob <= (96u << 10)) mode = 0;
     else if (fit1 >= 1024 && d.edge_count <= (256u << 10)) mode = 1;
@@ -558,10 +571,10 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
             b->op_n = idb;
         }
         a.op = b->op;
-        constexpr uint32_t kT = 256, kEcap = 4096;
+        constexpr uint32_t kT = 256, kEcap = 2048;
         const void* fn = mode == 2 ? reinterpret_cast<const void*>(k_once_pipe<true>)
                                    : reinterpret_cast<const void*>(k_once<2>);
-        const uint32_t smem = mode == 2 ? pipe_ring_bytes(kT, d.total_layers) + 3 * kEcap * 8 : 0;
+        const uint32_t smem = mode == 2 ? pipe_ring_bytes(kT, d.total_layers) + kES * kEcap * 8 : 0;
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kT, smem));
@@ -576,7 +589,7 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
         CK(cudaLaunchCooperativeKernel(fn, blocks, kT, mode == 2 ? args2 : args4, smem, st));
     } else if (mode == 1) {
         const uint32_t ecap = std::min<uint32_t>(fit1, 1u << 16);
-        const uint32_t smem = op_bytes + ring1 + ecap * 24;
+        const uint32_t smem = op_bytes + ring1 + ecap * 8 * kES;
         if (smem > 48 * 1024)
             CK(cudaFuncSetAttribute(k_once_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         k_once_pipe<false><<<1, T1, smem, st>>>(a, ecap, t1sh);

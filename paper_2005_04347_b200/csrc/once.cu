@@ -12,6 +12,10 @@
 //   -> [small]  one kernel: one CTA pulls the staged layout over PCIe into
 //               shared memory (zero-copy, every load in flight at once) and
 //               sweeps the layers there, __syncthreads between layers
+//   -> [medium, shallow] an 8-CTA cluster pulls its shares of the staged
+//               layout over PCIe into distributed shared memory, every CTA
+//               keeping a copy of the state (DSMEM stores + a cluster barrier
+//               per layer)
 //   -> [medium] one DMA, then one CTA with the state in shared memory
 //   -> [large]  one DMA, then one cooperative grid with the state in L2,
 //               grid.sync() between layers
@@ -365,6 +369,119 @@ __global__ void __launch_bounds__(512) k_once_pipe(const OnceArgs a, uint32_t ec
     if (bad) *reinterpret_cast<volatile uint32_t*>(a.err) = 1u;
 }
 
+// ---- mode 5: a cluster of CTAs holding the layout in distributed shared memory
+// Each of the kC CTAs of one thread-block cluster owns a contiguous 1/kC of
+// every layer's nodes.  At start every CTA pulls its share of the staged
+// layout (ids, row_ptr, predecessor ids / weights, sensor inputs) straight
+// from page-locked host memory into its own shared memory (cp.async, no DMA
+// operation); it keeps a full copy of the id-indexed state.  Per layer each
+// CTA sums its nodes from shared memory and stores every result into all kC
+// copies of the state (st.shared::cluster through DSMEM), then one cluster
+// barrier.  The host plans the shares: per (CTA, layer) {first node, nodes,
+// first edge, edges, node offset, edge offset} in shared memory.
+constexpr uint32_t kC = 8;
+
+struct PlanEnt {
+    uint32_t a, n, ea, m, noff, eoff, pad0, pad1;
+};
+
+__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(256) k_once_cluster(const OnceArgs a, const PlanEnt* plan,
+                                                                                 uint32_t n_loc, uint32_t e_loc) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    cg::cluster_group cl = cg::this_cluster();
+    const uint32_t r = cl.block_rank(), t = threadIdx.x, T = blockDim.x;
+    const uint32_t op_bytes = (a.idb * 4 + 15) & ~15u;
+    float* op = reinterpret_cast<float*>(smem);
+    PlanEnt* pl = reinterpret_cast<PlanEnt*>(smem + op_bytes);             // [L]
+    uint32_t* lid = reinterpret_cast<uint32_t*>(pl + a.L);                  // [n_loc]
+    uint32_t* lrp = lid + n_loc;                                            // [n_loc + L]
+    uint32_t* les = lrp + n_loc + a.L;                                      // [e_loc]
+    float* lew = reinterpret_cast<float*>(les + e_loc);                     // [e_loc]
+    float* lsx = lew + e_loc;                                               // [layer-0 share]
+    const uint32_t* ids = reinterpret_cast<const uint32_t*>(a.blob + a.off.ids);
+    const uint32_t* rp = reinterpret_cast<const uint32_t*>(a.blob + a.off.rp);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.blob + a.off.src);
+    const float* w = reinterpret_cast<const float*>(a.blob + a.off.w);
+    const float* sx = reinterpret_cast<const float*>(a.blob + a.off.sx);
+
+    for (uint32_t i = t; i < a.L * 8; i += T)
+        cpa4(reinterpret_cast<uint32_t*>(pl) + i, reinterpret_cast<const uint32_t*>(plan + static_cast<size_t>(r) * a.L) + i);
+    cpa_commit();
+    for (uint32_t i = t; i < a.idb; i += T) op[i] = 0.0f;  // make_state: outputs zero
+    cpa_wait_all();
+    __syncthreads();
+    // this CTA's share of the layout, over PCIe into shared memory
+    for (uint32_t l = 0; l < a.L; ++l) {
+        const PlanEnt e = pl[l];
+        for (uint32_t j = t; j < e.n; j += T) {
+            cpa4(lid + e.noff + j, ids + e.a + j);
+            if (l == 0) cpa4(lsx + j, sx + e.a + j);
+        }
+        if (l > 0) {
+            for (uint32_t j = t; j <= e.n; j += T) cpa4(lrp + e.noff + l + j, rp + e.a + j);
+            for (uint32_t j = t; j < e.m; j += T) {
+                cpa4(les + e.eoff + j, src + e.ea + j);
+                cpa4(lew + e.eoff + j, w + e.ea + j);
+            }
+        }
+    }
+    cpa_commit();
+    cpa_wait_all();
+    cl.sync();  // every copy of the state zeroed before any remote store
+    uint32_t bad = 0;
+    for (uint32_t l = 0; l < a.L; ++l) {
+        const PlanEnt e = pl[l];
+        for (uint32_t j = t; j < e.n; j += T) {
+            const uint32_t id = lid[e.noff + j];
+            float y;
+            if (l == 0) {
+                y = sigmoid32(lsx[j]);  // eval.cpp:17
+            } else {
+                uint32_t k = lrp[e.noff + l + j], ke = lrp[e.noff + l + j + 1];
+                if (ke < k || k < e.ea || ke > e.ea + e.m) {
+                    bad = 1;
+                    ke = k = e.ea;
+                }
+                const uint32_t* s_ = les + e.eoff - e.ea;
+                const float* w_ = lew + e.eoff - e.ea;
+                float sum = 0.0f;
+                for (; k + 4 <= ke; k += 4) {
+                    uint32_t u[4];
+                    float wv[4], v[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        u[q] = s_[k + q];
+                        wv[q] = w_[k + q];
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        bad |= u[q] >= a.idb;
+                        v[q] = u[q] < a.idb ? op[u[q]] : 0.0f;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) sum = __fadd_rn(sum, __fmul_rn(wv[q], v[q]));
+                }
+                for (; k < ke; ++k) {
+                    const uint32_t u = s_[k];
+                    bad |= u >= a.idb;
+                    sum = __fadd_rn(sum, __fmul_rn(w_[k], u < a.idb ? op[u] : 0.0f));
+                }
+                y = sigmoid32(sum);
+            }
+            if (id < a.idb) {
+#pragma unroll
+                for (uint32_t q = 0; q < kC; ++q) cl.map_shared_rank(op, q)[id] = y;
+            } else {
+                bad = 1;
+            }
+        }
+        cl.sync();
+    }
+    const uint32_t per = (a.idb + kC - 1) / kC, b0 = r * per, b1 = min(a.idb, b0 + per);
+    for (uint32_t i = b0 + t; i < b1; i += T) a.out[i] = op[i];
+    if (bad) *reinterpret_cast<volatile uint32_t*>(a.err) = 1u;
+}
+
 uint32_t align16(uint64_t b) { return static_cast<uint32_t>((b + 15) & ~15ull); }
 
 }  // namespace
@@ -375,6 +492,7 @@ struct asnn_eval_buf {
     OnceOff off{};
     bool staged = false;
     PinnedBuf blob;            // page-locked (mapped) staging of the layout
+    PinnedBuf plan;            // mode 5: per (CTA, layer) shares (mapped)
     uint8_t* dblob = nullptr;  // device copy (modes 1, 2)
     size_t dblob_bytes = 0;
     float* op = nullptr;       // global state (mode 2)
@@ -526,8 +644,47 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     const uint32_t T1 = 1u << t1sh;
     const uint32_t ring1 = pipe_ring_bytes(T1, d.total_layers);
     const uint32_t fit1 = kSmemCap - 1024 > op_bytes + ring1 ? (kSmemCap - 1024 - op_bytes - ring1) / (8 * kES) : 0;
+    // mode 5 plan: each CTA of the cluster takes a contiguous 1/kC of every
+    // layer; feasible when every share plus a full state fits shared memory
+    uint32_t n_max = 0, e_max = 0, s_max = 0, smem5 = 0;
+    bool fit5 = false;
+    const uint64_t plan_bytes = static_cast<uint64_t>(kC) * d.total_layers * sizeof(PlanEnt);
+    if (d.total_layers && plan_bytes <= (64u << 10) && op_bytes + d.total_layers * sizeof(PlanEnt) < kSmemCap) {
+        CK(b->plan.ensure(plan_bytes));
+        PlanEnt* pe = static_cast<PlanEnt*>(b->plan.p);
+        bool ok = true;
+        for (uint32_t r = 0; r < kC && ok; ++r) {
+            uint32_t noff = 0, eoff = 0;
+            for (uint32_t l = 0; l < d.total_layers; ++l) {
+                const uint32_t wl = lo[l + 1] - lo[l], ch = (wl + kC - 1) / kC;
+                const uint32_t a0 = std::min(wl, r * ch), a1 = std::min(wl, (r + 1) * ch);
+                PlanEnt& e = pe[static_cast<size_t>(r) * d.total_layers + l];
+                e = PlanEnt{lo[l] + a0, a1 - a0, 0, 0, noff, eoff, 0, 0};
+                if (l > 0) {
+                    e.ea = rp[e.a];
+                    const uint32_t eb = rp[e.a + e.n];
+                    if (eb < e.ea || eb > d.edge_count) {
+                        ok = false;  // malformed row_ptr: the other variants report it
+                        break;
+                    }
+                    e.m = eb - e.ea;
+                } else {
+                    s_max = std::max(s_max, e.n);
+                }
+                noff += e.n;
+                eoff += e.m;
+            }
+            n_max = std::max(n_max, noff);
+            e_max = std::max(e_max, eoff);
+        }
+        const uint64_t need = op_bytes + d.total_layers * sizeof(PlanEnt) + 4ull * n_max +
+                              4ull * (n_max + d.total_layers) + 8ull * e_max + 4ull * s_max;
+        fit5 = ok && need <= kSmemCap - 1024;
+        smem5 = static_cast<uint32_t>(need);
+    }
     uint32_t mode;
     if (op_bytes + static_cast<uint64_t>(blob) <= kSmemCap - 1024 && blob <= (96u << 10)) mode = 0;
+    else if (fit5 && d.total_layers <= 24) mode = 5;  // ~1 us per cluster barrier: shallow layouts
     else if (fit1 >= 1024 && d.edge_count <= (256u << 10)) mode = 1;
     else mode = d.total_layers <= 32 ? 2 : 4;  // deep: grid-wide syncs bind, the rings do not pay
     if (const char* m = getenv("ASNN_ONCE_MODE")) {
@@ -535,6 +692,7 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
         if ((f == 1 && fit1 >= 256) || f == 2) mode = static_cast<uint32_t>(f);
         if (f == 3 && op_bytes <= kSmemCap - 1024) mode = 3;
         if (f == 4) mode = 4;
+        if (f == 5 && fit5) mode = 5;
     }
     b->last_mode = mode;
 
@@ -547,7 +705,7 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     a.idb = idb;
     a.ns = d.sensor_count;
     a.E = static_cast<uint32_t>(d.edge_count);
-    if (mode == 0) {
+    if (mode == 0 || mode == 5) {
         void* hb = nullptr;
         CK(cudaHostGetDevicePointer(&hb, b->blob.p, 0));
         a.blob = static_cast<const uint8_t*>(hb);
@@ -587,6 +745,13 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
         void* args2[] = {&a, &ecap, &tsh};
         void* args4[] = {&a};
         CK(cudaLaunchCooperativeKernel(fn, blocks, kT, mode == 2 ? args2 : args4, smem, st));
+    } else if (mode == 5) {
+        void* pd = nullptr;
+        CK(cudaHostGetDevicePointer(&pd, b->plan.p, 0));
+        if (smem5 > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_once_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem5));
+        k_once_cluster<<<kC, 256, smem5, st>>>(a, static_cast<const PlanEnt*>(pd), n_max, e_max);
+        CK(cudaGetLastError());
     } else if (mode == 1) {
         const uint32_t ecap = std::min<uint32_t>(fit1, 1u << 16);
         const uint32_t smem = op_bytes + ring1 + ecap * 8 * kES;

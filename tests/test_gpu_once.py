@@ -17,7 +17,7 @@ from test_gpu_activate import to_layout
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["auto", "1", "2", "3", "4"], ids=["auto", "dma-cta", "dma-grid", "cta-plain", "grid-plain"])
+@pytest.fixture(params=["auto", "1", "2", "3", "4", "5"], ids=["auto", "dma-cta", "dma-grid", "cta-plain", "grid-plain", "cluster"])
 def once_mode(request):
     old = os.environ.get("ASNN_ONCE_MODE")
     if request.param == "auto":
@@ -82,7 +82,7 @@ def test_variant_selection(oracle):
     os.environ.pop("ASNN_ONCE_MODE", None)
     buf = A.EvalBuffer()
     try:
-        for c, want in [(1000, 0), (10000, 0), (100000, 1), (1000000, 2)]:
+        for c, want in [(1000, 0), (10000, 0), (100000, 5), (1000000, 2)]:
             spec = A.corpus_spec(c, 10, 8, 2, 7 + c)
             d = oracle.layout(A.generate(spec))
             lay = to_layout(d)

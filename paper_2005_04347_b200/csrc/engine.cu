@@ -1229,6 +1229,11 @@ bool rows_win_ok(const asnn_dev_layout* L, uint32_t l, uint32_t ldA) {
 // k_rows_tma (tma_rows.cuh): the TMA-gather level kernel for ldA a multiple
 // of 128; ASNN_LEVEL_VARIANT=13 selects it (experiments).
 bool tma_rows_enabled(uint32_t ldA) { return level_variant() == 13 && ldA >= 128 && ldA % 128 == 0; }
+// K-rows-bulk (bulk_rows.cuh): 14 = 16 edges per stage, 15 = 8, 16 = 24
+bool bulk_rows_enabled(uint32_t ldA) {
+    const int v = level_variant();
+    return v >= 14 && v <= 16 && ldA % bulkrows::kTile == 0;
+}
 
 int ensure_tmap_A(asnn_dev_layout* L, uint32_t ldA) {
     if (L->tmA_base == L->A.p && L->tmA_ld == ldA) return ASNN_OK;
@@ -1337,6 +1342,32 @@ int launch_levels(asnn_dev_layout* L, uint32_t ldA, cudaStream_t st, Mark& mark)
                 CK(cudaLaunchKernelEx(&cfg, k_rows_win, static_cast<const uint2*>(L->edges.p), L->A.p, ldA,
                                       static_cast<const uint4*>(L->rtask.p + L->lvl_off[l]), nrows, L->win_lo[l],
                                       L->win_hi[l] - L->win_lo[l] + 1, (L->max_deg + 1) & ~1u));
+            } else if (ll.rows && bulk_rows_enabled(ldA)) {
+                const int v = level_variant();
+                auto fn = v == 15 ? k_rows_bulk<8> : v == 16 ? k_rows_bulk<24> : k_rows_bulk<16>;
+                const uint32_t smem = v == 15   ? bulkrows::smem_bytes<8>()
+                                      : v == 16 ? bulkrows::smem_bytes<24>()
+                                                : bulkrows::smem_bytes<16>();
+                static bool attr_set = false;
+                if (!attr_set) {
+                    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                    attr_set = true;
+                }
+                const uint32_t tiles = ldA / bulkrows::kTile;
+                cudaLaunchConfig_t cfg{};
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.gridDim = dim3(static_cast<uint32_t>(static_cast<uint64_t>(nrows + ns) * tiles));
+                cfg.blockDim = dim3(bulkrows::kThreads);
+                cfg.dynamicSmemBytes = smem;
+                cfg.stream = st;
+                cfg.attrs = attr;
+                cfg.numAttrs = pdl_enabled() && !fork && !prev_join && l > 1 ? 1 : 0;
+                CK(cudaLaunchKernelEx(&cfg, fn, static_cast<const uint2*>(L->edges.p), L->A.p, ldA,
+                                      static_cast<const uint4*>(L->rtask.p + L->lvl_off[l] + nh), nrows, tiles,
+                                      static_cast<const uint4*>(segs ? L->seg.p + L->seg_short_off[l] : nullptr), ns,
+                                      L->accbuf.p));
             } else if (ll.rows && tma_rows_enabled(ldA)) {
                 RC_(ensure_tmap_A(L, ldA));
                 static bool attr_set = false;

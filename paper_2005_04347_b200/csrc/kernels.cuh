@@ -587,6 +587,7 @@ k_heavy(const uint32_t* __restrict__ row_ptr, const uint2* __restrict__ edges, f
 #include "chain.cuh"
 #include "serve.cuh"
 #include "tma_rows.cuh"
+#include "bulk_rows.cuh"
 #include "win_rows.cuh"
 #include "segments.cuh"
 

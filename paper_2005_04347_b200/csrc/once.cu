@@ -32,7 +32,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "engine.hpp"
@@ -484,6 +486,38 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(256) k_once_cluster
 
 uint32_t align16(uint64_t b) { return static_cast<uint32_t>((b + 15) & ~15ull); }
 
+// cudaFuncSetAttribute once per (kernel, device, size growth): the per-call
+// path pays no attribute calls after the first of each size class
+cudaError_t set_smem(const void* fn, int device, uint32_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, int>, uint32_t>> set;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : set)
+        if (e.first.first == fn && e.first.second == device) {
+            if (e.second >= bytes) return cudaSuccess;
+            const cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+            if (r == cudaSuccess) e.second = bytes;
+            return r;
+        }
+    const cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (r == cudaSuccess) set.push_back({{fn, device}, bytes});
+    return r;
+}
+
+// device address of page-locked host memory, cached per allocation
+template <class T>
+cudaError_t mapped(const void* h, const void*& h_cached, T*& d_cached) {
+    if (h == h_cached && d_cached) return cudaSuccess;
+    void* d = nullptr;
+    const cudaError_t r = cudaHostGetDevicePointer(&d, const_cast<void*>(h), 0);
+    if (r == cudaSuccess) {
+        h_cached = h;
+        d_cached = static_cast<T*>(d);
+    }
+    return r;
+}
+
 }  // namespace
 
 struct asnn_eval_buf {
@@ -501,6 +535,12 @@ struct asnn_eval_buf {
     size_t out_n = 0;
     uint32_t* err_h = nullptr;
     uint32_t last_mode = 0;
+    // device addresses of the mapped buffers (cached per allocation)
+    const void *blob_h = nullptr, *plan_h = nullptr, *out_hc = nullptr, *err_hc = nullptr;
+    const uint8_t* blob_d = nullptr;
+    const void* plan_d = nullptr;
+    float* out_d = nullptr;
+    uint32_t* err_d = nullptr;
     ~asnn_eval_buf() {
         if (dblob) cudaFree(dblob);
         if (op) cudaFree(op);
@@ -629,9 +669,12 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
         cudaGetLastError();
     }
     const bool direct = out_dev != nullptr;
-    if (!direct) CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&out_dev), b->out_h, 0));
-    uint32_t* err_dev = nullptr;
-    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&err_dev), b->err_h, 0));
+    if (!direct) {
+        CK(mapped(b->out_h, b->out_hc, b->out_d));
+        out_dev = b->out_d;
+    }
+    CK(mapped(b->err_h, b->err_hc, b->err_d));
+    uint32_t* err_dev = b->err_d;
     *reinterpret_cast<volatile uint32_t*>(b->err_h) = 0;
 
     const uint32_t op_bytes = align16(4ull * idb);
@@ -706,9 +749,8 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     a.ns = d.sensor_count;
     a.E = static_cast<uint32_t>(d.edge_count);
     if (mode == 0 || mode == 5) {
-        void* hb = nullptr;
-        CK(cudaHostGetDevicePointer(&hb, b->blob.p, 0));
-        a.blob = static_cast<const uint8_t*>(hb);
+        CK(mapped(b->blob.p, b->blob_h, b->blob_d));
+        a.blob = b->blob_d;
     } else {
         if (b->dblob_bytes < blob) {
             if (b->dblob) cudaFree(b->dblob);
@@ -733,7 +775,7 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
         const void* fn = mode == 2 ? reinterpret_cast<const void*>(k_once_pipe<true>)
                                    : reinterpret_cast<const void*>(k_once<2>);
         const uint32_t smem = mode == 2 ? pipe_ring_bytes(kT, d.total_layers) + kES * kEcap * 8 : 0;
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(set_smem(fn, dev->device, smem));
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kT, smem));
         if (per_sm < 1) return fail(dev, ASNN_E_CUDA, "cooperative kernel does not fit");
@@ -746,24 +788,21 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
         void* args4[] = {&a};
         CK(cudaLaunchCooperativeKernel(fn, blocks, kT, mode == 2 ? args2 : args4, smem, st));
     } else if (mode == 5) {
-        void* pd = nullptr;
-        CK(cudaHostGetDevicePointer(&pd, b->plan.p, 0));
-        if (smem5 > 48 * 1024)
-            CK(cudaFuncSetAttribute(k_once_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem5));
-        k_once_cluster<<<kC, 256, smem5, st>>>(a, static_cast<const PlanEnt*>(pd), n_max, e_max);
+        CK(mapped(b->plan.p, b->plan_h, b->plan_d));
+        CK(set_smem(reinterpret_cast<const void*>(k_once_cluster), dev->device, smem5));
+        k_once_cluster<<<kC, 256, smem5, st>>>(a, static_cast<const PlanEnt*>(b->plan_d), n_max, e_max);
         CK(cudaGetLastError());
     } else if (mode == 1) {
         const uint32_t ecap = std::min<uint32_t>(fit1, 1u << 16);
         const uint32_t smem = op_bytes + ring1 + ecap * 8 * kES;
-        if (smem > 48 * 1024)
-            CK(cudaFuncSetAttribute(k_once_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(set_smem(reinterpret_cast<const void*>(k_once_pipe<false>), dev->device, smem));
         k_once_pipe<false><<<1, T1, smem, st>>>(a, ecap, t1sh);
         CK(cudaGetLastError());
     } else {
         const uint32_t smem = op_bytes + (mode == 0 ? blob : 0);
         const uint32_t T = std::min<uint32_t>(1024, std::max<uint32_t>(128, (max_w + 31) / 32 * 32));
         auto fn = mode == 0 ? k_once<0> : k_once<1>;
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(set_smem(reinterpret_cast<const void*>(fn), dev->device, smem));
         fn<<<1, T, smem, st>>>(a);
         CK(cudaGetLastError());
     }

@@ -6,7 +6,7 @@
 //   compute_required    network.cpp:222-255      -> asnn_dev_compute_required
 //   segment             segmentation.cpp:20-101  -> asnn_dev_segment
 //   flatten             layout.cpp:12-83         -> asnn_dev_build_layout + download
-//   eval_parallel       eval.cpp:49-80           -> asnn_dev_upload_layout + asnn_dev_activate
+//   eval_parallel       eval.cpp:49-80           -> asnn_eval_buf_stage + asnn_eval_buf_run (one call)
 //   read_outputs, layer_slice_bounds, max_layer_width, depth, unassigned_outputs
 //   parse_network       io.cpp:83-156 + validate -> asnn_dev_parse_network
 //   read_network        io.cpp:167-173           -> asnn_dev_read_network
@@ -493,8 +493,9 @@ inline std::uint32_t max_layer_width(const LayeredLayout& layout) {
     return w;
 }
 
-// eval.cpp:49-80 with Backend::DeviceCompute: upload (every call), activate,
-// id-indexed state back.
+// eval.cpp:49-80 with Backend::DeviceCompute: the layout is staged straight
+// into a per-thread page-locked buffer and evaluated by one kernel on the
+// id-indexed state (asnn_eval_buf, once.cu); nothing stays on the device.
 inline ActivationState eval_parallel(const LayeredLayout& layout, std::span<const float> input_values,
                                      const ParallelConfig& cfg = {}) {
     if (cfg.backend != ParallelConfig::Backend::DeviceCompute)
@@ -504,37 +505,42 @@ inline ActivationState eval_parallel(const LayeredLayout& layout, std::span<cons
         throw InputArityMismatch("expected " + std::to_string(layout.input_order.size()) +
                                  " input values, got " + std::to_string(input_values.size()));
     asnn_dev* dev = detail::device();
-    std::vector<std::uint32_t> ids(layout.nodes.size());
-    std::vector<std::uint64_t> rp(layout.nodes.size() + 1, 0);
-    std::vector<std::uint32_t> in;
-    std::vector<float> w;
-    for (std::size_t k = 0; k < layout.nodes.size(); ++k) {
-        ids[k] = layout.nodes[k].id;
-        in.insert(in.end(), layout.nodes[k].in_nodes.begin(), layout.nodes[k].in_nodes.end());
-        w.insert(w.end(), layout.nodes[k].in_weights.begin(), layout.nodes[k].in_weights.end());
-        rp[k + 1] = in.size();
-    }
-    asnn_layout_desc d{};
-    d.total_layers = layout.total_layers;
-    d.layer_offsets = layout.layer_offsets.data();
-    d.node_count = static_cast<std::uint32_t>(layout.nodes.size());
-    d.node_ids = ids.data();
-    d.row_ptr = rp.data();
-    d.in_nodes = in.data();
-    d.in_weights = w.data();
-    d.n_inputs = static_cast<std::uint32_t>(layout.input_order.size());
-    d.input_order = layout.input_order.data();
-    d.id_bound = layout.id_bound;
-    asnn_dev_layout* h = nullptr;
-    detail::check(asnn_dev_upload_layout(dev, &d, &h), dev);
-    ActivationState st;
+    struct Buf {
+        asnn_eval_buf* b = nullptr;
+        ~Buf() { asnn_eval_buf_free(b); }
+    };
+    thread_local Buf buf;
+    if (!buf.b) detail::check(asnn_eval_buf_create(dev, &buf.b), dev);
+    ActivationState st;  // make_state (eval.cpp:29-33)
     st.inputs.assign(layout.id_bound, 0.0f);
     for (std::size_t i = 0; i < input_values.size(); ++i) st.inputs[layout.input_order[i]] = input_values[i];
-    st.outputs.assign(layout.id_bound, 0.0f);
-    const int rc = asnn_dev_activate(h, input_values.data(), 1, input_values.size(), nullptr,
-                                     st.outputs.data());
-    asnn_dev_free_layout(h);
-    detail::check(rc, dev);
+    std::uint64_t edges = 0;
+    for (const FlatNode& n : layout.nodes) edges += n.in_nodes.size();
+    asnn_eval_dims dims{};
+    dims.total_layers = layout.total_layers;
+    dims.node_count = static_cast<std::uint32_t>(layout.nodes.size());
+    dims.sensor_count = layout.total_layers ? layout.nodes_per_layer[0] : 0;
+    dims.id_bound = layout.id_bound;
+    dims.edge_count = edges;
+    asnn_eval_stage s{};
+    detail::check(asnn_eval_buf_stage(buf.b, &dims, &s), dev);
+    std::copy(layout.layer_offsets.begin(), layout.layer_offsets.end(), s.layer_offsets);
+    std::uint32_t at = 0;
+    for (std::size_t k = 0; k < layout.nodes.size(); ++k) {
+        const FlatNode& n = layout.nodes[k];
+        s.node_ids[k] = n.id;
+        s.row_ptr[k] = at;
+        std::copy(n.in_nodes.begin(), n.in_nodes.end(), s.in_nodes + at);
+        std::copy(n.in_weights.begin(), n.in_weights.end(), s.in_weights + at);
+        at += static_cast<std::uint32_t>(n.in_nodes.size());
+    }
+    s.row_ptr[layout.nodes.size()] = at;
+    for (std::uint32_t k = 0; k < dims.sensor_count; ++k) {
+        const NodeId id = layout.nodes[k].id;
+        s.sensor_inputs[k] = id < layout.id_bound ? st.inputs[id] : 0.0f;
+    }
+    st.outputs.resize(layout.id_bound);
+    detail::check(asnn_eval_buf_run(buf.b, st.outputs.data()), dev);
     return st;
 }
 

@@ -652,7 +652,10 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     CK(cudaSetDevice(dev->device));
     cudaStream_t st = dev->stream;
     const uint32_t idb = d.id_bound;
-    if (idb == 0) return ASNN_OK;
+    if (idb == 0) {
+        if (d.node_count) return fail(dev, ASNN_E_INVALID, "malformed layout: nodes with id_bound 0");
+        return ASNN_OK;
+    }
     if (b->out_n < idb) {
         if (b->out_h) cudaFreeHost(b->out_h);
         b->out_h = nullptr;
@@ -692,7 +695,11 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     uint32_t n_max = 0, e_max = 0, s_max = 0, smem5 = 0;
     bool fit5 = false;
     const uint64_t plan_bytes = static_cast<uint64_t>(kC) * d.total_layers * sizeof(PlanEnt);
-    if (d.total_layers && plan_bytes <= (64u << 10) && op_bytes + d.total_layers * sizeof(PlanEnt) < kSmemCap) {
+    const bool fit0 = op_bytes + static_cast<uint64_t>(blob) <= kSmemCap - 1024 && blob <= (96u << 10);
+    const char* force = getenv("ASNN_ONCE_MODE");
+    const int forced = force ? atoi(force) : -1;
+    if ((!fit0 || forced == 5) && d.total_layers && plan_bytes <= (64u << 10) &&
+        op_bytes + d.total_layers * sizeof(PlanEnt) < kSmemCap) {
         CK(b->plan.ensure(plan_bytes));
         PlanEnt* pe = static_cast<PlanEnt*>(b->plan.p);
         bool ok = true;
@@ -726,12 +733,12 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
         smem5 = static_cast<uint32_t>(need);
     }
     uint32_t mode;
-    if (op_bytes + static_cast<uint64_t>(blob) <= kSmemCap - 1024 && blob <= (96u << 10)) mode = 0;
+    if (fit0) mode = 0;
     else if (fit5 && d.total_layers <= 24) mode = 5;  // ~1 us per cluster barrier: shallow layouts
     else if (fit1 >= 1024 && d.edge_count <= (256u << 10)) mode = 1;
     else mode = d.total_layers <= 32 ? 2 : 4;  // deep: grid-wide syncs bind, the rings do not pay
-    if (const char* m = getenv("ASNN_ONCE_MODE")) {
-        const int f = atoi(m);
+    if (forced >= 0) {
+        const int f = forced;
         if ((f == 1 && fit1 >= 256) || f == 2) mode = static_cast<uint32_t>(f);
         if (f == 3 && op_bytes <= kSmemCap - 1024) mode = 3;
         if (f == 4) mode = 4;

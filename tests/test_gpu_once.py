@@ -167,6 +167,9 @@ def test_arity_and_malformed_layouts(oracle):
     bad.layer_offsets[-1] -= 1
     with pytest.raises(ValueError):
         A.eval_once(bad, np.zeros(2, np.float32))
+    # nodes but an empty state
+    with pytest.raises(ValueError, match="malformed"):
+        A.eval_once(A.LayeredLayout(1, [0, 1], [0], [0, 0], [], [], [], 0, 0), np.zeros(0, np.float32))
     # the handle still works afterwards
     x = np.array([0.5, -0.5], np.float32)
     assert np.array_equal(bits(A.eval_once(lay, x)), bits(oracle.eval_batch(d, x[None, :])[0]))

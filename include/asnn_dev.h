@@ -224,7 +224,9 @@ int asnn_eval_buf_stage(asnn_eval_buf* buf, const asnn_eval_dims* dims, asnn_eva
 int asnn_eval_buf_run(asnn_eval_buf* buf, float* state_outputs);
 /* kernel variant of the last run: 0 zero-copy into shared memory, 1 DMA +
  * one CTA, 2 DMA + cooperative grid, both with cp.async rings of the next
- * items' slices; 3 / 4 the same without the rings (ASNN_ONCE_MODE forces) */
+ * items' slices; 3 / 4 the same without the rings; 5 / 6 an 8-CTA cluster
+ * holding the layout in distributed shared memory (per-layer shares / layer
+ * ranges) (ASNN_ONCE_MODE forces) */
 int asnn_eval_buf_mode(const asnn_eval_buf* buf, uint32_t* mode);
 /* The same from a layout descriptor and one input vector (make_state on the
  * host; ASNN_E_ARITY when n_x != n_inputs, eval.cpp:26-28). */

@@ -387,8 +387,14 @@ struct PlanEnt {
     uint32_t a, n, ea, m, noff, eoff, pad0, pad1;
 };
 
+struct LayerRanges {
+    uint32_t b[kC + 1];  // mode 6: CTA r owns layers [b[r], b[r+1]); b[0] == kNoRanges: mode 5
+};
+constexpr uint32_t kNoRanges = 0xFFFFFFFFu;
+
 __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(256) k_once_cluster(const OnceArgs a, const PlanEnt* plan,
-                                                                                 uint32_t n_loc, uint32_t e_loc) {
+                                                                                 uint32_t n_loc, uint32_t e_loc,
+                                                                                 const LayerRanges rg) {
     extern __shared__ __align__(16) uint8_t smem[];
     cg::cluster_group cl = cg::this_cluster();
     const uint32_t r = cl.block_rank(), t = threadIdx.x, T = blockDim.x;
@@ -431,7 +437,8 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(256) k_once_cluster
     cpa_wait_all();
     cl.sync();  // every copy of the state zeroed before any remote store
     uint32_t bad = 0;
-    for (uint32_t l = 0; l < a.L; ++l) {
+    // this CTA's nodes of layer l; every result goes into all kC copies
+    auto layer = [&](uint32_t l, bool bcast) {
         const PlanEnt e = pl[l];
         for (uint32_t j = t; j < e.n; j += T) {
             const uint32_t id = lid[e.noff + j];
@@ -471,13 +478,33 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(256) k_once_cluster
                 y = sigmoid32(sum);
             }
             if (id < a.idb) {
+                op[id] = y;
+                if (bcast)
 #pragma unroll
-                for (uint32_t q = 0; q < kC; ++q) cl.map_shared_rank(op, q)[id] = y;
+                    for (uint32_t q = 1; q < kC; ++q) cl.map_shared_rank(op, (r + q) % kC)[id] = y;
             } else {
                 bad = 1;
             }
         }
-        cl.sync();
+    };
+    if (rg.b[0] == kNoRanges) {
+        // mode 5: every CTA takes 1/kC of every layer, one cluster barrier per layer
+        for (uint32_t l = 0; l < a.L; ++l) {
+            layer(l, true);
+            cl.sync();
+        }
+    } else {
+        // mode 6: CTA r runs its own contiguous range of layers (__syncthreads
+        // between them, every result also stored into the other copies as it
+        // is made); one cluster barrier per range hands the state on
+        for (uint32_t q = 0; q < kC; ++q) {
+            if (q == r)
+                for (uint32_t l = rg.b[r]; l < rg.b[r + 1]; ++l) {
+                    layer(l, true);
+                    __syncthreads();
+                }
+            cl.sync();
+        }
     }
     const uint32_t per = (a.idb + kC - 1) / kC, b0 = r * per, b1 = min(a.idb, b0 + per);
     for (uint32_t i = b0 + t; i < b1; i += T) a.out[i] = op[i];
@@ -690,31 +717,71 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     const uint32_t T1 = 1u << t1sh;
     const uint32_t ring1 = pipe_ring_bytes(T1, d.total_layers);
     const uint32_t fit1 = kSmemCap - 1024 > op_bytes + ring1 ? (kSmemCap - 1024 - op_bytes - ring1) / (8 * kES) : 0;
-    // mode 5 plan: each CTA of the cluster takes a contiguous 1/kC of every
-    // layer; feasible when every share plus a full state fits shared memory
+    // cluster plans.  Mode 5: each CTA takes a contiguous 1/kC of every layer
+    // (one cluster barrier per layer: shallow layouts).  Mode 6: each CTA
+    // takes a contiguous range of layers, split by bytes (one barrier per
+    // range: deep layouts).  Feasible when every share plus a full state fits
+    // shared memory.
     uint32_t n_max = 0, e_max = 0, s_max = 0, smem5 = 0;
     bool fit5 = false;
+    LayerRanges rg{};
+    rg.b[0] = kNoRanges;
     const uint64_t plan_bytes = static_cast<uint64_t>(kC) * d.total_layers * sizeof(PlanEnt);
     const bool fit0 = op_bytes + static_cast<uint64_t>(blob) <= kSmemCap - 1024 && blob <= (96u << 10);
     const char* force = getenv("ASNN_ONCE_MODE");
     const int forced = force ? atoi(force) : -1;
-    if ((!fit0 || forced == 5) && d.total_layers && plan_bytes <= (64u << 10) &&
+    const bool ranges = forced == 6 || (forced != 5 && d.total_layers > 24);
+    if ((!fit0 || forced == 5 || forced == 6) && d.total_layers && plan_bytes <= (64u << 10) &&
         op_bytes + d.total_layers * sizeof(PlanEnt) < kSmemCap) {
         CK(b->plan.ensure(plan_bytes));
         PlanEnt* pe = static_cast<PlanEnt*>(b->plan.p);
         bool ok = true;
+        for (uint32_t l = 1; l < d.total_layers && ok; ++l)
+            ok = rp[lo[l + 1]] >= rp[lo[l]] && rp[lo[l + 1]] <= d.edge_count;  // else the other variants report it
+        if (ok && ranges) {
+            // layers [rg.b[r], rg.b[r+1]) to CTA r: close a range once it holds
+            // 1/kC of the bytes (ids, row_ptr, edges)
+            auto cost = [&](uint32_t l) -> uint64_t {
+                const uint64_t n = lo[l + 1] - lo[l];
+                return 8 * n + 4 + (l ? 8ull * (rp[lo[l + 1]] - rp[lo[l]]) : 4 * n);
+            };
+            uint64_t total = 0;
+            for (uint32_t l = 0; l < d.total_layers; ++l) total += cost(l);
+            const uint64_t target = (total + kC - 1) / kC;
+            uint32_t r = 0;
+            uint64_t cur = 0;
+            rg.b[0] = 0;
+            for (uint32_t l = 0; l < d.total_layers; ++l) {
+                const uint64_t c = cost(l);
+                if (cur > 0 && cur + c > target && r + 1 < kC) {
+                    rg.b[++r] = l;
+                    cur = 0;
+                }
+                cur += c;
+            }
+            for (uint32_t q = r + 1; q <= kC; ++q) rg.b[q] = d.total_layers;
+        }
         for (uint32_t r = 0; r < kC && ok; ++r) {
             uint32_t noff = 0, eoff = 0;
             for (uint32_t l = 0; l < d.total_layers; ++l) {
-                const uint32_t wl = lo[l + 1] - lo[l], ch = (wl + kC - 1) / kC;
-                const uint32_t a0 = std::min(wl, r * ch), a1 = std::min(wl, (r + 1) * ch);
+                const uint32_t wl = lo[l + 1] - lo[l];
+                uint32_t a0, a1;
+                if (ranges) {
+                    const bool mine = l >= rg.b[r] && l < rg.b[r + 1];
+                    a0 = 0;
+                    a1 = mine ? wl : 0;
+                } else {
+                    const uint32_t ch = (wl + kC - 1) / kC;
+                    a0 = std::min(wl, r * ch);
+                    a1 = std::min(wl, (r + 1) * ch);
+                }
                 PlanEnt& e = pe[static_cast<size_t>(r) * d.total_layers + l];
                 e = PlanEnt{lo[l] + a0, a1 - a0, 0, 0, noff, eoff, 0, 0};
                 if (l > 0) {
                     e.ea = rp[e.a];
                     const uint32_t eb = rp[e.a + e.n];
                     if (eb < e.ea || eb > d.edge_count) {
-                        ok = false;  // malformed row_ptr: the other variants report it
+                        ok = false;
                         break;
                     }
                     e.m = eb - e.ea;
@@ -734,7 +801,7 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     }
     uint32_t mode;
     if (fit0) mode = 0;
-    else if (fit5 && d.total_layers <= 24) mode = 5;  // ~1 us per cluster barrier: shallow layouts
+    else if (fit5) mode = ranges ? 6 : 5;
     else if (fit1 >= 1024 && d.edge_count <= (256u << 10)) mode = 1;
     else mode = d.total_layers <= 32 ? 2 : 4;  // deep: grid-wide syncs bind, the rings do not pay
     if (forced >= 0) {
@@ -742,7 +809,7 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
         if ((f == 1 && fit1 >= 256) || f == 2) mode = static_cast<uint32_t>(f);
         if (f == 3 && op_bytes <= kSmemCap - 1024) mode = 3;
         if (f == 4) mode = 4;
-        if (f == 5 && fit5) mode = 5;
+        if ((f == 5 || f == 6) && fit5) mode = static_cast<uint32_t>(f);
     }
     b->last_mode = mode;
 
@@ -755,7 +822,7 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     a.idb = idb;
     a.ns = d.sensor_count;
     a.E = static_cast<uint32_t>(d.edge_count);
-    if (mode == 0 || mode == 5) {
+    if (mode == 0 || mode == 5 || mode == 6) {
         CK(mapped(b->blob.p, b->blob_h, b->blob_d));
         a.blob = b->blob_d;
     } else {
@@ -794,10 +861,10 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
         void* args2[] = {&a, &ecap, &tsh};
         void* args4[] = {&a};
         CK(cudaLaunchCooperativeKernel(fn, blocks, kT, mode == 2 ? args2 : args4, smem, st));
-    } else if (mode == 5) {
+    } else if (mode == 5 || mode == 6) {
         CK(mapped(b->plan.p, b->plan_h, b->plan_d));
         CK(set_smem(reinterpret_cast<const void*>(k_once_cluster), dev->device, smem5));
-        k_once_cluster<<<kC, 256, smem5, st>>>(a, static_cast<const PlanEnt*>(b->plan_d), n_max, e_max);
+        k_once_cluster<<<kC, 256, smem5, st>>>(a, static_cast<const PlanEnt*>(b->plan_d), n_max, e_max, rg);
         CK(cudaGetLastError());
     } else if (mode == 1) {
         const uint32_t ecap = std::min<uint32_t>(fit1, 1u << 16);

@@ -17,7 +17,8 @@ from test_gpu_activate import to_layout
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["auto", "1", "2", "3", "4", "5"], ids=["auto", "dma-cta", "dma-grid", "cta-plain", "grid-plain", "cluster"])
+@pytest.fixture(params=["auto", "1", "2", "3", "4", "5", "6"],
+                ids=["auto", "dma-cta", "dma-grid", "cta-plain", "grid-plain", "cluster", "cluster-ranges"])
 def once_mode(request):
     old = os.environ.get("ASNN_ONCE_MODE")
     if request.param == "auto":
@@ -82,8 +83,8 @@ def test_variant_selection(oracle):
     os.environ.pop("ASNN_ONCE_MODE", None)
     buf = A.EvalBuffer()
     try:
-        for c, want in [(1000, 0), (10000, 0), (100000, 5), (1000000, 2)]:
-            spec = A.corpus_spec(c, 10, 8, 2, 7 + c)
+        for c, dpt, want in [(1000, 10, 0), (10000, 10, 0), (100000, 10, 5), (1000000, 10, 2), (100000, 100, 6)]:
+            spec = A.corpus_spec(c, dpt, 8, 2, 7 + c)
             d = oracle.layout(A.generate(spec))
             lay = to_layout(d)
             x = np.linspace(-1, 1, len(lay.input_order)).astype(np.float32)

@@ -36,7 +36,7 @@ def main():
                                 lay["dropped_connections"], lay["id_bound"])
             x = np.full(len(L.input_order), 0.5, np.float32)
             row = [f"c{c}_d{d}"]
-            for m in ("auto", "1", "5", "2", "4"):
+            for m in ("auto", "1", "5", "6", "2", "4"):
                 if m == "auto":
                     os.environ.pop("ASNN_ONCE_MODE", None)
                 else:

@@ -81,7 +81,12 @@ __global__ void __launch_bounds__(1024) k_once(const OnceArgs a) {
         // zero-copy pull of the staged layout: independent 16-byte loads
         const uint4* s = reinterpret_cast<const uint4*>(a.blob);
         uint4* d = reinterpret_cast<uint4*>(smem + op_bytes);
-        for (uint32_t i = threadIdx.x; i < a.off.bytes / 16; i += blockDim.x) d[i] = s[i];
+        for (uint32_t i = threadIdx.x; i < a.off.bytes / 16; i += blockDim.x)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(d + i))),
+                         "l"(s + i)
+                         : "memory");
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
         base = smem + op_bytes;
     }
     constexpr bool ro = kMode != 0;
@@ -727,7 +732,10 @@ int asnn_eval_buf_run(asnn_eval_buf* b, float* state_outputs) {
     LayerRanges rg{};
     rg.b[0] = kNoRanges;
     const uint64_t plan_bytes = static_cast<uint64_t>(kC) * d.total_layers * sizeof(PlanEnt);
-    const bool fit0 = op_bytes + static_cast<uint64_t>(blob) <= kSmemCap - 1024 && blob <= (96u << 10);
+    // one CTA pulls the whole layout: small layouts, and deep ones that fit
+    // (its per-layer step is the cheapest; wide shallow ones pull faster with 8 CTAs)
+    const bool fit0 = op_bytes + static_cast<uint64_t>(blob) <= kSmemCap - 1024 &&
+                      (blob <= (96u << 10) || d.total_layers > 24);
     const char* force = getenv("ASNN_ONCE_MODE");
     const int forced = force ? atoi(force) : -1;
     const bool ranges = forced == 6 || (forced != 5 && d.total_layers > 24);

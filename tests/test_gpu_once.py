@@ -83,7 +83,8 @@ def test_variant_selection(oracle):
     os.environ.pop("ASNN_ONCE_MODE", None)
     buf = A.EvalBuffer()
     try:
-        for c, dpt, want in [(1000, 10, 0), (10000, 10, 0), (100000, 10, 5), (1000000, 10, 2), (100000, 100, 6)]:
+        for c, dpt, want in [(1000, 10, 0), (10000, 10, 0), (100000, 10, 5), (1000000, 10, 2), (100000, 100, 6),
+                             (20000, 100, 0)]:
             spec = A.corpus_spec(c, dpt, 8, 2, 7 + c)
             d = oracle.layout(A.generate(spec))
             lay = to_layout(d)

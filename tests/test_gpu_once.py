@@ -184,3 +184,41 @@ def test_empty_and_sensor_only():
     assert bits(out)[1] == 1  # sigmoid32(-200) = 0x1p-149, no flush to zero
     lay = A.LayeredLayout(0, [0], [], [0], [], [], [], 0, 0)
     assert A.eval_once(lay, np.zeros(0, np.float32)).size == 0
+
+
+def test_concurrent_callers(oracle):
+    """SPEC.md:331-332 on the one-call path: threads on one device handle, each
+    with its own staging buffer (EvalBuffer) or the handle's (eval_once)."""
+    import threading
+    cases = []
+    for i in range(6):
+        spec = A.corpus_spec(2000 * (i + 1), 5 + 7 * i, 8, 2, 900 + i)
+        d = oracle.layout(A.generate(spec))
+        lay = to_layout(d)
+        x = np.linspace(-1, 1, len(lay.input_order)).astype(np.float32) * (i + 1)
+        cases.append((lay, x, oracle.eval_batch(d, x[None, :])[0]))
+    errors = []
+
+    def worker(k):
+        try:
+            buf = A.EvalBuffer() if k % 2 else None
+            for r in range(20):
+                lay, x, ref = cases[(k + r) % len(cases)]
+                if buf is None:
+                    out = A.eval_once(lay, x)
+                else:
+                    buf.stage_layout(lay, x)
+                    out = buf.run()
+                if not np.array_equal(bits(out), bits(ref)):
+                    errors.append((k, r))
+            if buf is not None:
+                buf.free()
+        except Exception as e:  # noqa: BLE001
+            errors.append((k, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(6)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors

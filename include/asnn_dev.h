@@ -9,7 +9,9 @@
  *   flatten          (layout.cpp:12-83)         -> asnn_dev_build_layout (+ _download)
  *   eval_parallel, Backend::DeviceCompute
  *                    (eval.hpp:20,37-39; the seam at eval.cpp:51-52)
- *                                               -> asnn_dev_upload_layout + asnn_dev_activate
+ *                                               -> per call: asnn_eval_buf_stage + _run
+ *                                                  (or asnn_dev_eval_layout); resident:
+ *                                                  asnn_dev_upload_layout + asnn_dev_activate
  *   read_outputs     (eval.cpp:82-87)           -> `out` argument of asnn_dev_activate
  *   layer_slice_bounds / max_layer_width / depth
  *                    (layout.cpp:85-91, eval.cpp:89-94, segmentation.cpp:103-105)

@@ -9,16 +9,20 @@
 // the reference's own id-indexed state and runs the whole call as
 //
 //   caller writes the CSR straight into page-locked staging (asnn_eval_buf_stage)
-//   -> [small]  one kernel: one CTA pulls the staged layout over PCIe into
-//               shared memory (zero-copy, every load in flight at once) and
+//   -> mode 0 [small, or deep and fitting one SM]: one CTA pulls the staged
+//               layout over PCIe into shared memory (zero-copy cp.async) and
 //               sweeps the layers there, __syncthreads between layers
-//   -> [medium, shallow] an 8-CTA cluster pulls its shares of the staged
-//               layout over PCIe into distributed shared memory, every CTA
-//               keeping a copy of the state (DSMEM stores + a cluster barrier
-//               per layer)
-//   -> [medium] one DMA, then one CTA with the state in shared memory
-//   -> [large]  one DMA, then one cooperative grid with the state in L2,
-//               grid.sync() between layers
+//   -> mode 5 [medium, <= 24 layers] / mode 6 [medium, deeper]: an 8-CTA
+//               cluster pulls its shares of the staged layout over PCIe into
+//               distributed shared memory, every CTA keeping a copy of the
+//               state (DSMEM stores); shares of every layer and a cluster
+//               barrier per layer (5), or ranges of whole layers and a
+//               barrier per range (6)
+//   -> mode 1 [state fits one SM]: one DMA, then one CTA with the state in
+//               shared memory and cp.async rings of the next items
+//   -> mode 2 / 4 [large, shallow / deep]: one DMA, then one cooperative grid
+//               with the state in L2, grid.sync() between layers (with / without
+//               the rings); mode 3 = mode 1 without the rings (experiments)
 //   -> state.outputs written by the kernel into mapped host memory.
 //
 // Arithmetic is activate_node (eval.cpp:16-23): the stored predecessor order,

@@ -326,28 +326,50 @@ __global__ void __launch_bounds__(512) k_once_pipe(const OnceArgs a, uint32_t ec
                 }
                 float sum = 0.0f;
                 if (st) {
+                    // state in L2 (mode 2): batches of 8 predicated loads, so a
+                    // row's gathers cost one dependent L2 read per 8
+                    // predecessors, the partial batch included (no add for the
+                    // masked slots); mode 1 only runs its tail through it
                     const uint32_t* es_ = es + e_cur * ecap - e0;
                     const float* ew_ = ew + e_cur * ecap - e0;
-                    for (; k + 4 <= ke; k += 4) {
-                        uint32_t u[4];
-                        float wv[4], v[4];
+                    constexpr int U = 8;
+                    if constexpr (!kGrid) {
+                        // state in shared memory: plain batches of 4 and a scalar tail
+                        for (; k + 4 <= ke; k += 4) {
+                            uint32_t u[4];
+                            float wv[4], v[4];
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            u[j] = es_[k + j];
-                            wv[j] = ew_[k + j];
+                            for (int j = 0; j < 4; ++j) {
+                                u[j] = es_[k + j];
+                                wv[j] = ew_[k + j];
+                            }
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                bad |= u[j] >= a.idb;
+                                v[j] = u[j] < a.idb ? rd(u[j]) : 0.0f;
+                            }
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) sum = __fadd_rn(sum, __fmul_rn(wv[j], v[j]));
                         }
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            bad |= u[j] >= a.idb;
-                            v[j] = u[j] < a.idb ? rd(u[j]) : 0.0f;
-                        }
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) sum = __fadd_rn(sum, __fmul_rn(wv[j], v[j]));
                     }
-                    for (; k < ke; ++k) {
-                        const uint32_t u = es_[k];
-                        bad |= u >= a.idb;
-                        sum = __fadd_rn(sum, __fmul_rn(ew_[k], u < a.idb ? rd(u) : 0.0f));
+                    for (; k < ke; k += U) {
+                        uint32_t u[U];
+                        float wv[U], v[U];
+#pragma unroll
+                        for (int j = 0; j < U; ++j) {
+                            const bool in = k + j < ke;
+                            u[j] = in ? es_[k + j] : 0u;
+                            wv[j] = in ? ew_[k + j] : 0.0f;
+                        }
+#pragma unroll
+                        for (int j = 0; j < U; ++j) {
+                            const bool in = k + j < ke;
+                            bad |= in && u[j] >= a.idb;
+                            v[j] = in && u[j] < a.idb ? rd(u[j]) : 0.0f;
+                        }
+#pragma unroll
+                        for (int j = 0; j < U; ++j)
+                            if (k + j < ke) sum = __fadd_rn(sum, __fmul_rn(wv[j], v[j]));
                     }
                 } else {
                     for (; k < ke; ++k) {

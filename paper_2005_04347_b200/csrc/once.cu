@@ -133,6 +133,29 @@ __global__ void __launch_bounds__(1024) k_once(const OnceArgs a) {
                 ke = k;
             }
             float s = 0.0f;
+            if constexpr (kMode == 2) {
+                // state and edges in L2: predicated batches of 8, one dependent
+                // round of L2 reads per 8 predecessors, the tail included
+                for (; k < ke; k += 8) {
+                    uint32_t u[8];
+                    float wv[8], v[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const bool in = k + j < ke;
+                        u[j] = in ? __ldg(src + k + j) : 0u;
+                        wv[j] = in ? __ldg(w + k + j) : 0.0f;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const bool in = k + j < ke;
+                        bad |= in && u[j] >= a.idb;
+                        v[j] = in && u[j] < a.idb ? rd(u[j]) : 0.0f;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (k + j < ke) s = __fadd_rn(s, __fmul_rn(wv[j], v[j]));
+                }
+            }
             // predecessors in the stored order; four loads ahead of the chain
             for (; k + 4 <= ke; k += 4) {
                 uint32_t u[4];

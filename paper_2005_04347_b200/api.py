@@ -813,7 +813,9 @@ def eval_once(layout: LayeredLayout, x, device: int = 0) -> np.ndarray:
 
 class EvalBuffer:
     """asnn_eval_buf: page-locked staging the caller writes a layout into, then
-    one device call (once.cu).  `stage` returns numpy views of the staged arrays."""
+    one device call (once.cu).  `stage` returns numpy views of the staged arrays;
+    they stay valid until the next `stage` (which may reallocate) or `free`.
+    One buffer per thread."""
 
     def __init__(self, device: int = 0):
         self.dev = Device.get(device)

@@ -203,7 +203,9 @@ int asnn_dev_layout_download(asnn_dev_layout* layout, uint32_t net_index, uint32
  *                           writes state.outputs [id_bound] (unassigned ids
  *                           0.0f).  ASNN_E_INVALID for malformed layouts
  *                           (layer table, row_ptr or ids out of range).
- * One buffer per calling thread; runs on one handle serialise. */
+ * One buffer per calling thread; runs on one handle serialise.  The staged
+ * pointers stay valid until the buffer's next stage (which may reallocate)
+ * or free; a run may be repeated on the same staging. */
 typedef struct asnn_eval_buf asnn_eval_buf;
 typedef struct asnn_eval_dims {
     uint32_t total_layers;
